@@ -1,0 +1,150 @@
+/*
+ * purine_b200.h — C ABI of the B200 (sm_100a) kernel library for the Purine
+ * data-parallel SGD hot path.
+ *
+ * Every entry point replaces the arithmetic of one reference operator kind:
+ * the reference executes each kind through `OpKindSpec.execute` ->
+ * `_plain(fn)` -> a numpy kernel (pkg/src/biflow/ops.py:526-533, registry
+ * :750-809).  The Python host layer (paper_1412_6249_b200/gpu_ops.py) keeps
+ * that plugin interface and calls these functions through ctypes; the
+ * binding a maintainer would add to the reference itself is in
+ * INTEGRATION.md.
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers, element counts and dims; fp32 row-major NCHW /
+ *     KCRS exactly as the reference stores them (ops.py:1-10);
+ *   - `stream` is a cudaStream_t (passed as an opaque pointer);
+ *   - no allocation, no host synchronisation: work is only enqueued;
+ *     temporary storage comes from a caller-provided workspace;
+ *   - reentrant and callable from any host thread;
+ *   - return 0 on success, non-zero on failure with a message available
+ *     from bf_last_error() (thread-local).  The Python shim maps a failure
+ *     to KernelError (ops.py:48-49), which the dispatcher turns into
+ *     DispatchError (dispatcher.py:296-311).
+ *   - integer index outputs (max-pool argmax) are stored as exactly
+ *     representable float32 values, matching the reference's all-float32
+ *     tensor store (ops.py:79-157).
+ */
+#ifndef PURINE_B200_H
+#define PURINE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* bf_stream_t;
+
+/* library identity / errors --------------------------------------------- */
+int bf_version(void);
+const char* bf_last_error(void);
+/* number of SMs of `device` (grid sizing is done in multiples of it) */
+int bf_sm_count(int device);
+/* 1 if the library was compiled with the tcgen05 GEMM path */
+int bf_has_tcgen05(void);
+/* total kernels launched by this library so far (process-wide counter) */
+long long bf_launch_count(void);
+/* select the GEMM engine: 0 = auto (tcgen05 where supported), 1 = SIMT fp32 */
+int bf_set_gemm_engine(int engine);
+
+/* bind this library's CUDA runtime to `device` for the calling thread */
+int bf_set_device(int device);
+/* device-side injected latency on `stream` (reference delay_s / copy_latency_s,
+   dispatcher.py:289-294, ops.py:539-540) */
+int bf_delay_ns(int64_t ns, bf_stream_t stream);
+
+/* elementwise ------------------------------------------------------------ */
+/* relu_forward, ops.py:359-364 */
+int bf_relu_fwd(const float* x, float* y, int64_t n, bf_stream_t stream);
+/* relu_backward, ops.py:367-376 (dy where x > 0) */
+int bf_relu_bwd(const float* x, const float* dy, float* dx, int64_t n, bf_stream_t stream);
+/* sgd_update, ops.py:428-437: out = w - f32(lr)*g, product rounded first */
+int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t n,
+                  bf_stream_t stream);
+/* sgd_momentum (extension): v' = mu*v + lr*g; w' = w - v' */
+int bf_sgd_momentum(const float* w, const float* g, const float* v, float* w_new,
+                    float* v_new, float lr, float momentum, int64_t n, bf_stream_t stream);
+/* lowered aggregate(mean)+sgd_update (builders.py:589-603): out = w - f32(lr)*(gsum/f32(k)) */
+int bf_sgd_mean_update(const float* w, const float* gsum, float* out, float lr, int k,
+                       int64_t n, bf_stream_t stream);
+/* aggregate, ops.py:440-457: rank-ordered sum of k parts (k <= 32); mean divides by f32(k) */
+int bf_aggregate(const float* const* parts, int k, float* out, int64_t n, int mean,
+                 bf_stream_t stream);
+/* copy, ops.py:536-541: device-to-device (peer when devices differ) */
+int bf_copy(float* dst, int dst_device, const float* src, int src_device, int64_t n,
+            bf_stream_t stream);
+/* sets *flag (device int) to 1 if any element is non-finite (ops.py:61-64) */
+int bf_check_finite(const float* x, int64_t n, int* flag, bf_stream_t stream);
+
+/* softmax cross-entropy, ops.py:394-425 ---------------------------------- */
+/* workspace: >= n floats */
+int bf_softmax_xent(const float* logits, const float* labels, float* loss, float* dlogits,
+                    int n, int k, float* workspace, bf_stream_t stream);
+
+/* dense layer, ops.py:164-226 -------------------------------------------- */
+int bf_fc_fwd(const float* x, const float* w, const float* b, float* y, int n, int d, int m,
+              float* workspace, int64_t ws_bytes, bf_stream_t stream);
+int bf_fc_bwd_data(const float* w, const float* dy, float* dx, int n, int d, int m,
+                   float* workspace, int64_t ws_bytes, bf_stream_t stream);
+int bf_fc_bwd_weight(const float* x, const float* dy, float* dw, int n, int d, int m,
+                     float* workspace, int64_t ws_bytes, bf_stream_t stream);
+int bf_fc_bwd_bias(const float* dy, float* db, int n, int m, bf_stream_t stream);
+
+/* convolution, ops.py:229-352 (NCHW x, KCRS w; P,Q = output dims) -------- */
+int bf_conv2d_fwd(const float* x, const float* w, const float* b, float* y,
+                  int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                  int stride, int pad, float* workspace, int64_t ws_bytes, bf_stream_t stream);
+int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx,
+                       int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                       int stride, int pad, float* workspace, int64_t ws_bytes,
+                       bf_stream_t stream);
+int bf_conv2d_bwd_weight(const float* x, const float* dy, float* dw,
+                         int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                         int stride, int pad, float* workspace, int64_t ws_bytes,
+                         bf_stream_t stream);
+/* db[k] = sum over (n, p, q) of dy, deterministic order */
+int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, bf_stream_t stream);
+/* workspace bytes the conv/fc entry points want for this shape (0 = none) */
+int64_t bf_gemm_workspace_bytes(int op, int N, int C, int H, int W, int K, int R, int S,
+                                int P, int Q, int stride, int pad);
+
+/* pooling (extension; Caffe ceil-mode geometry) -------------------------- */
+int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, int W,
+                   int P, int Q, int kernel, int stride, int pad, bf_stream_t stream);
+int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, int H, int W,
+                   int P, int Q, int kernel, int stride, int pad, bf_stream_t stream);
+int bf_avgpool_fwd(const float* x, float* y, int N, int C, int H, int W, int P, int Q,
+                   int kernel, int stride, int pad, bf_stream_t stream);
+int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P, int Q,
+                   int kernel, int stride, int pad, bf_stream_t stream);
+
+/* local response normalisation across channels (extension; Caffe) ------- */
+int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int W, int size,
+               float alpha, float beta, float k, bf_stream_t stream);
+int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* dy, float* dx,
+               int N, int C, int H, int W, int size, float alpha, float beta, float k,
+               bf_stream_t stream);
+
+/* channel concat (extension); parts/channels are HOST arrays, k <= 32 ---- */
+int bf_concat_fwd(const float* const* parts, const int* channels, int k, float* y,
+                  int N, int H, int W, bf_stream_t stream);
+int bf_concat_bwd(const float* dy, float* const* parts, const int* channels, int k,
+                  int N, int H, int W, bf_stream_t stream);
+
+/* NCCL over NVLink for the lowered parameter exchange (exchange.py) ----- */
+int bf_nccl_unique_id(unsigned char out[128]);
+int bf_nccl_init(void** comm, int nranks, int rank, const unsigned char id[128]);
+int bf_nccl_destroy(void* comm);
+int bf_nccl_reduce_scatter(void* comm, const float* send, float* recv, int64_t recv_count,
+                           bf_stream_t stream);
+int bf_nccl_all_gather(void* comm, const float* send, float* recv, int64_t send_count,
+                       bf_stream_t stream);
+int bf_nccl_all_reduce(void* comm, const float* send, float* recv, int64_t count,
+                       bf_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PURINE_B200_H */

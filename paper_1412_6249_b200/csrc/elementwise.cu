@@ -1,0 +1,272 @@
+// Elementwise kernels: ReLU, SGD (plain / momentum / lowered mean), rank-ordered
+// aggregate, copy, non-finite check.  All HBM-bound: 128-bit vectorised,
+// grid-stride, grid sized in multiples of the SM count.  Rounding follows the
+// reference exactly (no FMA contraction: every product is rounded before the
+// add), so these kernels are bit-identical to the numpy reference.
+#include <stdarg.h>
+
+#include <atomic>
+
+#include "common.cuh"
+
+namespace bf {
+
+static thread_local char g_err[512];
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static std::atomic<long long> g_launches{0};
+
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int sm_count_current() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static int cached[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (cached[dev] == 0) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = v > 0 ? v : 148;
+  }
+  return cached[dev];
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// numpy maximum(x, 0): returns x when x >= 0 (keeps -0.0), else 0
+__device__ __forceinline__ float relu1(float x) { return x >= 0.f ? x : 0.f; }
+__device__ __forceinline__ float relu_g(float x, float g) { return x > 0.f ? g : 0.f; }
+__device__ __forceinline__ float sgd1(float w, float g, float lr) {
+  return __fsub_rn(w, __fmul_rn(lr, g));
+}
+
+__global__ void relu_fwd_v4(const float4* __restrict__ x, float4* __restrict__ y, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = x[i];
+    y[i] = make_float4(relu1(v.x), relu1(v.y), relu1(v.z), relu1(v.w));
+  }
+}
+
+__global__ void relu_fwd_s(const float* __restrict__ x, float* __restrict__ y, int64_t lo,
+                           int64_t n) {
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = relu1(x[i]);
+}
+
+__global__ void relu_bwd_v4(const float4* __restrict__ x, const float4* __restrict__ dy,
+                            float4* __restrict__ dx, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = x[i], g = dy[i];
+    dx[i] = make_float4(relu_g(a.x, g.x), relu_g(a.y, g.y), relu_g(a.z, g.z), relu_g(a.w, g.w));
+  }
+}
+
+__global__ void relu_bwd_s(const float* __restrict__ x, const float* __restrict__ dy,
+                           float* __restrict__ dx, int64_t lo, int64_t n) {
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dx[i] = relu_g(x[i], dy[i]);
+}
+
+__global__ void sgd_kernel(const float* __restrict__ w, const float* __restrict__ g,
+                           float* __restrict__ out, float lr, int64_t n) {
+  int64_t n4 = n >> 2;
+  const float4* w4 = reinterpret_cast<const float4*>(w);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 a = w4[i], b = g4[i];
+    o4[i] = make_float4(sgd1(a.x, b.x, lr), sgd1(a.y, b.y, lr), sgd1(a.z, b.z, lr),
+                        sgd1(a.w, b.w, lr));
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += stride)
+    out[i] = sgd1(w[i], g[i], lr);
+}
+
+__global__ void sgd_scalar(const float* __restrict__ w, const float* __restrict__ g,
+                           float* __restrict__ out, float lr, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = sgd1(w[i], g[i], lr);
+}
+
+__global__ void sgd_momentum_kernel(const float* __restrict__ w, const float* __restrict__ g,
+                                    const float* __restrict__ v, float* __restrict__ w_new,
+                                    float* __restrict__ v_new, float lr, float mu, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float vn = __fadd_rn(__fmul_rn(mu, v[i]), __fmul_rn(lr, g[i]));
+    v_new[i] = vn;
+    w_new[i] = __fsub_rn(w[i], vn);
+  }
+}
+
+__global__ void sgd_mean_kernel(const float* __restrict__ w, const float* __restrict__ gsum,
+                                float* __restrict__ out, float lr, float k, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __fsub_rn(w[i], __fmul_rn(lr, __fdiv_rn(gsum[i], k)));
+}
+
+struct Parts {
+  const float* p[32];
+};
+
+__global__ void aggregate_kernel(Parts parts, int k, float* __restrict__ out, int64_t n,
+                                 int mean) {
+  float fk = (float)k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = parts.p[0][i];
+    for (int j = 1; j < k; ++j) acc = __fadd_rn(acc, parts.p[j][i]);
+    if (mean) acc = __fdiv_rn(acc, fk);
+    out[i] = acc;
+  }
+}
+
+// device-side injected latency (the reference's delay_s / copy_latency_s,
+// dispatcher.py:289-294, ops.py:539-540): occupies the lane's stream
+__global__ void delay_kernel(int64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while ((int64_t)(t - t0) < ns);
+}
+
+__global__ void finite_kernel(const float* __restrict__ x, int64_t n, int* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+}
+
+}  // namespace
+}  // namespace bf
+
+using namespace bf;
+
+extern "C" {
+
+int bf_version(void) { return 1; }
+
+long long bf_launch_count(void) { return bf::g_launches.load(); }
+
+const char* bf_last_error(void) { return bf::g_err; }
+
+int bf_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+    set_error("bf_sm_count: cannot query device %d", device);
+    return -1;
+  }
+  return v;
+}
+
+int bf_set_device(int device) {
+  BF_CUDA(cudaSetDevice(device), "bf_set_device");
+  return 0;
+}
+
+int bf_delay_ns(int64_t ns, bf_stream_t s) {
+  if (ns <= 0) return 0;
+  delay_kernel<<<1, 1, 0, as_stream(s)>>>(ns);
+  return check_launch("delay");
+}
+
+int bf_relu_fwd(const float* x, float* y, int64_t n, bf_stream_t s) {
+  if (n <= 0) return 0;
+  cudaStream_t st = as_stream(s);
+  int64_t n4 = aligned16(x) && aligned16(y) ? n / 4 : 0;
+  if (n4) relu_fwd_v4<<<elementwise_grid(n4, kThreads), kThreads, 0, st>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y), n4);
+  if (n4 * 4 < n) relu_fwd_s<<<elementwise_grid(n - n4 * 4, kThreads), kThreads, 0, st>>>(
+      x, y, n4 * 4, n);
+  return check_launch("relu_forward", (n4 > 0) + (n4 * 4 < n));
+}
+
+int bf_relu_bwd(const float* x, const float* dy, float* dx, int64_t n, bf_stream_t s) {
+  if (n <= 0) return 0;
+  cudaStream_t st = as_stream(s);
+  int64_t n4 = aligned16(x) && aligned16(dy) && aligned16(dx) ? n / 4 : 0;
+  if (n4) relu_bwd_v4<<<elementwise_grid(n4, kThreads), kThreads, 0, st>>>(
+      reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy),
+      reinterpret_cast<float4*>(dx), n4);
+  if (n4 * 4 < n) relu_bwd_s<<<elementwise_grid(n - n4 * 4, kThreads), kThreads, 0, st>>>(
+      x, dy, dx, n4 * 4, n);
+  return check_launch("relu_backward", (n4 > 0) + (n4 * 4 < n));
+}
+
+int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t n,
+                  bf_stream_t s) {
+  if (n <= 0) return 0;
+  if (aligned16(w) && aligned16(g) && aligned16(out))
+    sgd_kernel<<<elementwise_grid((n + 3) / 4, kThreads), kThreads, 0, as_stream(s)>>>(
+        w, g, out, lr, n);
+  else
+    sgd_scalar<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(w, g, out, lr, n);
+  return check_launch("sgd_update");
+}
+
+int bf_sgd_momentum(const float* w, const float* g, const float* v, float* w_new, float* v_new,
+                    float lr, float momentum, int64_t n, bf_stream_t s) {
+  if (n <= 0) return 0;
+  sgd_momentum_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(
+      w, g, v, w_new, v_new, lr, momentum, n);
+  return check_launch("sgd_momentum");
+}
+
+int bf_sgd_mean_update(const float* w, const float* gsum, float* out, float lr, int k,
+                       int64_t n, bf_stream_t s) {
+  if (n <= 0) return 0;
+  BF_REQUIRE(k >= 1, "sgd_mean_update: k must be >= 1");
+  sgd_mean_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(
+      w, gsum, out, lr, (float)k, n);
+  return check_launch("sgd_mean_update");
+}
+
+int bf_aggregate(const float* const* parts, int k, float* out, int64_t n, int mean,
+                 bf_stream_t s) {
+  BF_REQUIRE(k >= 1 && k <= 32, "aggregate: 1 <= k <= 32 inputs supported, got %d", k);
+  if (n <= 0) return 0;
+  Parts p;
+  for (int i = 0; i < k; ++i) p.p[i] = parts[i];
+  aggregate_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(p, k, out, n,
+                                                                                 mean);
+  return check_launch("aggregate");
+}
+
+int bf_copy(float* dst, int dst_device, const float* src, int src_device, int64_t n,
+            bf_stream_t s) {
+  if (n <= 0) return 0;
+  size_t bytes = (size_t)n * sizeof(float);
+  if (dst_device == src_device)
+    BF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(s)), "copy");
+  else
+    BF_CUDA(cudaMemcpyPeerAsync(dst, dst_device, src, src_device, bytes, as_stream(s)),
+            "copy(peer)");
+  return 0;
+}
+
+int bf_check_finite(const float* x, int64_t n, int* flag, bf_stream_t s) {
+  if (n <= 0) return 0;
+  finite_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(x, n, flag);
+  return check_launch("check_finite");
+}
+
+}  // extern "C"

@@ -1,0 +1,117 @@
+// C-ABI entry points for the dense contractions: conv fwd / dgrad / wgrad and
+// the fully connected layer (reference ops.py:164-343).  Each maps its
+// operator onto D[m][n] = sum_k A(m,k) B(n,k) (gemm_common.cuh) and hands it
+// to the tcgen05 engine, or the SIMT engine when the tcgen05 engine declines
+// the shape or SIMT is forced.
+#include "gemm_common.cuh"
+#include "gemm_engines.cuh"
+
+namespace bf {
+
+int g_gemm_engine = 0;
+
+template <class LA, class LB, class Epi>
+static int run_gemm(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
+                    int64_t ws_bytes, cudaStream_t st, const char* what) {
+  if (g_gemm_engine == 0) {
+    int rc = tc_gemm(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
+    if (rc >= 0) return rc;
+  }
+  return simt_gemm(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
+}
+
+static int check_conv(int N, int C, int H, int W, int K, int R, int S, int P, int Q, int stride,
+                      int pad) {
+  BF_REQUIRE(N > 0 && C > 0 && H > 0 && W > 0 && K > 0 && R > 0 && S > 0 && P > 0 && Q > 0,
+             "conv2d: non-positive dimension");
+  BF_REQUIRE(stride >= 1 && pad >= 0, "conv2d: bad stride/pad");
+  BF_REQUIRE((H + 2 * pad - R) / stride + 1 == P && (W + 2 * pad - S) / stride + 1 == Q,
+             "conv2d: output dims %dx%d do not match geometry", P, Q);
+  BF_REQUIRE((int64_t)N * C * H * W < (1LL << 31) && (int64_t)N * K * P * Q < (1LL << 31),
+             "conv2d: tensor too large for 32-bit pixel indexing");
+  return 0;
+}
+
+}  // namespace bf
+
+using namespace bf;
+
+extern "C" {
+
+int bf_set_gemm_engine(int engine) {
+  BF_REQUIRE(engine == 0 || engine == 1, "bf_set_gemm_engine: 0 (auto) or 1 (simt)");
+  g_gemm_engine = engine;
+  return 0;
+}
+
+int bf_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int N, int C, int H,
+                  int W, int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
+                  int64_t ws_bytes, bf_stream_t s) {
+  if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
+  ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
+  LdFwdX la{x, g};
+  LdRowK lb{w, (int64_t)C * R * S};
+  EpiNCHW epi{y, b, P * Q, K};
+  return run_gemm(la, lb, N * P * Q, K, C * R * S, epi, ws, ws_bytes, as_stream(s),
+                  "conv2d_forward");
+}
+
+int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx, int N, int C, int H, int W,
+                       int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
+                       int64_t ws_bytes, bf_stream_t s) {
+  if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
+  ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
+  LdDgradDY la{dy, g};
+  LdDgradW lb{w, g};
+  EpiNCHW epi{dx, nullptr, H * W, C};
+  return run_gemm(la, lb, N * H * W, C, K * R * S, epi, ws, ws_bytes, as_stream(s),
+                  "conv2d_backward_data");
+}
+
+int bf_conv2d_bwd_weight(const float* x, const float* dy, float* dw, int N, int C, int H, int W,
+                         int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
+                         int64_t ws_bytes, bf_stream_t s) {
+  if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
+  ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
+  LdWgradX la{x, g};
+  LdWgradDY lb{dy, g};
+  EpiT epi{dw, nullptr, (int64_t)C * R * S};
+  return run_gemm(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
+                  "conv2d_backward_weight");
+}
+
+int bf_fc_fwd(const float* x, const float* w, const float* b, float* y, int n, int d, int m,
+              float* ws, int64_t ws_bytes, bf_stream_t s) {
+  BF_REQUIRE(n > 0 && d > 0 && m > 0, "fc_forward: non-positive dimension");
+  LdColK la{w, m};
+  LdRowK lb{x, d};
+  EpiT epi{y, b, m};
+  return run_gemm(la, lb, m, n, d, epi, ws, ws_bytes, as_stream(s), "fc_forward");
+}
+
+int bf_fc_bwd_data(const float* w, const float* dy, float* dx, int n, int d, int m, float* ws,
+                   int64_t ws_bytes, bf_stream_t s) {
+  BF_REQUIRE(n > 0 && d > 0 && m > 0, "fc_backward_data: non-positive dimension");
+  LdRowK la{w, m};
+  LdRowK lb{dy, m};
+  EpiT epi{dx, nullptr, d};
+  return run_gemm(la, lb, d, n, m, epi, ws, ws_bytes, as_stream(s), "fc_backward_data");
+}
+
+int bf_fc_bwd_weight(const float* x, const float* dy, float* dw, int n, int d, int m, float* ws,
+                     int64_t ws_bytes, bf_stream_t s) {
+  BF_REQUIRE(n > 0 && d > 0 && m > 0, "fc_backward_weight: non-positive dimension");
+  LdColK la{dy, m};
+  LdColK lb{x, d};
+  EpiT epi{dw, nullptr, m};
+  return run_gemm(la, lb, m, d, n, epi, ws, ws_bytes, as_stream(s), "fc_backward_weight");
+}
+
+int64_t bf_gemm_workspace_bytes(int op, int N, int C, int H, int W, int K, int R, int S, int P,
+                                int Q, int stride, int pad) {
+  (void)op; (void)N; (void)C; (void)H; (void)W; (void)K; (void)R; (void)S; (void)P; (void)Q;
+  (void)stride; (void)pad;
+  return 64LL << 20;  // one fixed 64 MiB split-K workspace per lane
+}
+
+}  // extern "C"

@@ -1,0 +1,20 @@
+// GEMM engine entry points (templated on loaders / epilogue).
+#pragma once
+
+#include "gemm_common.cuh"
+
+namespace bf {
+
+// SIMT fp32 engine (gemm_simt.cu)
+template <class LA, class LB, class Epi>
+int simt_gemm(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
+              int64_t ws_bytes, cudaStream_t st, const char* what);
+
+// tcgen05 3xTF32 engine (gemm_tc.cu); returns -1 when the shape is not taken
+template <class LA, class LB, class Epi>
+int tc_gemm(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
+            int64_t ws_bytes, cudaStream_t st, const char* what);
+
+extern int g_gemm_engine;  // 0 auto, 1 simt
+
+}  // namespace bf

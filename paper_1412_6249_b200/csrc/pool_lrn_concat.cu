@@ -1,0 +1,408 @@
+// Pooling (Caffe ceil-mode max / average), LRN across channels, channel
+// concat, softmax cross-entropy and bias-gradient reductions.  All HBM-bound.
+//
+// Backward passes of the overlapping 3x3/2 poolings are written as GATHERS
+// (one thread per input element visiting the output windows that cover it in
+// row-major order), so they need no atomics and reproduce the CPU oracle's
+// accumulation order bit for bit (oracle/kernels.py maxpool_backward /
+// avgpool_backward).
+#include "common.cuh"
+
+namespace bf {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void window_rows(int o, int stride, int pad, int k, int size, int& lo,
+                                            int& hi) {
+  int s = o * stride - pad;
+  hi = min(s + k, size);
+  lo = max(s, 0);
+}
+
+__global__ void maxpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
+                                   float* __restrict__ mask, int64_t total, int H, int W, int P,
+                                   int Q, int k, int stride, int pad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int pw = (int)(i % Q);
+    int ph = (int)((i / Q) % P);
+    int64_t plane = i / ((int64_t)P * Q);
+    const float* xp = x + plane * (int64_t)H * W;
+    int h0, h1, w0, w1;
+    window_rows(ph, stride, pad, k, H, h0, h1);
+    window_rows(pw, stride, pad, k, W, w0, w1);
+    float best = -INFINITY;
+    int arg = -1;
+    for (int h = h0; h < h1; ++h)
+      for (int w = w0; w < w1; ++w) {
+        float v = xp[h * W + w];
+        if (v > best) {
+          best = v;
+          arg = h * W + w;
+        }
+      }
+    y[i] = best;
+    mask[i] = (float)arg;
+  }
+}
+
+// output windows [lo, hi) along one axis that contain input coordinate h
+__device__ __forceinline__ void covering(int h, int stride, int pad, int k, int P, int& lo,
+                                         int& hi) {
+  lo = (h + pad < k) ? 0 : (h + pad - k) / stride + 1;
+  hi = min((h + pad) / stride + 1, P);
+}
+
+__global__ void maxpool_bwd_kernel(const float* __restrict__ mask, const float* __restrict__ dy,
+                                   float* __restrict__ dx, int64_t total, int H, int W, int P,
+                                   int Q, int k, int stride, int pad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int w = (int)(i % W);
+    int h = (int)((i / W) % H);
+    int64_t plane = i / ((int64_t)H * W);
+    const float* mp = mask + plane * (int64_t)P * Q;
+    const float* gp = dy + plane * (int64_t)P * Q;
+    int p0, p1, q0, q1;
+    covering(h, stride, pad, k, P, p0, p1);
+    covering(w, stride, pad, k, Q, q0, q1);
+    float me = (float)(h * W + w);
+    float acc = 0.f;
+    for (int p = p0; p < p1; ++p)
+      for (int q = q0; q < q1; ++q)
+        if (mp[p * Q + q] == me) acc = __fadd_rn(acc, gp[p * Q + q]);
+    dx[i] = acc;
+  }
+}
+
+__device__ __forceinline__ int avg_count(int o, int stride, int pad, int k, int size) {
+  int s = o * stride - pad;
+  int e = min(s + k, size + pad);
+  return e - s;
+}
+
+__global__ void avgpool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
+                                   int64_t total, int H, int W, int P, int Q, int k, int stride,
+                                   int pad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int pw = (int)(i % Q);
+    int ph = (int)((i / Q) % P);
+    int64_t plane = i / ((int64_t)P * Q);
+    const float* xp = x + plane * (int64_t)H * W;
+    int h0, h1, w0, w1;
+    window_rows(ph, stride, pad, k, H, h0, h1);
+    window_rows(pw, stride, pad, k, W, w0, w1);
+    float acc = 0.f;
+    for (int h = h0; h < h1; ++h)
+      for (int w = w0; w < w1; ++w) acc = __fadd_rn(acc, xp[h * W + w]);
+    float cnt = (float)(avg_count(ph, stride, pad, k, H) * avg_count(pw, stride, pad, k, W));
+    y[i] = __fdiv_rn(acc, cnt);
+  }
+}
+
+__global__ void avgpool_bwd_kernel(const float* __restrict__ dy, float* __restrict__ dx,
+                                   int64_t total, int H, int W, int P, int Q, int k, int stride,
+                                   int pad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int w = (int)(i % W);
+    int h = (int)((i / W) % H);
+    int64_t plane = i / ((int64_t)H * W);
+    const float* gp = dy + plane * (int64_t)P * Q;
+    int p0, p1, q0, q1;
+    covering(h, stride, pad, k, P, p0, p1);
+    covering(w, stride, pad, k, Q, q0, q1);
+    float acc = 0.f;
+    for (int p = p0; p < p1; ++p) {
+      int ch = avg_count(p, stride, pad, k, H);
+      for (int q = q0; q < q1; ++q) {
+        float cnt = (float)(ch * avg_count(q, stride, pad, k, W));
+        acc = __fadd_rn(acc, __fdiv_rn(gp[p * Q + q], cnt));
+      }
+    }
+    dx[i] = acc;
+  }
+}
+
+// LRN: one thread per element; window sums in channel order, as the oracle.
+__global__ void lrn_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
+                               float* __restrict__ scale, int64_t total, int C, int HW, int pre,
+                               int post, float a_n, float beta, float kk) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)((i / HW) % C);
+    int64_t base = i - (int64_t)c * HW;  // element (n, 0, hw)
+    int lo = max(c - pre, 0), hi = min(c + post, C - 1);
+    float acc = 0.f;
+    for (int cj = lo; cj <= hi; ++cj) {
+      float v = x[base + (int64_t)cj * HW];
+      acc = __fadd_rn(acc, __fmul_rn(v, v));
+    }
+    float sc = __fadd_rn(kk, __fmul_rn(a_n, acc));
+    scale[i] = sc;
+    y[i] = __fmul_rn(x[i], powf(sc, -beta));
+  }
+}
+
+__global__ void lrn_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
+                               const float* __restrict__ scale, const float* __restrict__ dy,
+                               float* __restrict__ dx, int64_t total, int C, int HW, int pre,
+                               int post, float coef, float beta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)((i / HW) % C);
+    int64_t base = i - (int64_t)c * HW;
+    int lo = max(c - post, 0), hi = min(c + pre, C - 1);
+    float acc = 0.f;
+    for (int cj = lo; cj <= hi; ++cj) {
+      int64_t j = base + (int64_t)cj * HW;
+      acc = __fadd_rn(acc, __fdiv_rn(__fmul_rn(dy[j], y[j]), scale[j]));
+    }
+    float a = __fmul_rn(dy[i], powf(scale[i], -beta));
+    float b = __fmul_rn(__fmul_rn(coef, x[i]), acc);
+    dx[i] = __fsub_rn(a, b);
+  }
+}
+
+// concat: copy one part [N][Ci*HW] into / out of the stacked [N][Ctot*HW]
+__global__ void concat_part_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                   int64_t chunk, int64_t src_stride, int64_t dst_stride,
+                                   int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = i / chunk, e = i - n * chunk;
+    dst[n * dst_stride + e] = src[n * src_stride + e];
+  }
+}
+
+__global__ void concat_part_v4(const float4* __restrict__ src, float4* __restrict__ dst,
+                               int64_t chunk, int64_t src_stride, int64_t dst_stride,
+                               int64_t total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = i / chunk, e = i - n * chunk;
+    dst[n * dst_stride + e] = src[n * src_stride + e];
+  }
+}
+
+int copy_rows(const float* src, float* dst, int64_t N, int64_t chunk, int64_t src_stride,
+              int64_t dst_stride, cudaStream_t st) {
+  int64_t total = N * chunk;
+  if (total <= 0) return 0;
+  bool v4 = chunk % 4 == 0 && src_stride % 4 == 0 && dst_stride % 4 == 0 && aligned16(src) &&
+            aligned16(dst);
+  if (v4)
+    concat_part_v4<<<elementwise_grid(total / 4, kThreads), kThreads, 0, st>>>(
+        reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), chunk / 4,
+        src_stride / 4, dst_stride / 4, total / 4);
+  else
+    concat_part_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, st>>>(
+        src, dst, chunk, src_stride, dst_stride, total);
+  return check_launch("concat");
+}
+
+// softmax cross-entropy: one CTA per row
+__device__ __forceinline__ float block_reduce(float v, float* red, bool is_max) {
+  for (int o = 16; o > 0; o >>= 1) {
+    float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  int nw = blockDim.x >> 5;
+  v = (threadIdx.x < nw) ? red[threadIdx.x] : (is_max ? -INFINITY : 0.f);
+  if (warp == 0)
+    for (int o = 16; o > 0; o >>= 1) {
+      float u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = is_max ? fmaxf(v, u) : v + u;
+    }
+  if (threadIdx.x == 0) red[32] = v;
+  __syncthreads();
+  return red[32];
+}
+
+__global__ void softmax_rows_kernel(const float* __restrict__ logits,
+                                    const float* __restrict__ labels, float* __restrict__ dlogits,
+                                    float* __restrict__ nll, int n, int k) {
+  __shared__ float red[33];
+  int row = blockIdx.x;
+  const float* z = logits + (int64_t)row * k;
+  float* g = dlogits + (int64_t)row * k;
+  float m = -INFINITY;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) m = fmaxf(m, z[j]);
+  m = block_reduce(m, red, true);
+  float s = 0.f;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) s += expf(z[j] - m);
+  s = block_reduce(s, red, false);
+  float lab = labels[row];
+  int li = (int)lab;
+  bool ok = (float)li == lab && li >= 0 && li < k;
+  float inv_n = (float)n;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    float p = __fdiv_rn(expf(z[j] - m), s);
+    if (j == li) p = p - 1.f;
+    g[j] = __fdiv_rn(p, inv_n);
+  }
+  if (threadIdx.x == 0) nll[row] = ok ? -((z[li] - m) - logf(s)) : NAN;  // NaN -> finite check
+}
+
+__global__ void mean_kernel(const float* __restrict__ v, float* __restrict__ out, int n) {
+  __shared__ float red[33];
+  float s = 0.f;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) s += v[j];
+  s = block_reduce(s, red, false);
+  if (threadIdx.x == 0) out[0] = s / (float)n;
+}
+
+// per-channel sum over (n, pq): one CTA per channel, fixed tree -> deterministic
+__global__ void channel_sum_kernel(const float* __restrict__ dy, float* __restrict__ db, int N,
+                                   int K, int PQ) {
+  __shared__ float red[33];
+  int c = blockIdx.x;
+  float acc = 0.f;
+  int64_t total = (int64_t)N * PQ;
+  for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+    int64_t n = i / PQ, e = i - n * PQ;
+    acc += dy[(n * K + c) * PQ + e];
+  }
+  acc = block_reduce(acc, red, false);
+  if (threadIdx.x == 0) db[c] = acc;
+}
+
+// column sum of [n][m]: one thread per column, rows in order
+__global__ void column_sum_kernel(const float* __restrict__ dy, float* __restrict__ db, int n,
+                                  int m) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  float acc = 0.f;
+  for (int i = 0; i < n; ++i) acc += dy[(int64_t)i * m + j];
+  db[j] = acc;
+}
+
+}  // namespace
+}  // namespace bf
+
+using namespace bf;
+
+extern "C" {
+
+int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, int W, int P,
+                   int Q, int kernel, int stride, int pad, bf_stream_t s) {
+  int64_t total = (int64_t)N * C * P * Q;
+  if (total <= 0) return 0;
+  maxpool_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
+      x, y, mask, total, H, W, P, Q, kernel, stride, pad);
+  return check_launch("maxpool_forward");
+}
+
+int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, int H, int W,
+                   int P, int Q, int kernel, int stride, int pad, bf_stream_t s) {
+  int64_t total = (int64_t)N * C * H * W;
+  if (total <= 0) return 0;
+  maxpool_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
+      mask, dy, dx, total, H, W, P, Q, kernel, stride, pad);
+  return check_launch("maxpool_backward");
+}
+
+int bf_avgpool_fwd(const float* x, float* y, int N, int C, int H, int W, int P, int Q,
+                   int kernel, int stride, int pad, bf_stream_t s) {
+  int64_t total = (int64_t)N * C * P * Q;
+  if (total <= 0) return 0;
+  avgpool_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
+      x, y, total, H, W, P, Q, kernel, stride, pad);
+  return check_launch("avgpool_forward");
+}
+
+int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P, int Q,
+                   int kernel, int stride, int pad, bf_stream_t s) {
+  int64_t total = (int64_t)N * C * H * W;
+  if (total <= 0) return 0;
+  avgpool_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
+      dy, dx, total, H, W, P, Q, kernel, stride, pad);
+  return check_launch("avgpool_backward");
+}
+
+int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int W, int size,
+               float alpha, float beta, float k, bf_stream_t s) {
+  BF_REQUIRE(size >= 1, "lrn_forward: size must be >= 1");
+  int64_t total = (int64_t)N * C * H * W;
+  if (total <= 0) return 0;
+  int pre = (size - 1) / 2, post = size - 1 - pre;
+  float a_n = alpha / (float)size;
+  lrn_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
+      x, y, scale, total, C, H * W, pre, post, a_n, beta, k);
+  return check_launch("lrn_forward");
+}
+
+int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* dy, float* dx,
+               int N, int C, int H, int W, int size, float alpha, float beta, float k,
+               bf_stream_t s) {
+  BF_REQUIRE(size >= 1, "lrn_backward: size must be >= 1");
+  int64_t total = (int64_t)N * C * H * W;
+  if (total <= 0) return 0;
+  int pre = (size - 1) / 2, post = size - 1 - pre;
+  float coef = 2.0f * alpha;
+  coef = coef * beta;
+  coef = coef / (float)size;
+  lrn_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
+      x, y, scale, dy, dx, total, C, H * W, pre, post, coef, beta);
+  (void)k;
+  return check_launch("lrn_backward");
+}
+
+int bf_concat_fwd(const float* const* parts, const int* channels, int k, float* y, int N, int H,
+                  int W, bf_stream_t s) {
+  BF_REQUIRE(k >= 1 && k <= 32, "concat_forward: 1..32 parts");
+  int64_t HW = (int64_t)H * W, Ct = 0;
+  for (int i = 0; i < k; ++i) Ct += channels[i];
+  int64_t off = 0;
+  for (int i = 0; i < k; ++i) {
+    int64_t chunk = (int64_t)channels[i] * HW;
+    int rc = copy_rows(parts[i], y + off * HW, N, chunk, chunk, Ct * HW, as_stream(s));
+    if (rc) return rc;
+    off += channels[i];
+  }
+  return 0;
+}
+
+int bf_concat_bwd(const float* dy, float* const* parts, const int* channels, int k, int N, int H,
+                  int W, bf_stream_t s) {
+  BF_REQUIRE(k >= 1 && k <= 32, "concat_backward: 1..32 parts");
+  int64_t HW = (int64_t)H * W, Ct = 0;
+  for (int i = 0; i < k; ++i) Ct += channels[i];
+  int64_t off = 0;
+  for (int i = 0; i < k; ++i) {
+    int64_t chunk = (int64_t)channels[i] * HW;
+    int rc = copy_rows(dy + off * HW, parts[i], N, chunk, Ct * HW, chunk, as_stream(s));
+    if (rc) return rc;
+    off += channels[i];
+  }
+  return 0;
+}
+
+int bf_softmax_xent(const float* logits, const float* labels, float* loss, float* dlogits, int n,
+                    int k, float* workspace, bf_stream_t s) {
+  BF_REQUIRE(n >= 1 && k >= 1, "softmax_xent: empty logits");
+  softmax_rows_kernel<<<n, 256, 0, as_stream(s)>>>(logits, labels, dlogits, workspace, n, k);
+  if (int rc = check_launch("softmax_xent")) return rc;
+  mean_kernel<<<1, 256, 0, as_stream(s)>>>(workspace, loss, n);
+  return check_launch("softmax_xent(mean)");
+}
+
+int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, bf_stream_t s) {
+  if (K <= 0) return 0;
+  channel_sum_kernel<<<K, 512, 0, as_stream(s)>>>(dy, db, N, K, PQ);
+  return check_launch("conv2d_backward_bias");
+}
+
+int bf_fc_bwd_bias(const float* dy, float* db, int n, int m, bf_stream_t s) {
+  if (m <= 0) return 0;
+  column_sum_kernel<<<(m + 127) / 128, 128, 0, as_stream(s)>>>(dy, db, n, m);
+  return check_launch("fc_backward_bias");
+}
+
+}  // extern "C"

@@ -1,0 +1,459 @@
+"""Event-driven graph execution on CUDA streams.
+
+Drop-in for the reference dispatcher (`pkg/src/biflow/dispatcher.py`):
+same `run` / `run_sequence` signatures and hooks, same `ReadinessState`
+bookkeeping, `TraceRecord` / `RunReport` / `merged_trace`, `DispatchError`
+with first-error-wins, `BIFLOW_LANES` lane cap.
+
+B200 design.  The reference runs one OS thread per lane, each pulling ready
+operators from a FIFO and executing numpy kernels synchronously.  Here a
+lane ``(host, device, thread)`` is a CUDA stream of the store's device and
+readiness is enforced ON THE DEVICE: every tensor carries the CUDA event its
+producer recorded, and an operator is enqueued behind
+``cudaStreamWaitEvent`` on each input produced on another stream.  The host
+therefore never waits for kernels; it walks the graph once, in the
+reference's serial-mode order (the `ReadinessState` arm/complete FIFO,
+dispatcher.py:144-191), which is topological, so FIFO streams cannot
+deadlock even when lanes share a stream, and every rank enqueues collectives
+in the same order.  Streams run concurrently, giving the reference's
+lane-level overlap (compute lanes vs. copy lanes) on the GPU.
+
+Lane cap: ``max_workers`` / ``BIFLOW_LANES`` bounds the number of streams;
+sorted lanes map round-robin onto them exactly as lanes map onto worker
+threads in the reference (dispatcher.py:261-267).  ``1`` is the fully serial
+mode: one stream, device execution order == dispatch order.
+
+Timing: with ``trace=True`` each operator is bracketed by CUDA events on its
+stream; `TraceRecord` start/end are ns since the sequence's zero event, so
+the reference's interval arithmetic (profiler.py) applies unchanged.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+import torch
+
+from .graph import BiGraph, GraphSequence, OperatorVertex
+from .kinds import KINDS, KernelError
+from .store import TensorStore
+
+__all__ = [
+    "DispatchError",
+    "LANES_ENV",
+    "ReadinessState",
+    "RunContext",
+    "RunReport",
+    "TraceRecord",
+    "WorkerLane",
+    "lane_of",
+    "merged_trace",
+    "run",
+    "run_sequence",
+    "serial_order",
+]
+
+LANES_ENV = "BIFLOW_LANES"
+
+
+class DispatchError(RuntimeError):
+    """A run could not start or finish; carries the offending operator's name."""
+
+
+@dataclass(frozen=True, order=True)
+class WorkerLane:
+    """A serial execution queue (here: one CUDA stream)."""
+
+    host: str
+    device: int
+    thread: int
+
+
+def lane_of(op: OperatorVertex) -> WorkerLane:
+    return WorkerLane(op.location.host, op.location.device, op.thread)
+
+
+@dataclass(frozen=True)
+class TraceRecord:
+    """One operator execution; times are ns since the run's zero event."""
+
+    op: int
+    name: str
+    lane: WorkerLane
+    start: int
+    end: int
+    iteration: int = 0
+
+
+@dataclass
+class RunReport:
+    trace: list[TraceRecord]
+    elapsed: int
+    iteration: int = 0
+    graph_index: int = 0
+    dispatch_order: list[str] = field(default_factory=list)
+
+
+def merged_trace(reports: list[RunReport]) -> list[TraceRecord]:
+    recs = [r for rep in reports for r in rep.trace]
+    recs.sort(key=lambda r: (r.start, r.end))
+    return recs
+
+
+# ---------------------------------------------------------------------------
+# readiness bookkeeping (dispatcher.py:96-206)
+
+
+class ReadinessState:
+    """Pending-count bookkeeping for one graph (same contract as the reference).
+
+    ``pending_inputs``: operator id -> unsatisfied input edges;
+    ``pending_producers``: tensor id -> producers not yet completed.
+    `arm` returns the initially ready operators and `complete` the newly
+    ready ones, both in graph-insertion order.
+    """
+
+    def __init__(self, graph: BiGraph) -> None:
+        self.graph = graph
+        self._rank = {oid: i for i, oid in enumerate(graph.insertion_order)}
+        self._tensor_sinks = {t for t in graph.tensors if not graph.consumers_of(t)}
+        self._op_sinks = {o for o, op in graph.operators.items() if not op.outputs}
+        self.sink_count = len(self._tensor_sinks) + len(self._op_sinks)
+        self._in_flight = 0
+        self.reset()
+
+    def reset(self) -> None:
+        if self._in_flight:
+            raise DispatchError("reset() while operators are in flight")
+        g = self.graph
+        self.pending_inputs = {o: len(op.inputs) for o, op in g.operators.items()}
+        self.pending_producers = {t: int(g.producer_of(t) is not None) for t in g.tensors}
+        self.completed_sinks = 0
+        self._executed = 0
+        self._armed = False
+
+    def _release(self, tid: int, out: list[int]) -> None:
+        if tid in self._tensor_sinks:
+            self.completed_sinks += 1
+        for oid, _pos in self.graph.consumers_of(tid):
+            self.pending_inputs[oid] -= 1
+            if self.pending_inputs[oid] == 0:
+                out.append(oid)
+
+    def arm(self) -> list[int]:
+        if self._armed:
+            raise DispatchError("arm() on an already armed state")
+        self._armed = True
+        ready = [o for o in self.graph.insertion_order if self.pending_inputs[o] == 0]
+        for tid in sorted(self.graph.tensors):
+            if self.pending_producers[tid] == 0:
+                self._release(tid, ready)
+        ordered = sorted(dict.fromkeys(ready), key=self._rank.__getitem__)
+        self._in_flight += len(ordered)
+        return ordered
+
+    def complete(self, op_id: int) -> list[int]:
+        op = self.graph.operators[op_id]
+        self._executed += 1
+        self._in_flight -= 1
+        if op_id in self._op_sinks:
+            self.completed_sinks += 1
+        fresh: list[int] = []
+        for tid in op.outputs:
+            self.pending_producers[tid] -= 1
+            if self.pending_producers[tid] == 0:
+                self._release(tid, fresh)
+        fresh.sort(key=self._rank.__getitem__)
+        self._in_flight += len(fresh)
+        return fresh
+
+    def abandon(self, count: int = 1) -> None:
+        self._in_flight -= count
+
+    @property
+    def in_flight(self) -> int:
+        return self._in_flight
+
+    @property
+    def done(self) -> bool:
+        return self._executed == len(self.graph.operators) and self.completed_sinks == self.sink_count
+
+
+_ORDER_CACHE: dict[int, tuple[int, list[int]]] = {}
+
+
+def serial_order(graph: BiGraph) -> list[int]:
+    """Reference serial-mode (one worker) dispatch order of ``graph``."""
+    key = id(graph)
+    stamp = len(graph.insertion_order) * 1_000_003 + len(graph.tensors)
+    hit = _ORDER_CACHE.get(key)
+    if hit is not None and hit[0] == stamp:
+        return hit[1]
+    st = ReadinessState(graph)
+    queue = st.arm()
+    head = 0
+    while head < len(queue):
+        queue.extend(st.complete(queue[head]))
+        head += 1
+    if len(queue) != len(graph.operators):
+        raise DispatchError("graph cannot complete: some operators never become ready")
+    _ORDER_CACHE[key] = (stamp, queue)
+    return queue
+
+
+# ---------------------------------------------------------------------------
+# run context and stream/workspace pools
+
+
+@dataclass
+class RunContext:
+    """Everything a kernel execution hook may touch (dispatcher.py:209-217),
+    plus the lane's CUDA stream handle and split-K workspace."""
+
+    store: TensorStore
+    graph: BiGraph
+    iteration: int = 0
+    transport: object | None = None
+    copy_latency_s: float = 0.0
+    stream: int = 0
+    workspace: torch.Tensor | None = None
+    lane: WorkerLane | None = None
+
+
+WORKSPACE_FLOATS = 16 << 20  # 64 MiB per stream
+
+
+class _Lanes:
+    """Per-store pool of CUDA streams (one per lane slot) and workspaces."""
+
+    def __init__(self, store: TensorStore) -> None:
+        self.device = store.device
+        self.streams: list[torch.cuda.Stream] = []
+        self.workspaces: list[torch.Tensor] = []
+
+    def get(self, idx: int) -> tuple[torch.cuda.Stream, torch.Tensor]:
+        while len(self.streams) <= idx:
+            self.streams.append(torch.cuda.Stream(device=self.device))
+            self.workspaces.append(torch.empty(WORKSPACE_FLOATS, dtype=torch.float32,
+                                               device=self.device))
+        return self.streams[idx], self.workspaces[idx]
+
+
+def lanes_of(store: TensorStore) -> _Lanes:
+    pool = getattr(store, "_lane_pool", None)
+    if pool is None:
+        pool = _Lanes(store)
+        store._lane_pool = pool
+        if store.device.type == "cuda":
+            from . import _native
+
+            _native.lib()("bf_set_device", store.device.index or 0)
+    return pool
+
+
+def _env_lane_cap() -> int:
+    raw = os.environ.get(LANES_ENV)
+    if not raw:
+        return 1 << 16
+    try:
+        cap = int(raw)
+    except ValueError:
+        raise DispatchError(f"{LANES_ENV} must be an integer, got {raw!r}") from None
+    if cap < 1:
+        raise DispatchError(f"{LANES_ENV} must be >= 1, got {cap}")
+    return cap
+
+
+def _check_sources(graph: BiGraph, store: TensorStore) -> None:
+    for tid, t in graph.tensors.items():
+        if graph.producer_of(tid) is None and graph.consumers_of(tid):
+            if not store.has(t.name):
+                raise DispatchError(f"source tensor {t.name!r} has no buffer in the store")
+            if store.get(t.name).shape != t.shape:
+                raise DispatchError(f"source tensor {t.name!r}: store shape "
+                                    f"{store.get(t.name).shape} != graph shape {t.shape}")
+
+
+class _Plan:
+    """Static per-(graph, lane cap) launch plan: order, lane slots, cross-stream edges."""
+
+    def __init__(self, graph: BiGraph, cap: int) -> None:
+        self.order = serial_order(graph)
+        lanes = sorted({lane_of(op) for op in graph.operators.values()})
+        n = max(1, min(len(lanes), cap)) if lanes else 0
+        self.slot_of_lane = {ln: i % n for i, ln in enumerate(lanes)} if n else {}
+        self.slot = {oid: self.slot_of_lane[lane_of(op)] for oid, op in graph.operators.items()}
+        self.n_slots = n
+        # inputs produced by an op on a different slot -> that producer must record an event
+        self.waits: dict[int, list[int]] = {}
+        self.signals: set[int] = set()
+        for oid, op in graph.operators.items():
+            deps = []
+            for tid in op.inputs:
+                p = graph.producer_of(tid)
+                if p is not None and self.slot[p] != self.slot[oid] and p not in deps:
+                    deps.append(p)
+                    self.signals.add(p)
+            self.waits[oid] = deps
+
+
+_PLAN_CACHE: dict[tuple[int, int], tuple[int, _Plan]] = {}
+
+
+def _plan(graph: BiGraph, cap: int) -> _Plan:
+    key = (id(graph), cap)
+    stamp = len(graph.insertion_order) * 1_000_003 + len(graph.tensors)
+    hit = _PLAN_CACHE.get(key)
+    if hit is not None and hit[0] == stamp:
+        return hit[1]
+    p = _Plan(graph, cap)
+    _PLAN_CACHE[key] = (stamp, p)
+    return p
+
+
+# ---------------------------------------------------------------------------
+# one graph run
+
+
+class _TimeBase:
+    def __init__(self) -> None:
+        self.event = torch.cuda.Event(enable_timing=True)
+        self.event.record()
+
+    def ns(self, ev: torch.cuda.Event) -> int:
+        return int(round(self.event.elapsed_time(ev) * 1e6))
+
+
+def _enqueue(graph, store, registry, cap, ctx, trace, base):
+    """Launch every operator of ``graph``; returns (dispatch names, timing events)."""
+    plan = _plan(graph, cap)
+    pool = lanes_of(store)
+    cur = torch.cuda.current_stream(store.device)
+    fork = torch.cuda.Event()
+    fork.record(cur)
+    slots = [pool.get(i) for i in range(plan.n_slots)]
+    for s, _ in slots:
+        s.wait_event(fork)
+    done_ev: dict[int, torch.cuda.Event] = {}
+    timing: list[tuple[int, torch.cuda.Event, torch.cuda.Event]] = []
+    names: list[str] = []
+    from . import _native
+
+    failure = None
+    for oid in plan.order:
+        op = graph.operators[oid]
+        spec = registry.get(op.kind)
+        if spec is None:
+            failure = (op.name, DispatchError(
+                f"operator kind {op.kind!r} unknown to registry (op {op.name!r})"))
+            break
+        stream, ws = slots[plan.slot[oid]]
+        for p in plan.waits[oid]:
+            stream.wait_event(done_ev[p])
+        ctx.stream = stream.cuda_stream
+        ctx.workspace = ws
+        ctx.lane = lane_of(op)
+        try:
+            with torch.cuda.stream(stream):
+                if trace:
+                    t_start = torch.cuda.Event(enable_timing=True)
+                    t_start.record(stream)
+                delay = float(op.attrs.get("delay_s", 0.0) or 0.0)
+                if delay > 0:
+                    _native.lib()("bf_delay_ns", int(delay * 1e9), ctx.stream)
+                spec.execute(ctx, op)
+                if trace:
+                    t_end = torch.cuda.Event(enable_timing=True)
+                    t_end.record(stream)
+                    timing.append((oid, t_start, t_end))
+        except BaseException as exc:  # noqa: BLE001 - first error wins
+            failure = (op.name, exc)
+            break
+        if oid in plan.signals:
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            done_ev[oid] = ev
+        names.append(op.name)
+    for s, _ in slots:
+        join = torch.cuda.Event()
+        join.record(s)
+        cur.wait_event(join)
+    if failure is not None:
+        for s, _ in slots:  # drain what was already enqueued
+            s.synchronize()
+        name, exc = failure
+        if isinstance(exc, DispatchError) and "unknown to registry" in str(exc):
+            raise exc
+        raise DispatchError(f"operator {name!r} failed: {exc}") from exc
+    return names, timing
+
+
+def run(graph: BiGraph, store: TensorStore, registry: dict | None = None, *,
+        max_workers: int | None = None, iteration: int = 0, t0=None,
+        transport: object | None = None, copy_latency_s: float = 0.0,
+        validated: bool = False, trace: bool = True) -> RunReport:
+    """Execute one graph to completion (dispatcher.py:378-417).
+
+    With ``trace=True`` (default, as in the reference) the call returns after
+    the device finished the graph and the report carries per-operator device
+    times.  With ``trace=False`` it returns as soon as everything is enqueued.
+    """
+    if not validated:
+        rep = graph.validate()
+        if not rep.ok:
+            raise DispatchError("graph failed validation: " + "; ".join(rep.violations))
+    _check_sources(graph, store)
+    registry = KINDS if registry is None else registry
+    cap = max_workers if max_workers is not None else _env_lane_cap()
+    base = t0 if isinstance(t0, _TimeBase) else None
+    host0 = time.monotonic_ns()
+    if trace and base is None:
+        base = _TimeBase()
+    ctx = RunContext(store=store, graph=graph, iteration=iteration, transport=transport,
+                     copy_latency_s=copy_latency_s)
+    names, timing = _enqueue(graph, store, registry, cap, ctx, trace, base)
+    records: list[TraceRecord] = []
+    if trace:
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(torch.cuda.current_stream(store.device))
+        end.synchronize()
+        for oid, a, b in timing:
+            op = graph.operators[oid]
+            s, e = base.ns(a), base.ns(b)
+            records.append(TraceRecord(oid, op.name, lane_of(op), s, max(e, s + 1), iteration))
+        records.sort(key=lambda r: (r.start, r.end))
+    return RunReport(trace=records, elapsed=time.monotonic_ns() - host0, iteration=iteration,
+                     dispatch_order=names)
+
+
+def run_sequence(seq: GraphSequence, store: TensorStore, registry: dict | None = None, *,
+                 max_workers: int | None = None, transport: object | None = None,
+                 copy_latency_s: float = 0.0, before_iteration=None, after_graph=None,
+                 iterations: int | None = None, trace: bool = True) -> list[RunReport]:
+    """Run every graph of ``seq`` in order, ``iterations`` times (dispatcher.py:420-469).
+
+    Graph completion is the synchronisation point: graph i+1's streams wait
+    on an event joined from all of graph i's streams.  ``before_iteration``
+    and ``after_graph`` hooks behave as in the reference.
+    """
+    for g in seq.graphs:
+        rep = g.validate()
+        if not rep.ok:
+            raise DispatchError("graph failed validation: " + "; ".join(rep.violations))
+    base = _TimeBase() if trace else None
+    reports: list[RunReport] = []
+    rounds = seq.iterations if iterations is None else iterations
+    for it in range(rounds):
+        if before_iteration is not None:
+            before_iteration(it, store)
+        for gi, g in enumerate(seq.graphs):
+            rep = run(g, store, registry, max_workers=max_workers, iteration=it, t0=base,
+                      transport=transport, copy_latency_s=copy_latency_s, validated=True,
+                      trace=trace)
+            rep.graph_index = gi
+            reports.append(rep)
+            if after_graph is not None:
+                after_graph(rep, store)
+    return reports

@@ -1,0 +1,122 @@
+"""CUDA-graph replay of a graph sequence (launch-overhead removal).
+
+An iteration of GoogLeNet enqueues ~520 operators (~1k kernels); walking the
+graph in Python every iteration would cost more host time than the device
+needs.  The dispatcher's launch walk is deterministic, so it is captured once
+into a `torch.cuda.CUDAGraph` per graph of the sequence and replayed.
+
+Buffer bindings change every iteration: the swap graph exchanges
+``w`` <-> ``w_new`` handles (ops.py:93-102).  A swap graph is an involution,
+so there are exactly two bindings; each graph is captured once per binding
+parity and the replays alternate (ping-pong).  Host-only graphs (pure swap
+graphs) are not captured: their handle exchanges run on the host each
+iteration so `TensorStore` lookups stay truthful.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from .dispatcher import (DispatchError, RunContext, RunReport, _check_sources, _enqueue,
+                         _env_lane_cap, lanes_of)
+from .gpu_ops import HOST_ONLY
+from .graph import GraphSequence
+from .kinds import KINDS
+
+__all__ = ["CapturedSequence"]
+
+
+def _binding(store) -> dict[str, int]:
+    return {n: store.get(n).ptr for n in store.names()}
+
+
+class CapturedSequence:
+    """Captured replay of ``seq`` on ``store``'s device.
+
+    Call `prepare()` after the store holds every source tensor (parameters,
+    data, labels); it runs one eager iteration (which allocates every
+    buffer and advances the parameters by one step, like any iteration) and
+    then captures.  `step()` replays one full iteration."""
+
+    def __init__(self, seq: GraphSequence, store, registry: dict | None = None,
+                 max_workers: int | None = None, trace: bool = False) -> None:
+        self.seq = seq
+        self.store = store
+        self.registry = KINDS if registry is None else registry
+        self.cap = max_workers if max_workers is not None else _env_lane_cap()
+        self.parity = 0
+        self.graphs: list[list[torch.cuda.CUDAGraph | None]] = [[], []]
+        self.host_only = [all(op.kind in HOST_ONLY for op in g.operators.values())
+                          for g in seq.graphs]
+        self.ready = False
+        self.trace = trace
+        # per parity, per graph: [(op id, start event, end event)] recorded by the replays
+        self.timing: list[list[list]] = [[], []]
+        self.launches_per_step = 0
+
+    def _ctx(self, g, it=0):
+        return RunContext(store=self.store, graph=g, iteration=it)
+
+    def _run_eager(self, gi: int, it: int = 0, trace: bool = False):
+        g = self.seq.graphs[gi]
+        return _enqueue(g, self.store, self.registry, self.cap, self._ctx(g, it), trace, None)[1]
+
+    def prepare(self) -> None:
+        for g in self.seq.graphs:
+            rep = g.validate()
+            if not rep.ok:
+                raise DispatchError("graph failed validation: " + "; ".join(rep.violations))
+            _check_sources(g, self.store)
+        lanes_of(self.store)
+        for gi in range(len(self.seq.graphs)):  # warm-up: allocates every output buffer
+            self._run_eager(gi)
+        torch.cuda.synchronize(self.store.device)
+        start = _binding(self.store)
+        pool = torch.cuda.graph_pool_handle()
+        cap_stream = torch.cuda.Stream(device=self.store.device)
+        from . import _native
+
+        count = _native.lib().raw("bf_launch_count")
+        for par in (0, 1):
+            per, times = [], []
+            before = count()
+            for gi, g in enumerate(self.seq.graphs):
+                if self.host_only[gi]:
+                    self._run_eager(gi)
+                    per.append(None)
+                    times.append([])
+                    continue
+                cg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(cg, pool=pool, stream=cap_stream):
+                    times.append(self._run_eager(gi, trace=self.trace))
+                per.append(cg)
+            self.launches_per_step = count() - before
+            self.graphs[par] = per
+            self.timing[par] = times
+        if _binding(self.store) != start:
+            raise DispatchError("graph capture needs a period-2 buffer binding "
+                                "(swap graphs must be involutions)")
+        self.ready = True
+
+    def op_times_ms(self, parity: int) -> list[tuple[int, object, float]]:
+        """(graph index, operator, device ms) of the last replay of ``parity``
+        (needs ``trace=True``; call after synchronising)."""
+        out = []
+        for gi, recs in enumerate(self.timing[parity]):
+            g = self.seq.graphs[gi]
+            for oid, a, b in recs:
+                out.append((gi, g.operators[oid], a.elapsed_time(b)))
+        return out
+
+    def step(self, after_graph=None, iteration: int = 0) -> None:
+        if not self.ready:
+            raise DispatchError("CapturedSequence.step() before prepare()")
+        for gi, cg in enumerate(self.graphs[self.parity]):
+            if cg is None:
+                self._run_eager(gi, iteration)
+            else:
+                cg.replay()
+            if after_graph is not None:
+                after_graph(RunReport(trace=[], elapsed=0, iteration=iteration, graph_index=gi),
+                            self.store)
+        self.parity ^= 1

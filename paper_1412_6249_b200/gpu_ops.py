@@ -1,0 +1,344 @@
+"""Execute hooks of the operator kinds: resolve names -> device buffers, launch.
+
+Each hook has the reference signature ``execute(ctx, op)`` (ops.py:526-533)
+and launches one or more sm_100a kernels through the C ABI
+(`include/purine_b200.h`) on the CUDA stream the dispatcher assigned to the
+operator's lane (``ctx.stream``).  Outputs are written into buffers the
+store preallocated; nothing here allocates per launch or synchronises the
+host.  A kernel failure surfaces as `KernelError`.
+"""
+
+from __future__ import annotations
+
+from . import _native
+from .kinds import KernelError, conv_attrs, conv_out_dim, lrn_attrs, pool_attrs, pool_out_dim
+
+
+def _names(ctx, ids):
+    return [ctx.graph.tensors[i].name for i in ids]
+
+
+def _ins(ctx, op):
+    return [ctx.store.get(n) for n in _names(ctx, op.inputs)]
+
+
+def _outs(ctx, op):
+    g = ctx.graph
+    return [ctx.store.ensure(g.tensors[i].name, g.tensors[i].shape) for i in op.outputs]
+
+
+def _ws(ctx):
+    w = ctx.workspace
+    return w.data_ptr(), w.numel() * 4
+
+
+def _L():
+    return _native.lib()
+
+
+# ---------------------------------------------------------------------------
+# dense layer (ops.py:164-226)
+
+
+def _fc_fwd(ctx, op):
+    x, w, b = _ins(ctx, op)
+    (y,) = _outs(ctx, op)
+    n, d = x.shape
+    m = w.shape[1]
+    _L()("bf_fc_fwd", x.ptr, w.ptr, b.ptr, y.ptr, n, d, m, *_ws(ctx), ctx.stream)
+
+
+def _fc_bwd_parts(ctx, x, w, dy, dx, dw, db):
+    n, d = x.shape
+    m = w.shape[1]
+    lib = _L()
+    if dx is not None:
+        lib("bf_fc_bwd_data", w.ptr, dy.ptr, dx.ptr, n, d, m, *_ws(ctx), ctx.stream)
+    if dw is not None:
+        lib("bf_fc_bwd_weight", x.ptr, dy.ptr, dw.ptr, n, d, m, *_ws(ctx), ctx.stream)
+    if db is not None:
+        lib("bf_fc_bwd_bias", dy.ptr, db.ptr, n, m, ctx.stream)
+
+
+def _fc_bwd(ctx, op):
+    x, w, dy = _ins(ctx, op)
+    dx, dw, db = _outs(ctx, op)
+    _fc_bwd_parts(ctx, x, w, dy, dx, dw, db)
+
+
+def _fc_bwd_data(ctx, op):
+    w, dy = _ins(ctx, op)
+    (dx,) = _outs(ctx, op)
+    n, m = dy.shape
+    _L()("bf_fc_bwd_data", w.ptr, dy.ptr, dx.ptr, n, w.shape[0], m, *_ws(ctx), ctx.stream)
+
+
+def _fc_bwd_weight(ctx, op):
+    x, dy = _ins(ctx, op)
+    (dw,) = _outs(ctx, op)
+    n, d = x.shape
+    _L()("bf_fc_bwd_weight", x.ptr, dy.ptr, dw.ptr, n, d, dy.shape[1], *_ws(ctx), ctx.stream)
+
+
+def _fc_bwd_bias(ctx, op):
+    (dy,) = _ins(ctx, op)
+    (db,) = _outs(ctx, op)
+    _L()("bf_fc_bwd_bias", dy.ptr, db.ptr, dy.shape[0], dy.shape[1], ctx.stream)
+
+
+# ---------------------------------------------------------------------------
+# convolution (ops.py:229-352)
+
+
+def _geom(x, w, attrs):
+    stride, pad, floor = conv_attrs(attrs)
+    n, c, h, wd = x.shape
+    k, _, r, s = w.shape
+    p = conv_out_dim(h, r, stride, pad, floor)
+    q = conv_out_dim(wd, s, stride, pad, floor)
+    return (n, c, h, wd, k, r, s, p, q, stride, pad)
+
+
+def _conv_fwd(ctx, op):
+    x, w, b = _ins(ctx, op)
+    (y,) = _outs(ctx, op)
+    _L()("bf_conv2d_fwd", x.ptr, w.ptr, b.ptr, y.ptr, *_geom(x, w, op.attrs), *_ws(ctx), ctx.stream)
+
+
+def _conv_bwd_parts(ctx, attrs, x, w, dy, dx, dw, db):
+    g = _geom(x, w, attrs)
+    lib = _L()
+    # weight and bias first: they feed the parameter exchange; data last
+    if dw is not None:
+        lib("bf_conv2d_bwd_weight", x.ptr, dy.ptr, dw.ptr, *g, *_ws(ctx), ctx.stream)
+    if db is not None:
+        lib("bf_conv2d_bwd_bias", dy.ptr, db.ptr, g[0], g[4], g[7] * g[8], ctx.stream)
+    if dx is not None:
+        lib("bf_conv2d_bwd_data", w.ptr, dy.ptr, dx.ptr, *g, *_ws(ctx), ctx.stream)
+
+
+def _conv_bwd(ctx, op):
+    x, w, dy = _ins(ctx, op)
+    dx, dw, db = _outs(ctx, op)
+    _conv_bwd_parts(ctx, op.attrs, x, w, dy, dx, dw, db)
+
+
+def _conv_bwd_data(ctx, op):
+    x, w, dy = _ins(ctx, op)
+    (dx,) = _outs(ctx, op)
+    _conv_bwd_parts(ctx, op.attrs, x, w, dy, dx, None, None)
+
+
+def _conv_bwd_weight(ctx, op):
+    x, w, dy = _ins(ctx, op)
+    (dw,) = _outs(ctx, op)
+    _conv_bwd_parts(ctx, op.attrs, x, w, dy, None, dw, None)
+
+
+def _conv_bwd_bias(ctx, op):
+    (dy,) = _ins(ctx, op)
+    (db,) = _outs(ctx, op)
+    n, k, p, q = dy.shape
+    _L()("bf_conv2d_bwd_bias", dy.ptr, db.ptr, n, k, p * q, ctx.stream)
+
+
+# ---------------------------------------------------------------------------
+# activation / reshape / loss / update / aggregation
+
+
+def _relu_fwd(ctx, op):
+    (x,) = _ins(ctx, op)
+    (y,) = _outs(ctx, op)
+    _L()("bf_relu_fwd", x.ptr, y.ptr, x.numel, ctx.stream)
+
+
+def _relu_bwd(ctx, op):
+    x, dy = _ins(ctx, op)
+    (dx,) = _outs(ctx, op)
+    _L()("bf_relu_bwd", x.ptr, dy.ptr, dx.ptr, x.numel, ctx.stream)
+
+
+def _flatten_fwd(ctx, op):
+    (src,) = _names(ctx, op.inputs)
+    (dst,) = _names(ctx, op.outputs)
+    if not ctx.store.is_alias_of(dst, src):
+        ctx.store.alias(dst, src, ctx.graph.tensors[op.outputs[0]].shape)
+
+
+def _flatten_bwd(ctx, op):
+    _x, dy = _names(ctx, op.inputs)
+    (dst,) = _names(ctx, op.outputs)
+    if not ctx.store.is_alias_of(dst, dy):
+        ctx.store.alias(dst, dy, ctx.graph.tensors[op.outputs[0]].shape)
+
+
+def _softmax_xent(ctx, op):
+    logits, labels = _ins(ctx, op)
+    loss, dlogits = _outs(ctx, op)
+    n, k = logits.shape
+    _L()("bf_softmax_xent", logits.ptr, labels.ptr, loss.ptr, dlogits.ptr, n, k,
+         ctx.workspace.data_ptr(), ctx.stream)
+
+
+def _sgd_update(ctx, op):
+    w, g = _ins(ctx, op)
+    (out,) = _outs(ctx, op)
+    _L()("bf_sgd_update", w.ptr, g.ptr, out.ptr, float(op.attrs["lr"]), w.numel, ctx.stream)
+
+
+def _sgd_momentum(ctx, op):
+    w, g, v = _ins(ctx, op)
+    w_new, v_new = _outs(ctx, op)
+    _L()("bf_sgd_momentum", w.ptr, g.ptr, v.ptr, w_new.ptr, v_new.ptr, float(op.attrs["lr"]),
+         float(op.attrs.get("momentum", 0.0)), w.numel, ctx.stream)
+
+
+def _aggregate(ctx, op):
+    parts = _ins(ctx, op)
+    (out,) = _outs(ctx, op)
+    mode = op.attrs.get("mode", "mean")
+    if mode not in ("sum", "mean"):
+        raise KernelError(f"aggregate: unknown mode {mode!r}")
+    if len(parts) > 32:
+        raise KernelError("aggregate: at most 32 inputs per operator")
+    arr = _native.ptr_array([p.ptr for p in parts])
+    _L()("bf_aggregate", arr, len(parts), out.ptr, out.numel, int(mode == "mean"), ctx.stream)
+
+
+def _copy(ctx, op):
+    (src,) = _ins(ctx, op)
+    (dst,) = _outs(ctx, op)
+    sv = ctx.graph.tensors[op.inputs[0]]
+    dv = ctx.graph.tensors[op.outputs[0]]
+    if ctx.copy_latency_s > 0 and sv.location != dv.location:
+        _L()("bf_delay_ns", int(ctx.copy_latency_s * 1e9), ctx.stream)
+    sd = src.data.device.index or 0
+    dd = dst.data.device.index or 0
+    _L()("bf_copy", dst.ptr, dd, src.ptr, sd, src.numel, ctx.stream)
+
+
+def _gate(ctx, op):
+    (src, _token) = _ins(ctx, op)
+    (dst,) = _outs(ctx, op)
+    d = src.data.device.index or 0
+    _L()("bf_copy", dst.ptr, d, src.ptr, d, src.numel, ctx.stream)
+
+
+def _swap(ctx, op):
+    a, b = _names(ctx, op.outputs)
+    ctx.store.swap(a, b)
+
+
+def _no_transport(ctx, op):
+    raise KernelError(f"{op.kind} {op.name!r}: no transport attached to this run "
+                      "(multi-host transport is out of scope; use the NCCL exchange)")
+
+
+# ---------------------------------------------------------------------------
+# pooling / LRN / concat (extension kinds)
+
+
+def _maxpool_fwd(ctx, op):
+    (x,) = _ins(ctx, op)
+    y, mask = _outs(ctx, op)
+    k, s, p = pool_attrs(op.attrs)
+    n, c, h, w = x.shape
+    _L()("bf_maxpool_fwd", x.ptr, y.ptr, mask.ptr, n, c, h, w, y.shape[2], y.shape[3], k, s, p,
+         ctx.stream)
+
+
+def _maxpool_bwd(ctx, op):
+    x, mask, dy = _ins(ctx, op)
+    (dx,) = _outs(ctx, op)
+    k, s, p = pool_attrs(op.attrs)
+    n, c, h, w = x.shape
+    _L()("bf_maxpool_bwd", mask.ptr, dy.ptr, dx.ptr, n, c, h, w, dy.shape[2], dy.shape[3], k, s,
+         p, ctx.stream)
+
+
+def _avgpool_fwd(ctx, op):
+    (x,) = _ins(ctx, op)
+    (y,) = _outs(ctx, op)
+    k, s, p = pool_attrs(op.attrs)
+    n, c, h, w = x.shape
+    _L()("bf_avgpool_fwd", x.ptr, y.ptr, n, c, h, w, y.shape[2], y.shape[3], k, s, p, ctx.stream)
+
+
+def _avgpool_bwd(ctx, op):
+    x, dy = _ins(ctx, op)
+    (dx,) = _outs(ctx, op)
+    k, s, p = pool_attrs(op.attrs)
+    n, c, h, w = x.shape
+    _L()("bf_avgpool_bwd", dy.ptr, dx.ptr, n, c, h, w, dy.shape[2], dy.shape[3], k, s, p,
+         ctx.stream)
+
+
+def _lrn_fwd(ctx, op):
+    (x,) = _ins(ctx, op)
+    y, scale = _outs(ctx, op)
+    size, alpha, beta, k = lrn_attrs(op.attrs)
+    _L()("bf_lrn_fwd", x.ptr, y.ptr, scale.ptr, *x.shape, size, alpha, beta, k, ctx.stream)
+
+
+def _lrn_bwd(ctx, op):
+    x, y, scale, dy = _ins(ctx, op)
+    (dx,) = _outs(ctx, op)
+    size, alpha, beta, k = lrn_attrs(op.attrs)
+    _L()("bf_lrn_bwd", x.ptr, y.ptr, scale.ptr, dy.ptr, dx.ptr, *x.shape, size, alpha, beta, k,
+         ctx.stream)
+
+
+def _concat_fwd(ctx, op):
+    parts = _ins(ctx, op)
+    (y,) = _outs(ctx, op)
+    n, _, h, w = y.shape
+    _L()("bf_concat_fwd", _native.ptr_array([p.ptr for p in parts]),
+         _native.int_array([p.shape[1] for p in parts]), len(parts), y.ptr, n, h, w, ctx.stream)
+
+
+def _concat_bwd(ctx, op):
+    (dy,) = _ins(ctx, op)
+    parts = _outs(ctx, op)
+    n, _, h, w = dy.shape
+    _L()("bf_concat_bwd", dy.ptr, _native.ptr_array([p.ptr for p in parts]),
+         _native.int_array([p.shape[1] for p in parts]), len(parts), n, h, w, ctx.stream)
+
+
+EXECUTORS = {
+    "fc_forward": _fc_fwd,
+    "fc_backward": _fc_bwd,
+    "fc_backward_data": _fc_bwd_data,
+    "fc_backward_weight": _fc_bwd_weight,
+    "fc_backward_bias": _fc_bwd_bias,
+    "conv2d_forward": _conv_fwd,
+    "conv2d_backward": _conv_bwd,
+    "conv2d_backward_data": _conv_bwd_data,
+    "conv2d_backward_weight": _conv_bwd_weight,
+    "conv2d_backward_bias": _conv_bwd_bias,
+    "relu_forward": _relu_fwd,
+    "relu_backward": _relu_bwd,
+    "flatten_forward": _flatten_fwd,
+    "flatten_backward": _flatten_bwd,
+    "softmax_xent": _softmax_xent,
+    "sgd_update": _sgd_update,
+    "sgd_momentum": _sgd_momentum,
+    "aggregate": _aggregate,
+    "copy": _copy,
+    "gate": _gate,
+    "swap": _swap,
+    "send": _no_transport,
+    "recv": _no_transport,
+    "maxpool_forward": _maxpool_fwd,
+    "maxpool_backward": _maxpool_bwd,
+    "avgpool_forward": _avgpool_fwd,
+    "avgpool_backward": _avgpool_bwd,
+    "lrn_forward": _lrn_fwd,
+    "lrn_backward": _lrn_bwd,
+    "concat_forward": _concat_fwd,
+    "concat_backward": _concat_bwd,
+}
+
+# kinds that launch nothing (host-side handle work only)
+HOST_ONLY = frozenset({"swap", "flatten_forward", "flatten_backward"})
+# kinds whose outputs alias an input buffer instead of owning storage
+ALIASING = {"flatten_forward": 0, "flatten_backward": 1}

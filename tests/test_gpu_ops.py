@@ -1,0 +1,207 @@
+"""Per-operator parity of the sm_100a kernels with the CPU oracle, through the
+product boundary.  Bit-exact for the integer/elementwise/pooling kinds,
+rel 1e-4 / abs 1e-5 (the NS tolerance) for the contractions."""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from gpu_util import ATOL, RTOL, assert_bitwise, assert_close, run_op
+
+pytestmark = pytest.mark.gpu
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32)
+
+
+RNG = np.random.default_rng(1234)
+
+
+def rnd(*shape, scale=1.0):
+    return f32(RNG.standard_normal(shape) * scale)
+
+
+# ---------------------------------------------------------------------------
+# contractions
+
+
+CONV_CASES = [
+    # (N, C, H, W, K, R, stride, pad, floor)
+    (2, 3, 9, 9, 4, 3, 1, 1, False),
+    (2, 5, 8, 8, 6, 1, 1, 0, False),
+    (1, 2, 11, 11, 3, 5, 2, 2, False),
+    (3, 4, 7, 7, 5, 5, 1, 2, False),
+    (2, 3, 32, 32, 32, 5, 1, 2, False),          # config 1
+    (2, 3, 224, 224, 64, 7, 2, 3, True),          # GoogLeNet conv1 (floor mode)
+    (2, 64, 56, 56, 192, 3, 1, 1, False),         # GoogLeNet conv2/3x3
+    (2, 192, 28, 28, 64, 1, 1, 0, False),         # inception 3a 1x1
+    (2, 16, 28, 28, 32, 5, 1, 2, False),          # inception 3a 5x5
+    (2, 832, 7, 7, 384, 1, 1, 0, False),          # inception 5b 1x1
+    (2, 160, 7, 7, 320, 3, 1, 1, False),          # inception 5a 3x3
+    (1, 3, 224, 224, 96, 11, 4, 0, True),         # NIN conv1
+    (2, 3, 13, 13, 8, 3, 2, 1, False),            # strided dgrad
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES, ids=lambda c: "x".join(map(str, c[:7])))
+def test_conv_forward_backward(case):
+    n, c, h, w, k, r, s, p, fl = case
+    x = rnd(n, c, h, w)
+    wt = rnd(k, c, r, r, scale=1.0 / np.sqrt(c * r * r))
+    b = rnd(k)
+    attrs = {"stride": s, "pad": p}
+    if fl:
+        attrs["floor"] = True
+    y_ref = O.conv2d_forward(x, wt, b, s, p, fl)
+    got = run_op("conv2d_forward", {"x": x, "w": wt, "b": b}, {"y": y_ref.shape}, attrs)["y"]
+    assert_close(got, y_ref, what="conv fwd")
+    dy = rnd(*y_ref.shape)
+    dx_ref, dw_ref, db_ref = O.conv2d_backward(x, wt, dy, s, p, fl)
+    outs = run_op("conv2d_backward", {"x": x, "w": wt, "dy": dy},
+                  {"dx": x.shape, "dw": wt.shape, "db": (k,)}, attrs)
+    assert_close(outs["dx"], dx_ref, what="conv dgrad")
+    assert_close(outs["dw"], dw_ref, rtol=RTOL, atol=ATOL * max(1.0, np.abs(dw_ref).max()),
+                 what="conv wgrad")
+    assert_close(outs["db"], db_ref, rtol=RTOL, atol=ATOL * max(1.0, np.abs(db_ref).max()),
+                 what="conv bgrad")
+
+
+@pytest.mark.parametrize("n,d,m", [(16, 32768, 10), (128, 1024, 1000), (6, 20, 7), (3, 5, 2)])
+def test_fc_forward_backward(n, d, m):
+    x, w, b, dy = rnd(n, d), rnd(d, m, scale=1 / np.sqrt(d)), rnd(m), rnd(n, m)
+    assert_close(run_op("fc_forward", {"x": x, "w": w, "b": b}, {"y": (n, m)})["y"],
+                 O.fc_forward(x, w, b), what="fc fwd")
+    dx, dw, db = O.fc_backward(x, w, dy)
+    out = run_op("fc_backward", {"x": x, "w": w, "dy": dy},
+                 {"dx": (n, d), "dw": (d, m), "db": (m,)})
+    assert_close(out["dx"], dx, what="fc dgrad")
+    assert_close(out["dw"], dw, what="fc wgrad")
+    assert_close(out["db"], db, what="fc bgrad")
+
+
+def test_reference_golden_vectors_on_gpu(golden_ops):
+    g = golden_ops
+    y = run_op("fc_forward", {"x": g["fc_x"], "w": g["fc_w"], "b": g["fc_b"]}, {"y": g["fc_y"].shape})
+    assert_close(y["y"], g["fc_y"])
+    for tag in ("c1", "c2", "c3", "c4"):
+        s, p = (int(v) for v in g[f"{tag}_geom"])
+        out = run_op("conv2d_forward", {"x": g[f"{tag}_x"], "w": g[f"{tag}_w"], "b": g[f"{tag}_b"]},
+                     {"y": g[f"{tag}_y"].shape}, {"stride": s, "pad": p})
+        assert_close(out["y"], g[f"{tag}_y"], what=tag)
+
+
+# ---------------------------------------------------------------------------
+# elementwise / pooling / normalisation: bit-exact
+
+
+def test_relu_bitwise(golden_ops):
+    x = golden_ops["relu_x"]
+    assert_bitwise(run_op("relu_forward", {"x": x}, {"y": x.shape})["y"], golden_ops["relu_y"])
+    x = rnd(3, 7, 5, 5)
+    x[0, 0, 0, :3] = [0.0, -0.0, 1e-38]
+    dy = rnd(3, 7, 5, 5)
+    assert_bitwise(run_op("relu_forward", {"x": x}, {"y": x.shape})["y"], O.relu_forward(x))
+    assert_bitwise(run_op("relu_backward", {"x": x, "dy": dy}, {"dx": x.shape})["dx"],
+                   O.relu_backward(x, dy))
+
+
+def test_sgd_momentum_aggregate_bitwise(golden_ops):
+    g = golden_ops
+    out = run_op("sgd_update", {"w": g["sgd_w"], "g": g["sgd_g"]}, {"o": g["sgd_w"].shape},
+                 {"lr": 0.0123})["o"]
+    assert_bitwise(out, g["sgd_out"])
+    parts = {f"p{i}": g[f"agg_p{i}"] for i in range(3)}
+    assert_bitwise(run_op("aggregate", parts, {"o": (777,)}, {"mode": "mean"})["o"], g["agg_mean"])
+    assert_bitwise(run_op("aggregate", parts, {"o": (777,)}, {"mode": "sum"})["o"], g["agg_sum"])
+    w, gg, v = rnd(1003), rnd(1003), rnd(1003)
+    for mu in (0.0, 0.9):
+        out = run_op("sgd_momentum", {"w": w, "g": gg, "v": v}, {"wn": w.shape, "vn": w.shape},
+                     {"lr": 0.01, "momentum": mu})
+        wn, vn = O.sgd_momentum(w, gg, v, 0.01, mu)
+        assert_bitwise(out["wn"], wn)
+        assert_bitwise(out["vn"], vn)
+
+
+@pytest.mark.parametrize("shape,k,s,p", [((2, 3, 9, 9), 3, 2, 0), ((2, 64, 112, 112), 3, 2, 0),
+                                         ((2, 192, 28, 28), 3, 1, 1), ((2, 832, 14, 14), 3, 2, 0),
+                                         ((2, 4, 8, 8), 2, 2, 0), ((1, 96, 54, 54), 3, 2, 0)])
+def test_maxpool_bitwise(shape, k, s, p):
+    x = rnd(*shape)
+    x[:, :, ::3, ::3] = 0.5  # plenty of ties
+    y, m = O.maxpool_forward(x, k, s, p)
+    out = run_op("maxpool_forward", {"x": x}, {"y": y.shape, "m": y.shape},
+                 {"kernel": k, "stride": s, "pad": p})
+    assert_bitwise(out["y"], y, "maxpool y")
+    assert_bitwise(out["m"], m, "maxpool argmax")
+    dy = rnd(*y.shape)
+    dx = run_op("maxpool_backward", {"x": x, "m": m, "dy": dy}, {"dx": x.shape},
+                {"kernel": k, "stride": s, "pad": p})["dx"]
+    assert_bitwise(dx, O.maxpool_backward(x, m, dy), "maxpool dx")
+
+
+@pytest.mark.parametrize("shape,k,s,p", [((2, 1024, 7, 7), 7, 1, 0), ((2, 5, 9, 9), 3, 2, 1),
+                                         ((2, 1000, 6, 6), 6, 1, 0)])
+def test_avgpool_bitwise(shape, k, s, p):
+    x = rnd(*shape)
+    y = O.avgpool_forward(x, k, s, p)
+    got = run_op("avgpool_forward", {"x": x}, {"y": y.shape}, {"kernel": k, "stride": s, "pad": p})
+    assert_bitwise(got["y"], y)
+    dy = rnd(*y.shape)
+    dx = run_op("avgpool_backward", {"x": x, "dy": dy}, {"dx": x.shape},
+                {"kernel": k, "stride": s, "pad": p})["dx"]
+    assert_bitwise(dx, O.avgpool_backward(x, dy, k, s, p))
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 56, 56), (2, 7, 5, 5)])
+def test_lrn(shape):
+    x = rnd(*shape, scale=3.0)
+    y, sc = O.lrn_forward(x)
+    out = run_op("lrn_forward", {"x": x}, {"y": shape, "s": shape},
+                 {"size": 5, "alpha": 1e-4, "beta": 0.75, "k": 1.0})
+    assert_bitwise(out["s"], sc, "lrn scale")
+    assert_close(out["y"], y, rtol=1e-6, atol=1e-7, what="lrn y")
+    dy = rnd(*shape)
+    dx = run_op("lrn_backward", {"x": x, "y": y, "s": sc, "dy": dy}, {"dx": shape},
+                {"size": 5, "alpha": 1e-4, "beta": 0.75, "k": 1.0})["dx"]
+    assert_close(dx, O.lrn_backward(x, y, sc, dy), rtol=1e-5, atol=1e-6, what="lrn dx")
+
+
+def test_concat_bitwise():
+    parts = {f"p{i}": rnd(2, c, 7, 7) for i, c in enumerate((64, 128, 32, 32))}
+    y = O.concat_forward(list(parts.values()))
+    assert_bitwise(run_op("concat_forward", parts, {"y": y.shape})["y"], y)
+    back = run_op("concat_backward", {"dy": y}, {f"g{i}": p.shape for i, p in enumerate(parts.values())},
+                  {"channels": [64, 128, 32, 32]})
+    for i, p in enumerate(parts.values()):
+        assert_bitwise(back[f"g{i}"], p)
+
+
+def test_softmax_xent(golden_ops):
+    g = golden_ops
+    out = run_op("softmax_xent", {"l": g["sm_logits"], "y": g["sm_labels"]},
+                 {"loss": (1,), "d": g["sm_logits"].shape})
+    assert_close(out["loss"], g["sm_loss"], rtol=1e-6, atol=1e-6)
+    assert_close(out["d"], g["sm_dlogits"], rtol=1e-5, atol=1e-7)
+    logits = rnd(128, 1000, scale=4.0)
+    labels = f32(RNG.integers(0, 1000, 128))
+    loss, d = O.softmax_xent(logits, labels)
+    out = run_op("softmax_xent", {"l": logits, "y": labels}, {"loss": (1,), "d": logits.shape})
+    assert_close(out["loss"], loss, rtol=1e-5)
+    assert_close(out["d"], d, rtol=1e-5, atol=1e-8)
+
+
+def test_flatten_is_zero_copy_alias():
+    from paper_1412_6249_b200 import BiGraph, Location, TensorStore, run
+
+    loc = Location("local", 0)
+    g = BiGraph()
+    a = g.add_tensor("a", (2, 3, 4, 4), loc)
+    f = g.add_tensor("f", (2, 48), loc)
+    g.add_operator("fl", "flatten_forward", [a], [f], loc)
+    st = TensorStore("cuda:0")
+    x = rnd(2, 3, 4, 4)
+    st.set("a", x)
+    run(g, st)
+    assert st.tensor("f").data_ptr() == st.tensor("a").data_ptr()
+    assert np.array_equal(st.array("f"), x.reshape(2, 48))

@@ -1,0 +1,108 @@
+"""Whole-iteration parity on the GPU: the product builders + CUDA-stream
+dispatcher + sm_100a kernels against the reference's own training results
+(golden fixtures) and, for the DAG nets, against the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from gpu_util import ATOL, RTOL, assert_close
+from paper_1412_6249_b200 import (Location, ParallelPlan, SyntheticFeed, TensorStore,
+                                  build_data_parallel, build_sgd_iteration, feeder, init_params,
+                                  run_sequence)
+from paper_1412_6249_b200.builders import LayerSpec, NetSpec
+from paper_1412_6249_b200.nets import cifar_convnet, conv_relu_fc, googlenet, nin
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan(n):
+    return ParallelPlan("data", peers=tuple(Location("local", k) for k in range(n)),
+                        server=Location("local", n))
+
+
+def _train(seq, net, feed, seed, iters, **kw):
+    store = TensorStore("cuda:0")
+    init_params(net, store, seed, seq.layout)
+    losses = []
+
+    def after(rep, st):
+        if rep.graph_index == 0:
+            losses.append([float(st.array(n)[0]) for n in seq.layout.loss_names])
+
+    reps = run_sequence(seq, store, before_iteration=feeder(feed, seq.layout), after_graph=after,
+                        iterations=iters, **kw)
+    return store, losses, reps
+
+
+def test_cfg1_matches_reference_training(golden_train, golden_graphs):
+    arrays, meta = golden_train
+    net = conv_relu_fc()
+    seq = build_sgd_iteration(net)
+    store, losses, reps = _train(seq, net, SyntheticFeed.for_net(net, 7, spread=0.0), 7, 2)
+    assert np.allclose(losses, meta["cfg1_losses"], rtol=RTOL)
+    for name in seq.layout.canonical_params:
+        assert_close(store.array(name), arrays[f"cfg1_{name}"], what=name)
+    # host dispatch order == reference serial-mode order, bit for bit
+    assert [reps[0].dispatch_order, reps[1].dispatch_order] == golden_graphs["cfg1"]["serial"]
+
+
+@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("lanes", [None, 1])
+def test_dp_mlp_matches_reference(golden_train, golden_graphs, split, lanes):
+    arrays, meta = golden_train
+    tag = f"mlp_dp2_{'split' if split else 'fused'}"
+    net = NetSpec((20,), (LayerSpec("fc", 16), LayerSpec("relu"), LayerSpec("fc", 4)), batch=8,
+                  lr=0.05)
+    seq = build_data_parallel(net, _plan(2), split_backward=split)
+    store, losses, reps = _train(seq, net, SyntheticFeed.for_net(net, 13, peers=2), 13, 3,
+                                 max_workers=lanes)
+    assert np.allclose(losses, meta[f"{tag}_losses"], rtol=RTOL, atol=ATOL)
+    for name in seq.layout.canonical_params:
+        assert_close(store.array(name), arrays[f"{tag}_{name}"], what=name)
+        for k in range(2):  # replicas stay bitwise identical to the server copy
+            assert np.array_equal(store.array(f"{name}_p{k}"), store.array(name))
+    assert [reps[0].dispatch_order, reps[1].dispatch_order] == golden_graphs[tag]["serial"]
+    if lanes == 1:  # serial mode: device order == dispatch order
+        assert [r.name for r in reps[0].trace] == golden_graphs[tag]["serial"][0]
+
+
+def test_cfg2_dp_matches_reference(golden_train, golden_graphs):
+    arrays, meta = golden_train
+    net = cifar_convnet(batch=16, lr=1e-3)
+    seq = build_data_parallel(net, _plan(2))
+    store, losses, reps = _train(seq, net, SyntheticFeed.for_net(net, 7, peers=2, spread=0.0), 7, 2)
+    assert np.allclose(losses, meta["cfg2_dp2_losses"], rtol=RTOL, atol=ATOL)
+    for name in seq.layout.canonical_params:
+        assert_close(store.array(name), arrays[f"cfg2_dp2_{name}"], what=name)
+    assert [reps[0].dispatch_order, reps[1].dispatch_order] == golden_graphs["cfg2_dp2"]["serial"]
+
+
+def _oracle_iteration(seq, net, feed, seed):
+    from oracle.serial import run_graph_serial
+
+    class _S(dict):
+        def set(self, name, arr):
+            self[name] = np.array(arr, dtype=np.float32, copy=True)
+
+    st = _S()
+    init_params(net, st, seed, seq.layout)
+    feeder(feed, seq.layout)(0, st)
+    order = run_graph_serial(seq.graphs[0], st)
+    return st, order
+
+
+@pytest.mark.parametrize("factory", [googlenet, nin])
+def test_dag_net_iteration_matches_oracle(factory):
+    """One training iteration at reduced batch: every parameter gradient and the
+    loss agree with the CPU oracle at the NS tolerance."""
+    net = factory(batch=2, lr=0.01)
+    seq = build_sgd_iteration(net)
+    feed = SyntheticFeed.for_net(net, 7, spread=0.0)
+    ref, order = _oracle_iteration(seq, net, feed, 7)
+    store, losses, reps = _train(seq, net, feed, 7, 1)
+    assert reps[0].dispatch_order == order
+    assert_close(store.array("loss"), ref["loss"], what="loss")
+    for pname, shape in net.param_shapes():
+        g = ref[f"d{pname}"]
+        scale = max(1.0, float(np.abs(g).max()))
+        assert_close(store.array(f"d{pname}"), g, rtol=RTOL, atol=ATOL * scale, what=f"d{pname}")
