@@ -358,14 +358,14 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
         try:
             with torch.cuda.stream(stream):
                 if trace:
-                    t_start = torch.cuda.Event(enable_timing=True)
+                    t_start = torch.cuda.Event(enable_timing=True, external=True)
                     t_start.record(stream)
                 delay = float(op.attrs.get("delay_s", 0.0) or 0.0)
                 if delay > 0:
                     _native.lib()("bf_delay_ns", int(delay * 1e9), ctx.stream)
                 spec.execute(ctx, op)
                 if trace:
-                    t_end = torch.cuda.Event(enable_timing=True)
+                    t_end = torch.cuda.Event(enable_timing=True, external=True)
                     t_end.record(stream)
                     timing.append((oid, t_start, t_end))
         except BaseException as exc:  # noqa: BLE001 - first error wins
