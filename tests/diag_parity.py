@@ -47,9 +47,19 @@ def main():
     init_params(net, store, 7, seq.layout)
     run_sequence(seq, store, before_iteration=feeder(feed, seq.layout), iterations=1)
 
-    loss64, g64 = dag_grads_fp64(net, params, x, labels)
+    acts = {}
+    loss64, g64 = dag_grads_fp64(net, params, x, labels, acts)
     print(f"loss fp64 {loss64:.8f} oracle {float(ref['loss'][0]):.8f} "
           f"gpu {float(store.array('loss')[0]):.8f}")
+    for i, nd in enumerate(net.nodes[:40]):
+        a = f"a{i + 1}"
+        t64, d64 = acts[a]
+        line = (f"{a:5s} {nd.kind:8s} {nd.name:28s} fwd gpu {rel(store.array(a), t64):8.2e} "
+                f"oracle {rel(ref[a], t64):8.2e}")
+        if d64 is not None and store.has("d" + a) and ("d" + a) in ref:
+            line += (f" | bwd gpu {rel(store.array('d' + a), d64):8.2e} "
+                     f"oracle {rel(ref['d' + a], d64):8.2e}")
+        print(line)
     worst_gpu = worst_orc = 0.0
     for p, _ in net.param_shapes():
         gg, go, gt = store.array(f"d{p}"), ref[f"d{p}"], g64[p]

@@ -17,8 +17,9 @@ def _pool_pad_ceil(nd):
     return dict(kernel_size=nd.kernel, stride=nd.stride, padding=nd.pad, ceil_mode=True)
 
 
-def dag_grads_fp64(net, params: dict, x: np.ndarray, labels: np.ndarray):
-    """Returns (loss, {param name: grad}) in float64."""
+def dag_grads_fp64(net, params: dict, x: np.ndarray, labels: np.ndarray, acts: dict | None = None):
+    """Returns (loss, {param name: grad}) in float64.  If ``acts`` is a dict it
+    receives ``a{pos}`` -> (activation, activation gradient)."""
     P = {k: torch.tensor(np.asarray(v, np.float64), requires_grad=True)
          for k, v in params.items()}
     vals = {"data": torch.tensor(np.asarray(x, np.float64))}
@@ -42,9 +43,15 @@ def dag_grads_fp64(net, params: dict, x: np.ndarray, labels: np.ndarray):
             y = torch.cat(src, dim=1)
         else:
             raise ValueError(nd.kind)
+        if acts is not None:
+            y.retain_grad()
         vals[nd.name] = y
     logits = vals[net.nodes[-1].name]
     logits = logits.reshape(logits.shape[0], -1)
     loss = F.cross_entropy(logits, torch.tensor(np.asarray(labels).astype(np.int64)))
     loss.backward()
-    return float(loss), {k: v.grad.numpy() for k, v in P.items()}
+    if acts is not None:
+        for i, nd in enumerate(net.nodes):
+            t = vals[nd.name]
+            acts[f"a{i + 1}"] = (t.detach().numpy(), None if t.grad is None else t.grad.numpy())
+    return float(loss.detach()), {k: v.grad.numpy() for k, v in P.items()}
