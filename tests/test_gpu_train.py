@@ -91,18 +91,58 @@ def _oracle_iteration(seq, net, feed, seed):
     return st, order
 
 
+def _teacher_forced_check(seq, store, skip=()):
+    """Every operator of the training graph, re-run by the oracle on the GPU's
+    own input tensors, reproduces the GPU's output tensors.
+
+    Comparing a whole deep iteration end to end is chaotic: a pre-activation
+    within ~1e-7 of zero flips a ReLU (or a near-tie flips a max-pool argmax)
+    differently in any two float32 implementations, and the gradient routed
+    through that element differs by O(1).  Measured against a float64 ground
+    truth (tests/diag_parity.py) both the oracle and the GPU show such flips.
+    Checking each operator on identical inputs removes the chaos and tests
+    every kernel at every real shape and data distribution of the net."""
+    import oracle
+
+    g = seq.graphs[0]
+    checked = 0
+    for oid in g.insertion_order:
+        op = g.operators[oid]
+        if op.kind in skip or op.kind == "copy":
+            continue
+        ins = [store.array(g.tensors[t].name) for t in op.inputs]
+        want = oracle.KERNELS[op.kind](ins, dict(op.attrs))
+        for t, w in zip(op.outputs, want):
+            name = g.tensors[t].name
+            got = store.array(name)
+            if op.kind in ("relu_forward", "relu_backward", "maxpool_forward", "maxpool_backward",
+                           "avgpool_forward", "avgpool_backward", "concat_forward",
+                           "concat_backward", "flatten_forward", "flatten_backward",
+                           "sgd_update", "aggregate"):
+                assert np.array_equal(got, w), f"{op.name} -> {name} not bit-exact"
+            else:
+                scale = max(1.0, float(np.abs(w).max()))
+                assert_close(got, w, rtol=RTOL, atol=ATOL * scale, what=f"{op.name} -> {name}")
+            checked += 1
+    return checked
+
+
 @pytest.mark.parametrize("factory", [googlenet, nin])
 def test_dag_net_iteration_matches_oracle(factory):
-    """One training iteration at reduced batch: every parameter gradient and the
-    loss agree with the CPU oracle at the NS tolerance."""
+    """One GoogLeNet / NIN training iteration at batch 2: host dispatch order ==
+    the oracle's serial order, the loss agrees at the NS tolerance, and every
+    operator reproduces the oracle on its own inputs (teacher-forced)."""
     net = factory(batch=2, lr=0.01)
     seq = build_sgd_iteration(net)
     feed = SyntheticFeed.for_net(net, 7, spread=0.0)
     ref, order = _oracle_iteration(seq, net, feed, 7)
-    store, losses, reps = _train(seq, net, feed, 7, 1)
-    assert reps[0].dispatch_order == order
-    assert_close(store.array("loss"), ref["loss"], what="loss")
-    for pname, shape in net.param_shapes():
-        g = ref[f"d{pname}"]
-        scale = max(1.0, float(np.abs(g).max()))
-        assert_close(store.array(f"d{pname}"), g, rtol=RTOL, atol=ATOL * scale, what=f"d{pname}")
+    store = TensorStore("cuda:0")
+    init_params(net, store, 7, seq.layout)
+    feeder(feed, seq.layout)(0, store)
+    from paper_1412_6249_b200 import run
+
+    rep = run(seq.graphs[0], store)
+    assert rep.dispatch_order == order
+    assert_close(store.array("loss"), ref["loss"], rtol=1e-5, atol=1e-5, what="loss")
+    n = _teacher_forced_check(seq, store)
+    assert n >= len(seq.graphs[0].operators) - 5
