@@ -228,14 +228,9 @@ def run_ours(args):
 
     net = (googlenet if args.net == "googlenet" else nin)(batch=args.batch, lr=0.01)
     store = TensorStore(dev)
-    if world > 1:
-        from paper_1412_6249_b200.exchange import build_rank_sequence
+    from paper_1412_6249_b200.exchange import build_rank_sequence
 
-        seq, exch = build_rank_sequence(net, world, rank, store)
-    else:
-        plan = ParallelPlan("data", peers=(Location("local", 0),), server=Location("local", 0))
-        seq = build_data_parallel(net, plan)
-        exch = None
+    seq, exch = build_rank_sequence(net, world, rank, store)
     layout = seq.layout
     init_params(net, store, 7, layout)
     feed = SyntheticFeed.for_net(net, 7, peers=world, spread=0.0)

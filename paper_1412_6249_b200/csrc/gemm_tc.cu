@@ -3,12 +3,12 @@
 //   D[m][n] = sum_k A(m,k) B(n,k)          (gemm_common.cuh explains the mapping
 //                                           of conv fwd/dgrad/wgrad and fc onto it)
 //
-// Each fp32 operand x is split into big = x with the low 13 mantissa bits
-// cleared (exactly representable in TF32) and small = x - big (exact in fp32);
-// the tensor core accumulates big*big + big*small + small*big into an fp32 TMEM
-// accumulator.  The dropped small*small term is < 2^-22 relative, so the result
-// is within fp32 rounding of an fp32 GEMM (SURVEY.md finding 7: 1xTF32 misses
-// the 1e-4 contract at GoogLeNet shapes, 3xTF32 passes).
+// Each fp32 operand x is split into big = TF32 round-to-nearest of x and
+// small = TF32(x - big); the tensor core accumulates big*big + big*small +
+// small*big into an fp32 TMEM accumulator.  The dropped small*small term and
+// the rounding of small are ~2^-22 relative, so the result is within a few
+// fp32 ulps of an fp32 GEMM (SURVEY.md finding 7: 1xTF32 misses the 1e-4
+// contract at GoogLeNet shapes, 3xTF32 passes).
 //
 // CTA = 8 producer warps + 1 MMA warp.  Producers gather the operand tiles
 // straight from the NCHW tensors (implicit GEMM: no materialised im2col),
@@ -246,9 +246,17 @@ __host__ __device__ constexpr uint32_t tf32_idesc(int bn) {
          ((uint32_t)(BM >> 4) << 24);
 }
 
+__device__ __forceinline__ float to_tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// big = round-to-nearest TF32 of x; small = TF32(x - big), |small| <= 2^-11 |x|;
+// big*big + big*small + small*big then misses x*y by at most ~2^-21 |x y|
 __device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
-  big = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  small = x - big;
+  big = to_tf32_rna(x);
+  small = to_tf32_rna(x - big);
 }
 
 // byte offset of 16B chunk `c` of row `r` in a 128B-swizzled tile

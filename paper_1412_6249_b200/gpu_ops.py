@@ -234,6 +234,34 @@ def _no_transport(ctx, op):
                       "(multi-host transport is out of scope; use the NCCL exchange)")
 
 
+def _dp_exchange(ctx, op):
+    """Lowered parameter-server subgraph for one gradient bucket (exchange.py)."""
+    from .exchange import check_bucket
+
+    ins = _ins(ctx, op)
+    outs = _outs(ctx, op)
+    n = len(outs)
+    w0, g0, o0 = check_bucket(ins[:n], ins[n:], outs, op.attrs["offsets"])
+    length = int(op.attrs["flat_len"])
+    world = int(op.attrs["world"])
+    lr = float(op.attrs["lr"])
+    lib = _L()
+    if world == 1:
+        lib("bf_sgd_mean_update", w0, g0, o0, lr, 1, length, ctx.stream)
+        return
+    comm = getattr(ctx.store, "_nccl", None)
+    if comm is None:
+        raise KernelError("dp_exchange: no NCCL communicator on this store "
+                          "(exchange.setup_nccl)")
+    from .exchange import shard_of
+
+    shard, first = shard_of(length, world, int(op.attrs["rank"]))
+    off = first * 4
+    lib("bf_nccl_reduce_scatter", comm, g0, g0 + off, shard, ctx.stream)
+    lib("bf_sgd_mean_update", w0 + off, g0 + off, o0 + off, lr, world, shard, ctx.stream)
+    lib("bf_nccl_all_gather", comm, o0 + off, o0, shard, ctx.stream)
+
+
 # ---------------------------------------------------------------------------
 # pooling / LRN / concat (extension kinds)
 
@@ -336,6 +364,7 @@ EXECUTORS = {
     "lrn_backward": _lrn_bwd,
     "concat_forward": _concat_fwd,
     "concat_backward": _concat_bwd,
+    "dp_exchange": _dp_exchange,
 }
 
 # kinds that launch nothing (host-side handle work only)

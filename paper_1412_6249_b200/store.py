@@ -179,6 +179,21 @@ class TensorStore:
         self._alias_of[name] = src
         return cur
 
+    def place(self, name: str, view: torch.Tensor) -> Tensor:
+        """Bind ``name`` to a caller-laid-out view (e.g. a slice of a flat
+        parameter/gradient arena).  Existing contents are copied in."""
+        shape = check_shape(tuple(int(d) for d in view.shape))
+        cur = self._tensors.get(name)
+        if cur is not None:
+            if cur.shape != shape:
+                raise KernelError(f"store: shape mismatch placing {name!r}")
+            view.copy_(cur.data)
+            cur.data = view
+            return cur
+        t = Tensor(shape, view)
+        self._tensors[name] = t
+        return t
+
     def is_alias_of(self, name: str, src: str) -> bool:
         if self._alias_of.get(name) != src or name not in self._tensors or src not in self._tensors:
             return False

@@ -77,6 +77,43 @@ def test_cfg2_dp_matches_reference(golden_train, golden_graphs):
     assert [reps[0].dispatch_order, reps[1].dispatch_order] == golden_graphs["cfg2_dp2"]["serial"]
 
 
+@pytest.mark.parametrize("factory,iters", [(cifar_convnet, 3), (googlenet, 1)])
+def test_lowered_exchange_world1_is_bitwise_the_server_graph(factory, iters):
+    """exchange.py at world=1 (flat arenas, fused mean+SGD per bucket) reproduces
+    the reference-shaped parameter-server graph (copies, aggregate, sgd_update)
+    bit for bit, also when replayed from captured CUDA graphs."""
+    from paper_1412_6249_b200.exchange import build_rank_sequence
+    from paper_1412_6249_b200.executor import CapturedSequence
+
+    net = factory(batch=2, lr=0.01)
+    feed = SyntheticFeed.for_net(net, 7, spread=0.0)
+    full = build_data_parallel(net, _plan(1))
+    st_full, _, _ = _train(full, net, feed, 7, iters, trace=False)
+    st_low = TensorStore("cuda:0")
+    seq, plan = build_rank_sequence(net, 1, 0, st_low, bucket_bytes=256 << 10)
+    init_params(net, st_low, 7, seq.layout)
+    run_sequence(seq, st_low, before_iteration=feeder(feed, seq.layout), iterations=iters,
+                 trace=False)
+    for pname, _ in net.param_shapes():
+        assert np.array_equal(st_low.array(f"{pname}_p0"), st_full.array(pname)), pname
+    # captured replay of the lowered sequence continues bit-identically
+    st_cap = TensorStore("cuda:0")
+    seq2, _ = build_rank_sequence(net, 1, 0, st_cap, bucket_bytes=256 << 10)
+    init_params(net, st_cap, 7, seq2.layout)
+    feeder(feed, seq2.layout)(0, st_cap)
+    exe = CapturedSequence(seq2, st_cap)
+    exe.prepare()  # one eager iteration
+    st_ref = TensorStore("cuda:0")
+    seq3, _ = build_rank_sequence(net, 1, 0, st_ref, bucket_bytes=256 << 10)
+    init_params(net, st_ref, 7, seq3.layout)
+    fix = feeder(feed, seq3.layout)
+    run_sequence(seq3, st_ref, before_iteration=lambda it, s: fix(0, s), iterations=4, trace=False)
+    for _ in range(3):
+        exe.step()
+    for pname, _ in net.param_shapes():
+        assert np.array_equal(st_cap.array(f"{pname}_p0"), st_ref.array(f"{pname}_p0")), pname
+
+
 def _oracle_iteration(seq, net, feed, seed):
     from oracle.serial import run_graph_serial
 
