@@ -180,6 +180,6 @@ def test_dag_net_iteration_matches_oracle(factory):
 
     rep = run(seq.graphs[0], store)
     assert rep.dispatch_order == order
-    assert_close(store.array("loss"), ref["loss"], rtol=1e-5, atol=1e-5, what="loss")
+    assert_close(store.array("loss"), ref["loss"], rtol=RTOL, atol=ATOL, what="loss")
     n = _teacher_forced_check(seq, store)
     assert n >= len(seq.graphs[0].operators) - 5
