@@ -264,6 +264,54 @@ __device__ __forceinline__ uint32_t sw_off(int r, int c) {
   return (uint32_t)(r * 128 + (((c ^ r) & 7) << 4));
 }
 
+// (row, 16B chunk) handled by producer thread t for its e-th chunk of an R-row tile
+template <bool kMContig, int E, int R>
+__device__ __forceinline__ void chunk_of(int t, int e, int& r, int& c) {
+  if (kMContig) {  // consecutive lanes -> consecutive rows (pixel-contiguous operands)
+    r = t % R;
+    c = (t / R) * E + e;
+  } else {         // 8 lanes per row -> 128 contiguous bytes along K
+    c = t & 7;
+    r = (t >> 3) + 32 * e;
+  }
+}
+
+template <bool kMContig, int E, int R>
+__device__ __forceinline__ void gather(int t, const float* __restrict__ p, const RowInfo* rows,
+                                       const RowInfo* ks, unsigned hb, unsigned wb,
+                                       float (&v)[E][4]) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    int r, c;
+    chunk_of<kMContig, E, R>(t, e, r, c);
+    const RowInfo ri = rows[r];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const RowInfo ki = ks[c * 4 + j];
+      bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
+      v[e][j] = ok ? __ldg(p + (ri.off + ki.off)) : 0.f;
+    }
+  }
+}
+
+template <bool kMContig, int E, int R>
+__device__ __forceinline__ void store_split(int t, const float (&v)[E][4], uint8_t* big,
+                                            uint8_t* small) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    int r, c;
+    chunk_of<kMContig, E, R>(t, e, r, c);
+    float4 bg, sm;
+    split_tf32(v[e][0], bg.x, sm.x);
+    split_tf32(v[e][1], bg.y, sm.y);
+    split_tf32(v[e][2], bg.z, sm.z);
+    split_tf32(v[e][3], bg.w, sm.w);
+    const uint32_t off = sw_off(r, c);
+    *reinterpret_cast<float4*>(big + off) = bg;
+    *reinterpret_cast<float4*>(small + off) = sm;
+  }
+}
+
 template <int BN, int STAGES>
 struct Smem {
   static constexpr int kA = BM * BK * 4;  // bytes of one A tile (big or small)
@@ -358,41 +406,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint8_t* b_big = st + 2 * L::kA;
       uint8_t* b_small = st + 2 * L::kA + L::kB;
 
-      auto fill = [&](auto sep_tag, const float* p, const RowInfo* rows, const RowInfo* ks,
-                      unsigned hb, unsigned wb, int R, uint8_t* big, uint8_t* small) {
-        using S = decltype(sep_tag);
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int E = R * 8 / kProducers;  // 16B chunks per thread
-        for (int e = 0; e < E; ++e) {
-          int r, c;
-          if (S::kMContig) {
-            r = t % R;
-            c = (t / R) * E + e;
-          } else {
-            c = t & 7;
-            r = (t >> 3) + 32 * e;
-          }
-          const RowInfo ri = rows[r];
-          float v[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const RowInfo ki = ks[c * 4 + j];
-            bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
-            v[j] = ok ? __ldg(p + (ri.off + ki.off)) : 0.f;
-          }
-          float4 bg, sm;
-          split_tf32(v[0], bg.x, sm.x);
-          split_tf32(v[1], bg.y, sm.y);
-          split_tf32(v[2], bg.z, sm.z);
-          split_tf32(v[3], bg.w, sm.w);
-          uint32_t off = sw_off(r, c);
-          *reinterpret_cast<float4*>(big + off) = bg;
-          *reinterpret_cast<float4*>(small + off) = sm;
-        }
-      };
-      fill(SA{}, pa, rowA, kA, hbA, wbA, BM, a_big, a_small);
-      fill(SB{}, pb, rowB, kB, hbB, wbB, BN, b_big, b_small);
+      // all loads of both operands are issued before the first use so that
+      // ~(BM+BN)*BK/256 gathers per thread are in flight at once
+      constexpr int EA = BM * 8 / kProducers, EB = BN * 8 / kProducers;
+      float va[EA][4], vb[EB][4];
+      gather<SA::kMContig, EA, BM>(t, pa, rowA, kA, hbA, wbA, va);
+      gather<SB::kMContig, EB, BN>(t, pb, rowB, kB, hbB, wbB, vb);
+      store_split<SA::kMContig, EA, BM>(t, va, a_big, a_small);
+      store_split<SB::kMContig, EB, BN>(t, vb, b_big, b_small);
       fence_async_smem();
       mbar_arrive(&full[stage]);
     }
