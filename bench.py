@@ -63,8 +63,10 @@ def _tf32_peak(peaks):
     p = ROOT / "profiles" / "tf32_peak.json"
     if p.exists():
         try:
-            tf = json.loads(p.read_text())["tf32_tflops"]
-            return tf / 3.0, "measured cuBLAS TF32 (profiles/tf32_peak.json) / 3 passes"
+            rec = json.loads(p.read_text())
+            tf = rec.get("tf32_tflops_sustained") or rec["tf32_tflops"]
+            return tf / 3.0, ("measured cuBLAS TF32 sustained (profiles/tf32_peak.json) / 3 "
+                              "passes (kernels timed inside a long step)")
         except Exception:
             pass
     bf = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops") or 1398.2
