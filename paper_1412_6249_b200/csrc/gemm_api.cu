@@ -13,7 +13,7 @@ int g_gemm_engine = 0;
 template <class LA, class LB, class Epi>
 static int run_gemm(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
                     int64_t ws_bytes, cudaStream_t st, const char* what) {
-  if (g_gemm_engine == 0) {
+  if (g_gemm_engine == 0 || g_gemm_engine == 2) {
     int rc = tc_gemm(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
     if (rc >= 0) return rc;
   }
@@ -39,7 +39,8 @@ using namespace bf;
 extern "C" {
 
 int bf_set_gemm_engine(int engine) {
-  BF_REQUIRE(engine == 0 || engine == 1, "bf_set_gemm_engine: 0 (auto) or 1 (simt)");
+  BF_REQUIRE(engine >= 0 && engine <= 2,
+             "bf_set_gemm_engine: 0 (auto), 1 (simt), 2 (tcgen05 v1 only)");
   g_gemm_engine = engine;
   return 0;
 }
@@ -52,6 +53,11 @@ int bf_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int 
   LdFwdX la{x, g};
   LdRowK lb{w, (int64_t)C * R * S};
   EpiNCHW epi{y, b, P * Q, K};
+  if (g_gemm_engine == 0) {
+    int rc = tc2_conv_fwd(la, lb, N * P * Q, K, C * R * S, epi, ws, ws_bytes, as_stream(s),
+                          "conv2d_forward");
+    if (rc >= 0) return rc;
+  }
   return run_gemm(la, lb, N * P * Q, K, C * R * S, epi, ws, ws_bytes, as_stream(s),
                   "conv2d_forward");
 }
@@ -64,6 +70,11 @@ int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx, int N, int C,
   LdDgradDY la{dy, g};
   LdDgradW lb{w, g};
   EpiNCHW epi{dx, nullptr, H * W, C};
+  if (g_gemm_engine == 0) {
+    int rc = tc2_conv_dgrad(la, lb, N * H * W, C, K * R * S, epi, ws, ws_bytes, as_stream(s),
+                            "conv2d_backward_data");
+    if (rc >= 0) return rc;
+  }
   return run_gemm(la, lb, N * H * W, C, K * R * S, epi, ws, ws_bytes, as_stream(s),
                   "conv2d_backward_data");
 }

@@ -15,6 +15,13 @@ template <class LA, class LB, class Epi>
 int tc_gemm(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
             int64_t ws_bytes, cudaStream_t st, const char* what);
 
-extern int g_gemm_engine;  // 0 auto, 1 simt
+// tcgen05 engine v2 (gemm_tc2.cu): A in TMEM, pre-packed B via bulk TMA
+int tc2_conv_fwd(const LdFwdX& la, const LdRowK& lb, int M, int N, int K, const EpiNCHW& epi,
+                 float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+int tc2_conv_dgrad(const LdDgradDY& la, const LdDgradW& lb, int M, int N, int K,
+                   const EpiNCHW& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
+                   const char* what);
+
+extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only
 
 }  // namespace bf

@@ -1,0 +1,447 @@
+// tcgen05 implicit-GEMM engine v2 for conv forward / data-gradient (3xTF32).
+//
+// Why a second engine: in v1 both operands are gathered, split and stored to
+// shared memory by producer warps; ncu (profiles/r01_conv2_fwd_v1.md) shows
+// it issue-bound (IPC 1.5, tensor pipe 16%) and 3xTF32 needs
+// 2x operand writes + 3x operand reads of shared memory per k-step.  v2:
+//
+//  * A (the pixel-major im2col operand, gathered from NCHW) never touches
+//    shared memory: each producer thread owns one TMEM lane (= one output
+//    pixel), gathers its K slice, splits it into TF32 big/small in registers
+//    and writes both with tcgen05.st; the MMA reads A from TMEM
+//    (tcgen05.mma ... [a_tmem], b_desc).
+//  * B (the weights) is split and laid out ONCE per operator by a pack kernel
+//    into the exact 128B-swizzled K-major shared-memory image, per (n-tile,
+//    k-block); the GEMM fetches each stage with one cp.async.bulk (TMA) that
+//    completes on the stage's mbarrier.  Shared memory then carries only the
+//    B tile (1 write, 3 tensor-core reads per k-step).
+//  * N tile = the whole output-channel extent up to 256 (rounded to 32), so
+//    A is gathered once per output pixel tile.
+//
+// TMEM map (512 columns): [0, BN) fp32 accumulator; [256 + 64*s, +32) A_big
+// and [256 + 64*s + 32, +32) A_small of stage s (4 stages).
+#include <algorithm>
+
+#include "gemm_common.cuh"
+#include "gemm_engines.cuh"
+
+namespace bf {
+namespace tc2 {
+
+constexpr int BM = 128;
+constexpr int BK = 32;
+constexpr int STAGES = 4;
+constexpr int kProducerWarps = 8;
+constexpr int kProducers = kProducerWarps * 32;
+constexpr int kThreads = kProducers + 32;
+constexpr int kInvalid = -30000;
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kAColBase = 256;
+
+struct __align__(8) RowInfo {
+  int off;
+  short h, w;
+};
+
+// same separable loader views as engine v1 (gemm_tc.cu)
+template <class L>
+struct Sep;
+
+template <>
+struct Sep<LdFwdX> {
+  __device__ static RowInfo row(const LdFwdX& l, int m) {
+    const ConvShape& g = l.g;
+    int PQ = g.P * g.Q;
+    int n = m / PQ, pq = m - n * PQ;
+    int p = pq / g.Q, q = pq - p * g.Q;
+    int ih = p * g.stride - g.pad, iw = q * g.stride - g.pad;
+    return {n * g.C * g.H * g.W + ih * g.W + iw, (short)ih, (short)iw};
+  }
+  __device__ static RowInfo kin(const LdFwdX& l, int k) {
+    const ConvShape& g = l.g;
+    int RS = g.R * g.S;
+    int c = k / RS, rs = k - c * RS;
+    int r = rs / g.S, s = rs - r * g.S;
+    return {c * g.H * g.W + r * g.W + s, (short)r, (short)s};
+  }
+  __device__ static unsigned hb(const LdFwdX& l) { return (unsigned)l.g.H; }
+  __device__ static unsigned wb(const LdFwdX& l) { return (unsigned)l.g.W; }
+  __device__ static const float* ptr(const LdFwdX& l) { return l.x; }
+};
+
+template <>
+struct Sep<LdDgradDY> {  // stride 1
+  __device__ static RowInfo row(const LdDgradDY& l, int m) {
+    const ConvShape& g = l.g;
+    int HW = g.H * g.W;
+    int n = m / HW, hw = m - n * HW;
+    int h = hw / g.W, w = hw - h * g.W;
+    int th = h + g.pad, tw = w + g.pad;
+    return {n * g.K * g.P * g.Q + th * g.Q + tw, (short)th, (short)tw};
+  }
+  __device__ static RowInfo kin(const LdDgradDY& l, int k) {
+    const ConvShape& g = l.g;
+    int RS = g.R * g.S;
+    int ko = k / RS, rs = k - ko * RS;
+    int r = rs / g.S, s = rs - r * g.S;
+    return {ko * g.P * g.Q - r * g.Q - s, (short)-r, (short)-s};
+  }
+  __device__ static unsigned hb(const LdDgradDY& l) { return (unsigned)l.g.P; }
+  __device__ static unsigned wb(const LdDgradDY& l) { return (unsigned)l.g.Q; }
+  __device__ static const float* ptr(const LdDgradDY& l) { return l.dy; }
+};
+
+// ---- PTX helpers --------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem desc]
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t tf32_idesc(int bn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ float to_tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ uint32_t sw_off(int r, int c) {
+  return (uint32_t)(r * 128 + (((c ^ r) & 7) << 4));
+}
+
+// ---- B pre-pack: [n_tile][k_block][big BN x 128B | small BN x 128B], swizzled ----
+
+template <class LB>
+__global__ void pack_b_kernel(LB lb, int N, int K, int BN, int nkb, uint8_t* __restrict__ out) {
+  const int tile = blockIdx.y, kb = blockIdx.x;
+  uint8_t* base = out + ((size_t)tile * nkb + kb) * 2 * BN * 128;
+  const int chunks = BN * 8;
+  for (int i = threadIdx.x; i < chunks; i += blockDim.x) {
+    int r = i >> 3, c = i & 7;
+    int n = tile * BN + r;
+    float4 bg, sm;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int k = kb * BK + c * 4 + j;
+      v[j] = (n < N && k < K) ? lb(n, k) : 0.f;
+    }
+    bg.x = to_tf32_rna(v[0]); sm.x = to_tf32_rna(v[0] - bg.x);
+    bg.y = to_tf32_rna(v[1]); sm.y = to_tf32_rna(v[1] - bg.y);
+    bg.z = to_tf32_rna(v[2]); sm.z = to_tf32_rna(v[2] - bg.z);
+    bg.w = to_tf32_rna(v[3]); sm.w = to_tf32_rna(v[3] - bg.w);
+    uint32_t off = sw_off(r, c);
+    *reinterpret_cast<float4*>(base + off) = bg;
+    *reinterpret_cast<float4*>(base + BN * 128 + off) = sm;
+  }
+}
+
+// ---- main kernel ------------------------------------------------------------------
+
+template <class LA, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc2_kernel(LA la, int M, int N, int K, int BN, int nst, const uint8_t* __restrict__ bpack,
+               int nkb, int kb_per_split, Epi epi, EpiPartial part, int splits) {
+  using SA = Sep<LA>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int stage_bytes = 2 * BN * 128;
+  uint8_t* tiles = base;                                            // nst x stage_bytes
+  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + nst * stage_bytes);  // [STAGES][BK]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ktab + STAGES * BK);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+  const int ntile = blockIdx.y;
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nk = min(kb_per_split, nkb - kb0);
+
+  if (warp == kProducerWarps) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], kProducers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < kProducerWarps) {
+    // ============ producers: A gather -> TF32 split -> TMEM; thread 0 also issues B TMA ============
+    const int t = threadIdx.x;
+    const int q = warp & 3;            // TMEM lane quarter
+    const int kc0 = (warp >> 2) * 16;  // which 16 of the 32 k columns
+    const int row = q * 32 + lane;
+    const int m = m0 + row;
+    const RowInfo ri = m < M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+    const float* __restrict__ pa = SA::ptr(la);
+    const unsigned hb = SA::hb(la), wb = SA::wb(la);
+    const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
+    const uint8_t* bsrc = bpack + ((size_t)ntile * nkb) * stage_bytes;
+    for (int i = 0; i < nk; ++i) {
+      const int stage = i % nst;
+      const uint32_t phase = (i / nst) & 1;
+      const int kbase = (kb0 + i) * BK;
+      RowInfo* kt = ktab + stage * BK;
+      if (t < BK) {
+        int k = kbase + t;
+        kt[t] = k < K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+      }
+      named_sync(1, kProducers);
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const RowInfo ki = kt[kc0 + j];
+        bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
+        v[j] = ok ? __ldg(pa + (ri.off + ki.off)) : 0.f;
+      }
+      float big[16], small[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        big[j] = to_tf32_rna(v[j]);
+        small[j] = to_tf32_rna(v[j] - big[j]);
+      }
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (t == 0) {
+        mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+        bulk_g2s(smem_u32(tiles + stage * stage_bytes), bsrc + (size_t)(kb0 + i) * stage_bytes,
+                 (uint32_t)stage_bytes, &full[stage]);
+      }
+      const uint32_t acol = kAColBase + stage * 64 + kc0;
+      tmem_st16(lane_addr + acol, big);
+      tmem_st16(lane_addr + acol + 32, small);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(&full[stage]);
+    }
+  } else if (lane == 0) {
+    // ============ MMA issuer ============
+    const uint32_t idesc = tf32_idesc(BN);
+    for (int i = 0; i < nk; ++i) {
+      const int stage = i % nst;
+      const uint32_t phase = (i / nst) & 1;
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      const uint32_t bb = smem_u32(tiles + stage * stage_bytes);
+      const uint32_t bs = bb + BN * 128;
+      const uint32_t ab = tmem + kAColBase + stage * 64;
+#pragma unroll
+      for (int ks = 0; ks < BK / 8; ++ks) {
+        const uint64_t dbb = sw128_desc(bb + ks * 32), dbs = sw128_desc(bs + ks * 32);
+        const uint32_t a_big = ab + ks * 8, a_small = ab + 32 + ks * 8;
+        mma_ts(tmem, a_small, dbb, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+        mma_ts(tmem, a_big, dbs, idesc, 1u);
+        mma_ts(tmem, a_big, dbb, idesc, 1u);
+      }
+      tc_commit(&empty[stage]);
+    }
+    tc_commit(done);
+  }
+
+  // ============ epilogue ============
+  if (warp < kProducerWarps) {
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int q = warp & 3;
+    const int half = warp >> 2;
+    const int m = m0 + q * 32 + lane;
+    const int cols = BN / 2;
+    const int n0 = ntile * BN;
+#pragma unroll 1
+    for (int c0 = half * cols; c0 < half * cols + cols; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+      if (m < M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          int n = n0 + c0 + j;
+          if (n < N) {
+            if (splits > 1)
+              part(blockIdx.z, m, n, __uint_as_float(v[j]));
+            else
+              epi(m, n, __uint_as_float(v[j]));
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kProducerWarps) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+inline int pick_bn(int N, int& ntiles) {
+  ntiles = (N + 255) / 256;
+  int per = (N + ntiles - 1) / ntiles;
+  return (per + 31) / 32 * 32;
+}
+
+template <class LA, class LB, class Epi>
+int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
+           int64_t ws_bytes, cudaStream_t st, const char* what) {
+  int ntiles = 0;
+  const int BN = pick_bn(N, ntiles);
+  const int nkb = (K + BK - 1) / BK;
+  const int64_t pack_bytes = (int64_t)ntiles * nkb * 2 * BN * 128;
+  const int64_t pack_aligned = (pack_bytes + 1023) / 1024 * 1024;
+  if (!ws || ws_bytes < pack_aligned) return -1;
+  uint8_t* bpack = reinterpret_cast<uint8_t*>(ws);
+  float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned);
+  const int64_t part_bytes = ws_bytes - pack_aligned;
+
+  pack_b_kernel<LB><<<dim3(nkb, ntiles), 256, 0, st>>>(lb, N, K, BN, nkb, bpack);
+  if (int rc = check_launch(what)) return rc;
+
+  const int mtiles = (M + BM - 1) / BM;
+  int splits = 1;
+  {
+    int64_t ctas = (int64_t)mtiles * ntiles;
+    int sms = sm_count_current();
+    if (ctas < sms) {
+      int64_t want = (sms + ctas - 1) / ctas;
+      int64_t by_k = nkb / 4;
+      int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
+      splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k), std::min<int64_t>(by_ws, 16)));
+    }
+  }
+  int kbps = (nkb + splits - 1) / splits;
+  splits = (nkb + kbps - 1) / kbps;
+  const int stage_bytes = 2 * BN * 128;
+  const int nst = std::min(STAGES, (200 << 10) / stage_bytes);
+  const int tail = STAGES * BK * 8 + (2 * STAGES + 1) * 8 + 16;
+  // >= 120 KB so that exactly one CTA (and one 512-column TMEM allocation) lives per SM
+  const int smem = std::max(1024 + nst * stage_bytes + tail, 120 << 10);
+  auto kern = tc2_kernel<LA, Epi>;
+  static bool configured = false;
+  if (!configured) {
+    BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 1024 + (200 << 10) + tail),
+            "tc2 smem attribute");
+    configured = true;
+  }
+  dim3 grid(mtiles, ntiles, splits);
+  EpiPartial part{part_ws, M, N};
+  kern<<<grid, kThreads, smem, st>>>(la, M, N, K, BN, nst, bpack, nkb, kbps, epi, part, splits);
+  if (int rc = check_launch(what)) return rc;
+  if (splits > 1) {
+    splitk_reduce_kernel<Epi><<<elementwise_grid((int64_t)M * N, 256), 256, 0, st>>>(
+        part_ws, splits, M, N, epi);
+    return check_launch(what);
+  }
+  return 0;
+}
+
+}  // namespace tc2
+
+// conv forward / stride-1 data gradient through engine v2; -1 = not taken
+int tc2_conv_fwd(const LdFwdX& la, const LdRowK& lb, int M, int N, int K, const EpiNCHW& epi,
+                 float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
+  if (M < 128 || K < 8) return -1;
+  return tc2::launch(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
+}
+
+int tc2_conv_dgrad(const LdDgradDY& la, const LdDgradW& lb, int M, int N, int K,
+                   const EpiNCHW& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
+                   const char* what) {
+  if (la.g.stride != 1 || M < 128 || K < 8) return -1;
+  return tc2::launch(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
+}
+
+}  // namespace bf
