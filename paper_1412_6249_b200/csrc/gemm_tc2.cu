@@ -33,7 +33,6 @@ constexpr int BK = 32;
 constexpr int STAGES = 4;
 constexpr int kProducerWarps = 8;
 constexpr int kProducers = kProducerWarps * 32;
-constexpr int kThreads = kProducers + 32;
 constexpr int kInvalid = -30000;
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kAColBase = 256;
@@ -216,31 +215,55 @@ __global__ void pack_b_kernel(LB lb, int N, int K, int BN, int nkb, uint8_t* __r
   }
 }
 
-// ---- main kernel ------------------------------------------------------------------
+// ---- persistent warp-specialised kernel ---------------------------------------------
+//
+// warps 0-7  : producers — A gather -> split -> tcgen05.st into the stage's TMEM
+//              columns; thread 0 also streams the stage's packed B tile by TMA
+// warp  8    : MMA issuer (one elected thread) + TMEM allocator
+// warps 9-12 : epilogue — TMEM accumulator -> registers -> NCHW / partial stores
+//
+// Work units (m-tile, n-tile, k-split) are dealt round-robin to a grid of at
+// most one CTA per SM; the stage ring (full/empty) runs continuously across
+// units and the accumulator is double-buffered when BN <= 128, so the
+// epilogue of unit u overlaps the mainloop of unit u+1.
+
+constexpr int kEpiWarps = 4;
+constexpr int kMmaWarp = kProducerWarps;
+constexpr int kAllThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
+constexpr int kKtabMax = 4096;  // k-table entries cached in shared memory per CTA
+
+struct Work {
+  int M, N, K, BN, nst, nkb, kbps, splits, mtiles, ntiles, units, nacc, full_ktab;
+};
+
+__device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& nt, int& sp) {
+  sp = u % w.splits;
+  int r = u / w.splits;
+  nt = r % w.ntiles;
+  mt = r / w.ntiles;
+}
 
 template <class LA, class Epi>
-__global__ void __launch_bounds__(kThreads, 1)
-    tc2_kernel(LA la, int M, int N, int K, int BN, int nst, const uint8_t* __restrict__ bpack,
-               int nkb, int kb_per_split, Epi epi, EpiPartial part, int splits) {
+__global__ void __launch_bounds__(kAllThreads, 1)
+    tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part) {
   using SA = Sep<LA>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
+  const int BN = w.BN;
   const int stage_bytes = 2 * BN * 128;
-  uint8_t* tiles = base;                                            // nst x stage_bytes
-  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + nst * stage_bytes);  // [STAGES][BK]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ktab + STAGES * BK);
+  uint8_t* tiles = base;
+  const int ktab_n = w.full_ktab ? w.nkb * BK : STAGES * BK;
+  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nst * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ktab + ktab_n);
   uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM;
-  const int ntile = blockIdx.y;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int nk = min(kb_per_split, nkb - kb0);
 
-  if (warp == kProducerWarps) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(kTmemCols));
@@ -251,8 +274,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], kProducers);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kEpiWarps * 32);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (w.full_ktab) {  // k -> gather offsets for the whole (padded) K extent, once per CTA
+    for (int k = threadIdx.x; k < ktab_n; k += kAllThreads)
+      ktab[k] = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
   }
   tc_fence_before();
   __syncthreads();
@@ -260,107 +290,140 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp < kProducerWarps) {
-    // ============ producers: A gather -> TF32 split -> TMEM; thread 0 also issues B TMA ============
+    // ======================= producers =======================
     const int t = threadIdx.x;
-    const int q = warp & 3;            // TMEM lane quarter
-    const int kc0 = (warp >> 2) * 16;  // which 16 of the 32 k columns
-    const int row = q * 32 + lane;
-    const int m = m0 + row;
-    const RowInfo ri = m < M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+    const int q = warp & 3;
+    const int kc0 = (warp >> 2) * 16;
     const float* __restrict__ pa = SA::ptr(la);
     const unsigned hb = SA::hb(la), wb = SA::wb(la);
     const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
-    const uint8_t* bsrc = bpack + ((size_t)ntile * nkb) * stage_bytes;
-    for (int i = 0; i < nk; ++i) {
-      const int stage = i % nst;
-      const uint32_t phase = (i / nst) & 1;
-      const int kbase = (kb0 + i) * BK;
-      RowInfo* kt = ktab + stage * BK;
-      if (t < BK) {
-        int k = kbase + t;
-        kt[t] = k < K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
-      }
-      named_sync(1, kProducers);
-      float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const RowInfo ki = kt[kc0 + j];
-        bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
-        v[j] = ok ? __ldg(pa + (ri.off + ki.off)) : 0.f;
-      }
-      float big[16], small[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        big[j] = to_tf32_rna(v[j]);
-        small[j] = to_tf32_rna(v[j] - big[j]);
-      }
-      mbar_wait(&empty[stage], phase ^ 1);
-      if (t == 0) {
-        mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-        bulk_g2s(smem_u32(tiles + stage * stage_bytes), bsrc + (size_t)(kb0 + i) * stage_bytes,
-                 (uint32_t)stage_bytes, &full[stage]);
-      }
-      const uint32_t acol = kAColBase + stage * 64 + kc0;
-      tmem_st16(lane_addr + acol, big);
-      tmem_st16(lane_addr + acol + 32, small);
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      mbar_arrive(&full[stage]);
-    }
-  } else if (lane == 0) {
-    // ============ MMA issuer ============
-    const uint32_t idesc = tf32_idesc(BN);
-    for (int i = 0; i < nk; ++i) {
-      const int stage = i % nst;
-      const uint32_t phase = (i / nst) & 1;
-      mbar_wait(&full[stage], phase);
-      tc_fence_after();
-      const uint32_t bb = smem_u32(tiles + stage * stage_bytes);
-      const uint32_t bs = bb + BN * 128;
-      const uint32_t ab = tmem + kAColBase + stage * 64;
-#pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        const uint64_t dbb = sw128_desc(bb + ks * 32), dbs = sw128_desc(bs + ks * 32);
-        const uint32_t a_big = ab + ks * 8, a_small = ab + 32 + ks * 8;
-        mma_ts(tmem, a_small, dbb, idesc, (i > 0 || ks > 0) ? 1u : 0u);
-        mma_ts(tmem, a_big, dbs, idesc, 1u);
-        mma_ts(tmem, a_big, dbb, idesc, 1u);
-      }
-      tc_commit(&empty[stage]);
-    }
-    tc_commit(done);
-  }
-
-  // ============ epilogue ============
-  if (warp < kProducerWarps) {
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int q = warp & 3;
-    const int half = warp >> 2;
-    const int m = m0 + q * 32 + lane;
-    const int cols = BN / 2;
-    const int n0 = ntile * BN;
-#pragma unroll 1
-    for (int c0 = half * cols; c0 < half * cols + cols; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-      if (m < M) {
+    int it = 0;  // global stage-ring iteration
+    for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
+      int mt, nt, sp;
+      unit_coords(w, u, mt, nt, sp);
+      const int m = mt * BM + q * 32 + lane;
+      const RowInfo ri =
+          m < w.M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+      const int kb0 = sp * w.kbps;
+      const int nk = min(w.kbps, w.nkb - kb0);
+      const uint8_t* bsrc = bpack + ((size_t)nt * w.nkb + kb0) * stage_bytes;
+      for (int i = 0; i < nk; ++i, ++it) {
+        const int stage = it % w.nst;
+        const uint32_t phase = (it / w.nst) & 1;
+        const int kbase = (kb0 + i) * BK;
+        const RowInfo* kt;
+        if (w.full_ktab) {
+          kt = ktab + kbase;
+        } else {
+          RowInfo* slot = ktab + stage * BK;
+          if (t < BK) {
+            int k = kbase + t;
+            slot[t] = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+          }
+          named_sync(1, kProducers);
+          kt = slot;
+        }
+        float v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          int n = n0 + c0 + j;
-          if (n < N) {
-            if (splits > 1)
-              part(blockIdx.z, m, n, __uint_as_float(v[j]));
-            else
-              epi(m, n, __uint_as_float(v[j]));
+          const RowInfo ki = kt[kc0 + j];
+          bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
+          v[j] = ok ? __ldg(pa + (ri.off + ki.off)) : 0.f;
+        }
+        float big[16], small[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          big[j] = to_tf32_rna(v[j]);
+          small[j] = to_tf32_rna(v[j] - big[j]);
+        }
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (t == 0) {
+          mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+          bulk_g2s(smem_u32(tiles + stage * stage_bytes), bsrc + (size_t)i * stage_bytes,
+                   (uint32_t)stage_bytes, &full[stage]);
+        }
+        const uint32_t acol = kAColBase + stage * 64 + kc0;
+        tmem_st16(lane_addr + acol, big);
+        tmem_st16(lane_addr + acol + 32, small);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&full[stage]);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ======================= MMA issuer =======================
+    if (lane == 0) {
+      const uint32_t idesc = tf32_idesc(BN);
+      int it = 0, local = 0;
+      for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
+        int mt, nt, sp;
+        unit_coords(w, u, mt, nt, sp);
+        const int nk = min(w.kbps, w.nkb - sp * w.kbps);
+        const int b = local % w.nacc;
+        const uint32_t use = local / w.nacc;
+        mbar_wait(&acc_empty[b], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem + (uint32_t)(b * 128);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int stage = it % w.nst;
+          const uint32_t phase = (it / w.nst) & 1;
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t bb = smem_u32(tiles + stage * stage_bytes);
+          const uint32_t bs = bb + BN * 128;
+          const uint32_t ab = tmem + kAColBase + stage * 64;
+#pragma unroll
+          for (int ks = 0; ks < BK / 8; ++ks) {
+            const uint64_t dbb = sw128_desc(bb + ks * 32), dbs = sw128_desc(bs + ks * 32);
+            const uint32_t a_big = ab + ks * 8, a_small = ab + 32 + ks * 8;
+            mma_ts(dacc, a_small, dbb, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+            mma_ts(dacc, a_big, dbs, idesc, 1u);
+            mma_ts(dacc, a_big, dbb, idesc, 1u);
+          }
+          tc_commit(&empty[stage]);
+        }
+        tc_commit(&acc_full[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================= epilogue =======================
+    const int q = warp & 3;
+    int local = 0;
+    for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
+      int mt, nt, sp;
+      unit_coords(w, u, mt, nt, sp);
+      const int b = local % w.nacc;
+      const uint32_t use = local / w.nacc;
+      mbar_wait(&acc_full[b], use & 1);
+      tc_fence_after();
+      const int m = mt * BM + q * 32 + lane;
+      const int n0 = nt * BN;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 128);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(taddr + (uint32_t)c0, v);
+        if (m < w.M) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            int n = n0 + c0 + j;
+            if (n < w.N) {
+              if (w.splits > 1)
+                part(sp, m, n, __uint_as_float(v[j]));
+              else
+                epi(m, n, __uint_as_float(v[j]));
+            }
           }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[b]);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kProducerWarps) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
@@ -376,53 +439,64 @@ inline int pick_bn(int N, int& ntiles) {
 template <class LA, class LB, class Epi>
 int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
            int64_t ws_bytes, cudaStream_t st, const char* what) {
-  int ntiles = 0;
-  const int BN = pick_bn(N, ntiles);
-  const int nkb = (K + BK - 1) / BK;
-  const int64_t pack_bytes = (int64_t)ntiles * nkb * 2 * BN * 128;
+  Work w{};
+  w.M = M;
+  w.N = N;
+  w.K = K;
+  w.BN = pick_bn(N, w.ntiles);
+  w.nkb = (K + BK - 1) / BK;
+  w.mtiles = (M + BM - 1) / BM;
+  w.nacc = w.BN <= 128 ? 2 : 1;
+  const int64_t stage_bytes = 2LL * w.BN * 128;
+  const int64_t pack_bytes = (int64_t)w.ntiles * w.nkb * stage_bytes;
   const int64_t pack_aligned = (pack_bytes + 1023) / 1024 * 1024;
   if (!ws || ws_bytes < pack_aligned) return -1;
   uint8_t* bpack = reinterpret_cast<uint8_t*>(ws);
   float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned);
   const int64_t part_bytes = ws_bytes - pack_aligned;
 
-  pack_b_kernel<LB><<<dim3(nkb, ntiles), 256, 0, st>>>(lb, N, K, BN, nkb, bpack);
+  pack_b_kernel<LB><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lb, N, K, w.BN, w.nkb, bpack);
   if (int rc = check_launch(what)) return rc;
 
-  const int mtiles = (M + BM - 1) / BM;
-  int splits = 1;
+  const int sms = sm_count_current();
+  w.splits = 1;
   {
-    int64_t ctas = (int64_t)mtiles * ntiles;
-    int sms = sm_count_current();
-    if (ctas < sms) {
-      int64_t want = (sms + ctas - 1) / ctas;
-      int64_t by_k = nkb / 4;
+    int64_t tiles = (int64_t)w.mtiles * w.ntiles;
+    if (tiles < sms) {
+      int64_t want = (sms + tiles - 1) / tiles;
+      int64_t by_k = w.nkb / 4;
       int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
-      splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k), std::min<int64_t>(by_ws, 16)));
+      w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
+                                                   std::min<int64_t>(by_ws, 16)));
     }
   }
-  int kbps = (nkb + splits - 1) / splits;
-  splits = (nkb + kbps - 1) / kbps;
-  const int stage_bytes = 2 * BN * 128;
-  const int nst = std::min(STAGES, (200 << 10) / stage_bytes);
-  const int tail = STAGES * BK * 8 + (2 * STAGES + 1) * 8 + 16;
-  // >= 120 KB so that exactly one CTA (and one 512-column TMEM allocation) lives per SM
-  const int smem = std::max(1024 + nst * stage_bytes + tail, 120 << 10);
+  w.kbps = (w.nkb + w.splits - 1) / w.splits;
+  w.splits = (w.nkb + w.kbps - 1) / w.kbps;
+  w.units = w.mtiles * w.ntiles * w.splits;
+
+  const int smem_cap = 227 * 1024;
+  const int tail = 4 * 8 + 4 * 8 + 16 + 1024 + 64;
+  w.full_ktab = K <= kKtabMax ? 1 : 0;
+  const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;
+  w.nst = (int)std::min<int64_t>(STAGES, (smem_cap - tail - ktab_bytes) / stage_bytes);
+  if (w.nst < 2) return -1;
+  const int smem = tail + (int)(w.nst * stage_bytes) + ktab_bytes;
   auto kern = tc2_kernel<LA, Epi>;
   static bool configured = false;
   if (!configured) {
-    BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 1024 + (200 << 10) + tail),
+    BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap),
             "tc2 smem attribute");
     configured = true;
   }
-  dim3 grid(mtiles, ntiles, splits);
+  // >= 120 KB of shared memory keeps one CTA (one 512-column TMEM allocation) per SM
+  const int smem_req = std::max(smem, 120 << 10);
+  const int grid = std::min(w.units, sms);
   EpiPartial part{part_ws, M, N};
-  kern<<<grid, kThreads, smem, st>>>(la, M, N, K, BN, nst, bpack, nkb, kbps, epi, part, splits);
+  kern<<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part);
   if (int rc = check_launch(what)) return rc;
-  if (splits > 1) {
+  if (w.splits > 1) {
     splitk_reduce_kernel<Epi><<<elementwise_grid((int64_t)M * N, 256), 256, 0, st>>>(
-        part_ws, splits, M, N, epi);
+        part_ws, w.splits, M, N, epi);
     return check_launch(what);
   }
   return 0;
