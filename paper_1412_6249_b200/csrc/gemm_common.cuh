@@ -123,6 +123,14 @@ struct LdWgradDY {
 
 // ---- epilogues --------------------------------------------------------------
 
+// Epilogues store D[m][n] with a per-row base and a per-column stride, so a
+// thread that owns row m computes its base once (row(m)) and then writes
+// out[base + n*stride] (+ bias) per column (store(r, n, v)).
+struct RowPtr {
+  float* p;
+  float bias_row;  // EpiT's per-row bias (0 if none)
+};
+
 // out[(img*Cout + n)*PQ + pq] = v (+ bias[n]);  m = img*PQ + pq
 struct EpiNCHW {
   float* out;
@@ -132,6 +140,14 @@ struct EpiNCHW {
     int img = m / PQ, pq = m - img * PQ;
     if (bias) v = __fadd_rn(v, bias[n]);
     out[((int64_t)img * Cout + n) * PQ + pq] = v;
+  }
+  __device__ __forceinline__ RowPtr row(int m) const {
+    int img = m / PQ, pq = m - img * PQ;
+    return {out + (int64_t)img * Cout * PQ + pq, 0.f};
+  }
+  __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
+    if (bias) v = __fadd_rn(v, __ldg(bias + n));
+    r.p[(int64_t)n * PQ] = v;
   }
 };
 
@@ -144,6 +160,11 @@ struct EpiT {
     if (bias) v = __fadd_rn(v, bias[m]);
     out[n * ldo + m] = v;
   }
+  __device__ __forceinline__ RowPtr row(int m) const { return {out + m, bias ? bias[m] : 0.f}; }
+  __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
+    if (bias) v = __fadd_rn(v, r.bias_row);
+    r.p[n * ldo] = v;
+  }
 };
 
 // split-K partial: ws[split][n][m]
@@ -152,6 +173,12 @@ struct EpiPartial {
   int M, N;
   __device__ __forceinline__ void operator()(int split, int m, int n, float v) const {
     ws[((int64_t)split * N + n) * M + m] = v;
+  }
+  __device__ __forceinline__ RowPtr row(int split, int m) const {
+    return {ws + (int64_t)split * N * M + m, 0.f};
+  }
+  __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
+    r.p[(int64_t)n * M] = v;
   }
 };
 

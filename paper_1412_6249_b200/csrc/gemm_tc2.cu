@@ -217,17 +217,20 @@ __global__ void pack_b_kernel(LB lb, int N, int K, int BN, int nkb, uint8_t* __r
 
 // ---- persistent warp-specialised kernel ---------------------------------------------
 //
-// warps 0-7  : producers — A gather -> split -> tcgen05.st into the stage's TMEM
-//              columns; thread 0 also streams the stage's packed B tile by TMA
-// warp  8    : MMA issuer (one elected thread) + TMEM allocator
-// warps 9-12 : epilogue — TMEM accumulator -> registers -> NCHW / partial stores
+// warps 0-7   : producers — A gather -> split -> tcgen05.st into the stage's TMEM
+//               columns (the next k-block's gathers are issued before the current
+//               one is split and stored, so two k-blocks of loads are in flight);
+//               thread 0 also streams the stage's packed B tile by TMA
+// warp  8     : MMA issuer (one elected thread) + TMEM allocator
+// warps 9-16  : epilogue — TMEM accumulator -> registers -> global stores
+//               (two warps per TMEM lane quarter, each half of the columns)
 //
 // Work units (m-tile, n-tile, k-split) are dealt round-robin to a grid of at
 // most one CTA per SM; the stage ring (full/empty) runs continuously across
 // units and the accumulator is double-buffered when BN <= 128, so the
 // epilogue of unit u overlaps the mainloop of unit u+1.
 
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 8;
 constexpr int kMmaWarp = kProducerWarps;
 constexpr int kAllThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
 constexpr int kKtabMax = 4096;  // k-table entries cached in shared memory per CTA
@@ -243,6 +246,24 @@ __device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& 
   mt = r / w.ntiles;
 }
 
+template <class SA, class LA>
+__device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowInfo* ktab,
+                                         const RowInfo& ri, int kbase, int kc0,
+                                         const float* __restrict__ pa, unsigned hb, unsigned wb,
+                                         float (&v)[16]) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int k = kbase + kc0 + j;
+    RowInfo ki;
+    if (w.full_ktab)
+      ki = ktab[k];
+    else
+      ki = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+    const bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
+    v[j] = ok ? __ldg(pa + (ri.off + ki.off)) : 0.f;
+  }
+}
+
 template <class LA, class Epi>
 __global__ void __launch_bounds__(kAllThreads, 1)
     tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part) {
@@ -253,7 +274,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   const int BN = w.BN;
   const int stage_bytes = 2 * BN * 128;
   uint8_t* tiles = base;
-  const int ktab_n = w.full_ktab ? w.nkb * BK : STAGES * BK;
+  const int ktab_n = w.full_ktab ? w.nkb * BK : 2;
   RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nst * stage_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + ktab_n);
   uint64_t* empty = full + STAGES;
@@ -297,50 +318,57 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     const float* __restrict__ pa = SA::ptr(la);
     const unsigned hb = SA::hb(la), wb = SA::wb(la);
     const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
-    int it = 0;  // global stage-ring iteration
-    for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
+    auto row_of = [&](int u) {
       int mt, nt, sp;
       unit_coords(w, u, mt, nt, sp);
       const int m = mt * BM + q * 32 + lane;
-      const RowInfo ri =
-          m < w.M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
-      const int kb0 = sp * w.kbps;
-      const int nk = min(w.kbps, w.nkb - kb0);
-      const uint8_t* bsrc = bpack + ((size_t)nt * w.nkb + kb0) * stage_bytes;
-      for (int i = 0; i < nk; ++i, ++it) {
-        const int stage = it % w.nst;
-        const uint32_t phase = (it / w.nst) & 1;
-        const int kbase = (kb0 + i) * BK;
-        const RowInfo* kt;
-        if (w.full_ktab) {
-          kt = ktab + kbase;
-        } else {
-          RowInfo* slot = ktab + stage * BK;
-          if (t < BK) {
-            int k = kbase + t;
-            slot[t] = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+      return m < w.M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+    };
+    int u = blockIdx.x, i = 0, it = 0;
+    if (u < w.units) {
+      RowInfo ri = row_of(u);
+      int mt, nt, sp;
+      unit_coords(w, u, mt, nt, sp);
+      int kb0 = sp * w.kbps;
+      int nk = min(w.kbps, w.nkb - kb0);
+      float v[16];
+      gather16<SA>(la, w, ktab, ri, kb0 * BK, kc0, pa, hb, wb, v);
+      while (true) {
+        // next (unit, k-block) and its prefetch
+        int u2 = u, i2 = i + 1;
+        if (i2 >= nk) {
+          u2 = u + gridDim.x;
+          i2 = 0;
+        }
+        const bool more = u2 < w.units;
+        RowInfo ri2 = ri;
+        int kb02 = kb0, nk2 = nk, nt2 = nt;
+        float v2[16];
+        if (more) {
+          if (u2 != u) {
+            int mt2, sp2;
+            unit_coords(w, u2, mt2, nt2, sp2);
+            ri2 = row_of(u2);
+            kb02 = sp2 * w.kbps;
+            nk2 = min(w.kbps, w.nkb - kb02);
           }
-          named_sync(1, kProducers);
-          kt = slot;
+          gather16<SA>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
         }
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const RowInfo ki = kt[kc0 + j];
-          bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
-          v[j] = ok ? __ldg(pa + (ri.off + ki.off)) : 0.f;
-        }
+        // current k-block: split, publish to TMEM + kick off the B tile
         float big[16], small[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           big[j] = to_tf32_rna(v[j]);
           small[j] = to_tf32_rna(v[j] - big[j]);
         }
+        const int stage = it % w.nst;
+        const uint32_t phase = (it / w.nst) & 1;
         mbar_wait(&empty[stage], phase ^ 1);
         if (t == 0) {
           mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-          bulk_g2s(smem_u32(tiles + stage * stage_bytes), bsrc + (size_t)i * stage_bytes,
-                   (uint32_t)stage_bytes, &full[stage]);
+          bulk_g2s(smem_u32(tiles + stage * stage_bytes),
+                   bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
+                   &full[stage]);
         }
         const uint32_t acol = kAColBase + stage * 64 + kc0;
         tmem_st16(lane_addr + acol, big);
@@ -348,6 +376,16 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&full[stage]);
+        ++it;
+        if (!more) break;
+        u = u2;
+        i = i2;
+        ri = ri2;
+        kb0 = kb02;
+        nk = nk2;
+        nt = nt2;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = v2[j];
       }
     }
   } else if (warp == kMmaWarp) {
@@ -388,7 +426,9 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     __syncwarp();
   } else {
     // ======================= epilogue =======================
+    const int ew = warp - kMmaWarp - 1;  // 0..7
     const int q = warp & 3;
+    const int half = ew >> 2;
     int local = 0;
     for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
       int mt, nt, sp;
@@ -399,21 +439,24 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       tc_fence_after();
       const int m = mt * BM + q * 32 + lane;
       const int n0 = nt * BN;
+      const int cols = BN / 2;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 128);
+      const bool live = m < w.M;
+      const RowPtr rp = live ? (w.splits > 1 ? part.row(sp, m) : epi.row(m)) : RowPtr{nullptr, 0.f};
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
+      for (int c0 = half * cols; c0 < half * cols + cols; c0 += 16) {
         uint32_t v[16];
         tmem_ld16(taddr + (uint32_t)c0, v);
-        if (m < w.M) {
+        if (live) {
+          const int nlim = w.N - (n0 + c0);
+          if (w.splits > 1) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            int n = n0 + c0 + j;
-            if (n < w.N) {
-              if (w.splits > 1)
-                part(sp, m, n, __uint_as_float(v[j]));
-              else
-                epi(m, n, __uint_as_float(v[j]));
-            }
+            for (int j = 0; j < 16; ++j)
+              if (j < nlim) part.store(rp, n0 + c0 + j, __uint_as_float(v[j]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nlim) epi.store(rp, n0 + c0 + j, __uint_as_float(v[j]));
           }
         }
       }
@@ -475,9 +518,9 @@ int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, floa
   w.units = w.mtiles * w.ntiles * w.splits;
 
   const int smem_cap = 227 * 1024;
-  const int tail = 4 * 8 + 4 * 8 + 16 + 1024 + 64;
+  const int tail = 1024 + 16 * 8 + 64;
   w.full_ktab = K <= kKtabMax ? 1 : 0;
-  const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;
+  const int ktab_bytes = (w.full_ktab ? w.nkb * BK : 2) * 8;
   w.nst = (int)std::min<int64_t>(STAGES, (smem_cap - tail - ktab_bytes) / stage_bytes);
   if (w.nst < 2) return -1;
   const int smem = tail + (int)(w.nst * stage_bytes) + ktab_bytes;
