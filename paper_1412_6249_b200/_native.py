@@ -9,12 +9,15 @@ silently degrade to CPU arithmetic.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .kinds import KernelError
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpurine_b200.so"
+if os.environ.get("PURINE_B200_LIB"):  # A/B builds of the same library (tools/)
+    LIB_PATH = Path(os.environ["PURINE_B200_LIB"]).resolve()
 
 _p = C.c_void_p
 _f = C.c_float

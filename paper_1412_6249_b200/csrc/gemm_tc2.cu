@@ -230,7 +230,13 @@ __global__ void pack_b_kernel(LB lb, int N, int K, int BN, int nkb, uint8_t* __r
 // units and the accumulator is double-buffered when BN <= 128, so the
 // epilogue of unit u overlaps the mainloop of unit u+1.
 
-constexpr int kEpiWarps = 8;
+#ifndef TC2_EPI_WARPS
+#define TC2_EPI_WARPS 8
+#endif
+#ifndef TC2_PREFETCH
+#define TC2_PREFETCH 1
+#endif
+constexpr int kEpiWarps = TC2_EPI_WARPS;
 constexpr int kMmaWarp = kProducerWarps;
 constexpr int kAllThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
 constexpr int kKtabMax = 4096;  // k-table entries cached in shared memory per CTA
@@ -246,22 +252,35 @@ __device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& 
   mt = r / w.ntiles;
 }
 
-template <class SA, class LA>
-__device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowInfo* ktab,
-                                         const RowInfo& ri, int kbase, int kc0,
-                                         const float* __restrict__ pa, unsigned hb, unsigned wb,
-                                         float (&v)[16]) {
+template <class SA, bool kTable, class LA>
+__device__ __forceinline__ void gather16_impl(const LA& la, const Work& w, const RowInfo* ktab,
+                                              const RowInfo& ri, int kbase, int kc0,
+                                              const float* __restrict__ pa, unsigned hb,
+                                              unsigned wb, float (&v)[16]) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int k = kbase + kc0 + j;
     RowInfo ki;
-    if (w.full_ktab)
+    if (kTable)
       ki = ktab[k];
     else
       ki = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
     const bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
     v[j] = ok ? __ldg(pa + (ri.off + ki.off)) : 0.f;
   }
+}
+
+// the table/no-table choice is hoisted out of the unrolled loop so the
+// division-heavy fallback is never if-converted into the common path
+template <class SA, class LA>
+__device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowInfo* ktab,
+                                         const RowInfo& ri, int kbase, int kc0,
+                                         const float* __restrict__ pa, unsigned hb, unsigned wb,
+                                         float (&v)[16]) {
+  if (w.full_ktab)
+    gather16_impl<SA, true>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
+  else
+    gather16_impl<SA, false>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
 }
 
 template <class LA, class Epi>
@@ -344,16 +363,16 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         RowInfo ri2 = ri;
         int kb02 = kb0, nk2 = nk, nt2 = nt;
         float v2[16];
-        if (more) {
-          if (u2 != u) {
-            int mt2, sp2;
-            unit_coords(w, u2, mt2, nt2, sp2);
-            ri2 = row_of(u2);
-            kb02 = sp2 * w.kbps;
-            nk2 = min(w.kbps, w.nkb - kb02);
-          }
-          gather16<SA>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
+        if (more && u2 != u) {
+          int mt2, sp2;
+          unit_coords(w, u2, mt2, nt2, sp2);
+          ri2 = row_of(u2);
+          kb02 = sp2 * w.kbps;
+          nk2 = min(w.kbps, w.nkb - kb02);
         }
+#if TC2_PREFETCH
+        if (more) gather16<SA>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
+#endif
         // current k-block: split, publish to TMEM + kick off the B tile
         float big[16], small[16];
 #pragma unroll
@@ -378,6 +397,9 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         mbar_arrive(&full[stage]);
         ++it;
         if (!more) break;
+#if !TC2_PREFETCH
+        gather16<SA>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
+#endif
         u = u2;
         i = i2;
         ri = ri2;
@@ -426,9 +448,9 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     __syncwarp();
   } else {
     // ======================= epilogue =======================
-    const int ew = warp - kMmaWarp - 1;  // 0..7
+    const int ew = warp - kMmaWarp - 1;  // 0..kEpiWarps-1
     const int q = warp & 3;
-    const int half = ew >> 2;
+    const int half = kEpiWarps == 8 ? (ew >> 2) : 0;
     int local = 0;
     for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
       int mt, nt, sp;
@@ -439,7 +461,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       tc_fence_after();
       const int m = mt * BM + q * 32 + lane;
       const int n0 = nt * BN;
-      const int cols = BN / 2;
+      const int cols = kEpiWarps == 8 ? BN / 2 : BN;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 128);
       const bool live = m < w.M;
       const RowPtr rp = live ? (w.splits > 1 ? part.row(sp, m) : epi.row(m)) : RowPtr{nullptr, 0.f};
