@@ -90,6 +90,61 @@ struct Sep<LdDgradDY> {  // stride 1
   __device__ static const float* ptr(const LdDgradDY& l) { return l.dy; }
 };
 
+// ---- fast A views: K ordered (r, s, c) with c fastest ----------------------------
+// A thread's 16-element chunk is then 16 consecutive input channels at one filter
+// tap: one bounds check and a constant address stride per chunk.  Needs the
+// channel count divisible by 16 (all GoogLeNet / NIN layers except conv1).
+
+struct ChunkInfo {
+  int off;
+  short dh, dw;
+};
+
+template <class L>
+struct Fast;
+
+template <>
+struct Fast<LdFwdX> {
+  __device__ static ChunkInfo chunk(const LdFwdX& l, int kk) {  // kk = first k of the chunk
+    const ConvShape& g = l.g;
+    int rs = kk / g.C, c0 = kk - rs * g.C;
+    int r = rs / g.S, s = rs - r * g.S;
+    return {c0 * g.H * g.W + r * g.W + s, (short)r, (short)s};
+  }
+  __device__ static int stride(const LdFwdX& l) { return l.g.H * l.g.W; }
+  static bool ok(const LdFwdX& l) { return l.g.C % 16 == 0; }
+};
+
+template <>
+struct Fast<LdDgradDY> {
+  __device__ static ChunkInfo chunk(const LdDgradDY& l, int kk) {
+    const ConvShape& g = l.g;
+    int rs = kk / g.K, k0 = kk - rs * g.K;
+    int r = rs / g.S, s = rs - r * g.S;
+    return {k0 * g.P * g.Q - r * g.Q - s, (short)-r, (short)-s};
+  }
+  __device__ static int stride(const LdDgradDY& l) { return l.g.P * l.g.Q; }
+  static bool ok(const LdDgradDY& l) { return l.g.K % 16 == 0 && l.g.stride == 1; }
+};
+
+// B views with the same (r, s, c) K order for the pack kernel
+struct LdFwdWPerm {  // B(n = kout, k' = (rs, c)) = w[kout][c][rs]
+  const float* w;
+  int C, RS;
+  __device__ __forceinline__ float operator()(int n, int k) const {
+    int rs = k / C, c = k - rs * C;
+    return w[((int64_t)n * C + c) * RS + rs];
+  }
+};
+struct LdDgradWPerm {  // B(n = c, k' = (rs, ko)) = w[ko][c][rs]
+  const float* w;
+  int C, Kout, RS;
+  __device__ __forceinline__ float operator()(int n, int k) const {
+    int rs = k / Kout, ko = k - rs * Kout;
+    return w[((int64_t)ko * C + n) * RS + rs];
+  }
+};
+
 // ---- PTX helpers --------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -179,10 +234,10 @@ __device__ __forceinline__ uint32_t tf32_idesc(int bn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) |
          ((uint32_t)(BM >> 4) << 24);
 }
+// round to the nearest TF32 value (ties away from zero) in two integer ops:
+// add half a TF32 ulp to the magnitude bits, clear the 13 dropped bits
 __device__ __forceinline__ float to_tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 __device__ __forceinline__ uint32_t sw_off(int r, int c) {
   return (uint32_t)(r * 128 + (((c ^ r) & 7) << 4));
@@ -270,20 +325,45 @@ __device__ __forceinline__ void gather16_impl(const LA& la, const Work& w, const
   }
 }
 
+__device__ __forceinline__ float ldg_pred(const float* p, int ok) {
+  float v;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, 0;\n\t"
+      "@q ld.global.nc.f32 %0, [%1];\n\t}"
+      : "=f"(v)
+      : "l"(p), "r"(ok));
+  return v;
+}
+
+// fast path: the chunk is 16 consecutive channels at one filter tap
+template <class LA>
+__device__ __forceinline__ void gather16_fast(const LA& la, const RowInfo* ktab,
+                                              const RowInfo& ri, int kbase, int kc0,
+                                              const float* __restrict__ pa, unsigned hb,
+                                              unsigned wb, float (&v)[16]) {
+  const ChunkInfo ci = reinterpret_cast<const ChunkInfo*>(ktab)[(kbase + kc0) >> 4];
+  const int ok = (unsigned)(ri.h + ci.dh) < hb && (unsigned)(ri.w + ci.dw) < wb;
+  const float* p = pa + (ok ? ri.off + ci.off : 0);
+  const int stride = Fast<LA>::stride(la);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = ldg_pred(p + j * stride, ok);
+}
+
 // the table/no-table choice is hoisted out of the unrolled loop so the
 // division-heavy fallback is never if-converted into the common path
-template <class SA, class LA>
+template <class SA, bool FAST, class LA>
 __device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowInfo* ktab,
                                          const RowInfo& ri, int kbase, int kc0,
                                          const float* __restrict__ pa, unsigned hb, unsigned wb,
                                          float (&v)[16]) {
-  if (w.full_ktab)
+  if (FAST)
+    gather16_fast(la, ktab, ri, kbase, kc0, pa, hb, wb, v);
+  else if (w.full_ktab)
     gather16_impl<SA, true>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
   else
     gather16_impl<SA, false>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
 }
 
-template <class LA, class Epi>
+template <class LA, class Epi, bool FAST>
 __global__ void __launch_bounds__(kAllThreads, 1)
     tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part) {
   using SA = Sep<LA>;
@@ -320,7 +400,12 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (w.full_ktab) {  // k -> gather offsets for the whole (padded) K extent, once per CTA
+  if (FAST) {  // per 16-channel chunk: offset and filter tap, once per CTA
+    ChunkInfo* ct = reinterpret_cast<ChunkInfo*>(ktab);
+    for (int c = threadIdx.x; c < ktab_n / 16; c += kAllThreads)
+      ct[c] = c * 16 < w.K ? Fast<LA>::chunk(la, c * 16)
+                           : ChunkInfo{0, (short)kInvalid, (short)kInvalid};
+  } else if (w.full_ktab) {  // k -> gather offsets for the whole (padded) K extent, once per CTA
     for (int k = threadIdx.x; k < ktab_n; k += kAllThreads)
       ktab[k] = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
   }
@@ -351,7 +436,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       int kb0 = sp * w.kbps;
       int nk = min(w.kbps, w.nkb - kb0);
       float v[16];
-      gather16<SA>(la, w, ktab, ri, kb0 * BK, kc0, pa, hb, wb, v);
+      gather16<SA, FAST>(la, w, ktab, ri, kb0 * BK, kc0, pa, hb, wb, v);
       while (true) {
         // next (unit, k-block) and its prefetch
         int u2 = u, i2 = i + 1;
@@ -371,7 +456,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           nk2 = min(w.kbps, w.nkb - kb02);
         }
 #if TC2_PREFETCH
-        if (more) gather16<SA>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
+        if (more) gather16<SA, FAST>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
 #endif
         // current k-block: split, publish to TMEM + kick off the B tile
         float big[16], small[16];
@@ -398,7 +483,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         ++it;
         if (!more) break;
 #if !TC2_PREFETCH
-        gather16<SA>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
+        gather16<SA, FAST>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
 #endif
         u = u2;
         i = i2;
@@ -501,9 +586,10 @@ inline int pick_bn(int N, int& ntiles) {
   return (per + 31) / 32 * 32;
 }
 
-template <class LA, class LB, class Epi>
-int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
-           int64_t ws_bytes, cudaStream_t st, const char* what) {
+template <class LA, class LB, class LBP, class Epi>
+int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, const Epi& epi,
+           float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
+  const bool fast = Fast<LA>::ok(la);
   Work w{};
   w.M = M;
   w.N = N;
@@ -520,7 +606,10 @@ int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, floa
   float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned);
   const int64_t part_bytes = ws_bytes - pack_aligned;
 
-  pack_b_kernel<LB><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lb, N, K, w.BN, w.nkb, bpack);
+  if (fast)
+    pack_b_kernel<LBP><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack);
+  else
+    pack_b_kernel<LB><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lb, N, K, w.BN, w.nkb, bpack);
   if (int rc = check_launch(what)) return rc;
 
   const int sms = sm_count_current();
@@ -541,17 +630,17 @@ int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, floa
 
   const int smem_cap = 227 * 1024;
   const int tail = 1024 + 16 * 8 + 64;
-  w.full_ktab = K <= kKtabMax ? 1 : 0;
+  w.full_ktab = (fast || K <= kKtabMax) ? 1 : 0;
   const int ktab_bytes = (w.full_ktab ? w.nkb * BK : 2) * 8;
   w.nst = (int)std::min<int64_t>(STAGES, (smem_cap - tail - ktab_bytes) / stage_bytes);
   if (w.nst < 2) return -1;
   const int smem = tail + (int)(w.nst * stage_bytes) + ktab_bytes;
-  auto kern = tc2_kernel<LA, Epi>;
-  static bool configured = false;
-  if (!configured) {
+  auto kern = fast ? tc2_kernel<LA, Epi, true> : tc2_kernel<LA, Epi, false>;
+  static bool configured[2] = {false, false};
+  if (!configured[fast]) {
     BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap),
             "tc2 smem attribute");
-    configured = true;
+    configured[fast] = true;
   }
   // >= 120 KB of shared memory keeps one CTA (one 512-column TMEM allocation) per SM
   const int smem_req = std::max(smem, 120 << 10);
@@ -573,14 +662,16 @@ int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, floa
 int tc2_conv_fwd(const LdFwdX& la, const LdRowK& lb, int M, int N, int K, const EpiNCHW& epi,
                  float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
   if (M < 128 || K < 8) return -1;
-  return tc2::launch(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
+  tc2::LdFwdWPerm lbp{lb.p, la.g.C, la.g.R * la.g.S};
+  return tc2::launch(la, lb, lbp, M, N, K, epi, ws, ws_bytes, st, what);
 }
 
 int tc2_conv_dgrad(const LdDgradDY& la, const LdDgradW& lb, int M, int N, int K,
                    const EpiNCHW& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
                    const char* what) {
   if (la.g.stride != 1 || M < 128 || K < 8) return -1;
-  return tc2::launch(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
+  tc2::LdDgradWPerm lbp{lb.w, la.g.C, la.g.K, la.g.R * la.g.S};
+  return tc2::launch(la, lb, lbp, M, N, K, epi, ws, ws_bytes, st, what);
 }
 
 }  // namespace bf
