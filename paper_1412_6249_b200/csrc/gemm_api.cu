@@ -87,6 +87,11 @@ int bf_conv2d_bwd_weight(const float* x, const float* dy, float* dw, int N, int 
   LdWgradX la{x, g};
   LdWgradDY lb{dy, g};
   EpiT epi{dw, nullptr, (int64_t)C * R * S};
+  if (g_gemm_engine == 0) {
+    int rc = tc2_conv_wgrad(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
+                            "conv2d_backward_weight");
+    if (rc >= 0) return rc;
+  }
   return run_gemm(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
                   "conv2d_backward_weight");
 }

@@ -21,6 +21,9 @@ int tc2_conv_fwd(const LdFwdX& la, const LdRowK& lb, int M, int N, int K, const 
 int tc2_conv_dgrad(const LdDgradDY& la, const LdDgradW& lb, int M, int N, int K,
                    const EpiNCHW& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
                    const char* what);
+int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
+                   const EpiT& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
+                   const char* what);
 
 extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only
 

@@ -90,6 +90,28 @@ struct Sep<LdDgradDY> {  // stride 1
   __device__ static const float* ptr(const LdDgradDY& l) { return l.dy; }
 };
 
+template <>
+struct Sep<LdWgradX> {  // row = (c,r,s), k = output pixel (n,p,q)
+  __device__ static RowInfo row(const LdWgradX& l, int crs) {
+    const ConvShape& g = l.g;
+    int RS = g.R * g.S;
+    int c = crs / RS, rs = crs - c * RS;
+    int r = rs / g.S, s = rs - r * g.S;
+    return {c * g.H * g.W + r * g.W + s, (short)r, (short)s};
+  }
+  __device__ static RowInfo kin(const LdWgradX& l, int k) {
+    const ConvShape& g = l.g;
+    int PQ = g.P * g.Q;
+    int n = k / PQ, pq = k - n * PQ;
+    int p = pq / g.Q, q = pq - p * g.Q;
+    int ih = p * g.stride - g.pad, iw = q * g.stride - g.pad;
+    return {n * g.C * g.H * g.W + ih * g.W + iw, (short)ih, (short)iw};
+  }
+  __device__ static unsigned hb(const LdWgradX& l) { return (unsigned)l.g.H; }
+  __device__ static unsigned wb(const LdWgradX& l) { return (unsigned)l.g.W; }
+  __device__ static const float* ptr(const LdWgradX& l) { return l.x; }
+};
+
 // ---- fast A views: K ordered (r, s, c) with c fastest ----------------------------
 // A thread's 16-element chunk is then 16 consecutive input channels at one filter
 // tap: one bounds check and a constant address stride per chunk.  Needs the
@@ -101,7 +123,11 @@ struct ChunkInfo {
 };
 
 template <class L>
-struct Fast;
+struct Fast {
+  __device__ static ChunkInfo chunk(const L&, int) { return {0, 0, 0}; }
+  __device__ static int stride(const L&) { return 0; }
+  static bool ok(const L&) { return false; }
+};
 
 template <>
 struct Fast<LdFwdX> {
@@ -307,6 +333,15 @@ __device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& 
   mt = r / w.ntiles;
 }
 
+__device__ __forceinline__ float ldg_pred(const float* p, int ok) {
+  float v;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, 0;\n\t"
+      "@q ld.global.nc.f32 %0, [%1];\n\t}"
+      : "=f"(v)
+      : "l"(p), "r"(ok));
+  return v;
+}
+
 template <class SA, bool kTable, class LA>
 __device__ __forceinline__ void gather16_impl(const LA& la, const Work& w, const RowInfo* ktab,
                                               const RowInfo& ri, int kbase, int kc0,
@@ -320,18 +355,9 @@ __device__ __forceinline__ void gather16_impl(const LA& la, const Work& w, const
       ki = ktab[k];
     else
       ki = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
-    const bool ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
-    v[j] = ok ? __ldg(pa + (ri.off + ki.off)) : 0.f;
+    const int ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
+    v[j] = ldg_pred(pa + (ok ? ri.off + ki.off : 0), ok);
   }
-}
-
-__device__ __forceinline__ float ldg_pred(const float* p, int ok) {
-  float v;
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\tmov.b32 %0, 0;\n\t"
-      "@q ld.global.nc.f32 %0, [%1];\n\t}"
-      : "=f"(v)
-      : "l"(p), "r"(ok));
-  return v;
 }
 
 // fast path: the chunk is 16 consecutive channels at one filter tap
@@ -373,7 +399,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   const int BN = w.BN;
   const int stage_bytes = 2 * BN * 128;
   uint8_t* tiles = base;
-  const int ktab_n = w.full_ktab ? w.nkb * BK : 2;
+  const int ktab_n = w.full_ktab ? w.nkb * BK : STAGES * BK;
   RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nst * stage_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + ktab_n);
   uint64_t* empty = full + STAGES;
@@ -429,7 +455,49 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       return m < w.M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
     };
     int u = blockIdx.x, i = 0, it = 0;
-    if (u < w.units) {
+    if (!FAST && !w.full_ktab) {
+      // K too long for a cached table (weight gradients: K = N*P*Q pixels):
+      // the k-block's 32 gather offsets are computed per stage into a ring slot
+      for (; u < w.units; u += gridDim.x) {
+        int mt, nt, sp;
+        unit_coords(w, u, mt, nt, sp);
+        const RowInfo ri = row_of(u);
+        const int kb0 = sp * w.kbps;
+        const int nk = min(w.kbps, w.nkb - kb0);
+        for (int i2 = 0; i2 < nk; ++i2, ++it) {
+          const int stage = it % w.nst;
+          const uint32_t phase = (it / w.nst) & 1;
+          const int kbase = (kb0 + i2) * BK;
+          RowInfo* slot = ktab + stage * BK;
+          if (t < BK) {
+            const int k = kbase + t;
+            slot[t] = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
+          }
+          named_sync(1, kProducers);
+          float v[16];
+          gather16_impl<SA, true>(la, w, slot - kbase, ri, kbase, kc0, pa, hb, wb, v);
+          float big[16], small[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            big[j] = to_tf32_rna(v[j]);
+            small[j] = to_tf32_rna(v[j] - big[j]);
+          }
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (t == 0) {
+            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
+            bulk_g2s(smem_u32(tiles + stage * stage_bytes),
+                     bpack + ((size_t)nt * w.nkb + kb0 + i2) * stage_bytes,
+                     (uint32_t)stage_bytes, &full[stage]);
+          }
+          const uint32_t acol = kAColBase + stage * 64 + kc0;
+          tmem_st16(lane_addr + acol, big);
+          tmem_st16(lane_addr + acol + 32, small);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_arrive(&full[stage]);
+        }
+      }
+    } else if (u < w.units) {
       RowInfo ri = row_of(u);
       int mt, nt, sp;
       unit_coords(w, u, mt, nt, sp);
@@ -621,7 +689,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
       int64_t by_k = w.nkb / 4;
       int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
       w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                   std::min<int64_t>(by_ws, 16)));
+                                                   std::min<int64_t>(by_ws, 64)));
     }
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
@@ -631,7 +699,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   const int smem_cap = 227 * 1024;
   const int tail = 1024 + 16 * 8 + 64;
   w.full_ktab = (fast || K <= kKtabMax) ? 1 : 0;
-  const int ktab_bytes = (w.full_ktab ? w.nkb * BK : 2) * 8;
+  const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;
   w.nst = (int)std::min<int64_t>(STAGES, (smem_cap - tail - ktab_bytes) / stage_bytes);
   if (w.nst < 2) return -1;
   const int smem = tail + (int)(w.nst * stage_bytes) + ktab_bytes;
@@ -664,6 +732,13 @@ int tc2_conv_fwd(const LdFwdX& la, const LdRowK& lb, int M, int N, int K, const 
   if (M < 128 || K < 8) return -1;
   tc2::LdFwdWPerm lbp{lb.p, la.g.C, la.g.R * la.g.S};
   return tc2::launch(la, lb, lbp, M, N, K, epi, ws, ws_bytes, st, what);
+}
+
+int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
+                   const EpiT& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
+                   const char* what) {
+  if (M < 128 || K < 8) return -1;
+  return tc2::launch(la, lb, lb, M, N, K, epi, ws, ws_bytes, st, what);
 }
 
 int tc2_conv_dgrad(const LdDgradDY& la, const LdDgradW& lb, int M, int N, int K,

@@ -218,11 +218,31 @@ class RunContext:
     transport: object | None = None
     copy_latency_s: float = 0.0
     stream: int = 0
-    workspace: torch.Tensor | None = None
+    workspace: object | None = None  # _Workspace: .data_ptr() / .numel(), lazily allocated
     lane: WorkerLane | None = None
 
 
-WORKSPACE_FLOATS = 16 << 20  # 64 MiB per stream
+WORKSPACE_FLOATS = int(os.environ.get("PURINE_B200_WORKSPACE_MB", "1024")) << 18  # 1 GiB
+
+
+class _Workspace:
+    """Per-stream scratch (split-K partials, pre-packed GEMM operands),
+    allocated on first use so lanes that never run a contraction cost nothing."""
+
+    def __init__(self, device) -> None:
+        self.device = device
+        self.buf: torch.Tensor | None = None
+
+    def tensor(self) -> torch.Tensor:
+        if self.buf is None:
+            self.buf = torch.empty(WORKSPACE_FLOATS, dtype=torch.float32, device=self.device)
+        return self.buf
+
+    def data_ptr(self) -> int:
+        return self.tensor().data_ptr()
+
+    def numel(self) -> int:
+        return WORKSPACE_FLOATS
 
 
 class _Lanes:
@@ -231,13 +251,12 @@ class _Lanes:
     def __init__(self, store: TensorStore) -> None:
         self.device = store.device
         self.streams: list[torch.cuda.Stream] = []
-        self.workspaces: list[torch.Tensor] = []
+        self.workspaces: list[_Workspace] = []
 
-    def get(self, idx: int) -> tuple[torch.cuda.Stream, torch.Tensor]:
+    def get(self, idx: int) -> tuple[torch.cuda.Stream, _Workspace]:
         while len(self.streams) <= idx:
             self.streams.append(torch.cuda.Stream(device=self.device))
-            self.workspaces.append(torch.empty(WORKSPACE_FLOATS, dtype=torch.float32,
-                                               device=self.device))
+            self.workspaces.append(_Workspace(self.device))
         return self.streams[idx], self.workspaces[idx]
 
 

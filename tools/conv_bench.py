@@ -50,7 +50,7 @@ def main():
     lib("bf_set_device", 0)
     lib("bf_set_gemm_engine", a.engine)
     net = (googlenet if a.net == "googlenet" else nin)(batch=a.batch)
-    ws = torch.empty(16 << 20, device="cuda")
+    ws = torch.empty(256 << 20, device="cuda")
     stream = torch.cuda.current_stream().cuda_stream
     totals = {}
     layers = conv_layers(net)
