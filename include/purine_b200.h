@@ -103,8 +103,10 @@ int bf_conv2d_bwd_weight(const float* x, const float* dy, float* dw,
                          int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                          int stride, int pad, float* workspace, int64_t ws_bytes,
                          bf_stream_t stream);
-/* db[k] = sum over (n, p, q) of dy, deterministic order */
-int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, bf_stream_t stream);
+/* db[k] = sum over (n, p, q) of dy, deterministic order; workspace >= 4*K*slices bytes
+   (optional: NULL falls back to one CTA per channel) */
+int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, float* workspace,
+                       int64_t ws_bytes, bf_stream_t stream);
 /* workspace bytes the conv/fc entry points want for this shape (0 = none) */
 int64_t bf_gemm_workspace_bytes(int op, int N, int C, int H, int W, int K, int R, int S,
                                 int P, int Q, int stride, int pad);

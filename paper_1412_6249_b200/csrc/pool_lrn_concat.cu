@@ -12,6 +12,7 @@ namespace bf {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kPlaneSmemMax = 100 << 10;  // shared-memory plane kernels up to 100 KB
 
 __device__ __forceinline__ void window_rows(int o, int stride, int pad, int k, int size, int& lo,
                                             int& hi) {
@@ -258,6 +259,186 @@ __global__ void mean_kernel(const float* __restrict__ v, float* __restrict__ out
   if (threadIdx.x == 0) out[0] = s / (float)n;
 }
 
+// ---- shared-memory plane kernels ---------------------------------------------------
+// One CTA per (n, c) plane: the plane is staged in shared memory once, so every
+// input is read from HBM once although 3x3 windows overlap; the window scan and
+// the accumulation order are exactly those of the per-element kernels above
+// (bit-identical results).
+
+__global__ void maxpool_fwd_plane(const float* __restrict__ x, float* __restrict__ y,
+                                  float* __restrict__ mask, int H, int W, int P, int Q, int k,
+                                  int stride, int pad) {
+  extern __shared__ float plane[];
+  const int64_t pl = blockIdx.x;
+  const float* xp = x + pl * (int64_t)H * W;
+  const int HW = H * W;
+  for (int i = threadIdx.x; i < HW; i += blockDim.x) plane[i] = xp[i];
+  __syncthreads();
+  float* yp = y + pl * (int64_t)P * Q;
+  float* mp = mask + pl * (int64_t)P * Q;
+  for (int o = threadIdx.x; o < P * Q; o += blockDim.x) {
+    int ph = o / Q, pw = o - ph * Q;
+    int h0, h1, w0, w1;
+    window_rows(ph, stride, pad, k, H, h0, h1);
+    window_rows(pw, stride, pad, k, W, w0, w1);
+    float best = -INFINITY;
+    int arg = -1;
+    for (int h = h0; h < h1; ++h)
+      for (int w = w0; w < w1; ++w) {
+        float v = plane[h * W + w];
+        if (v > best) {
+          best = v;
+          arg = h * W + w;
+        }
+      }
+    yp[o] = best;
+    mp[o] = (float)arg;
+  }
+}
+
+__global__ void maxpool_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
+                                  float* __restrict__ dx, int H, int W, int P, int Q, int k,
+                                  int stride, int pad) {
+  extern __shared__ float sm[];
+  float* ms = sm;
+  float* gs = sm + P * Q;
+  const int64_t pl = blockIdx.x;
+  const int PQ = P * Q;
+  for (int i = threadIdx.x; i < PQ; i += blockDim.x) {
+    ms[i] = mask[pl * PQ + i];
+    gs[i] = dy[pl * PQ + i];
+  }
+  __syncthreads();
+  float* dp = dx + pl * (int64_t)H * W;
+  for (int i = threadIdx.x; i < H * W; i += blockDim.x) {
+    int h = i / W, w = i - h * W;
+    int p0, p1, q0, q1;
+    covering(h, stride, pad, k, P, p0, p1);
+    covering(w, stride, pad, k, Q, q0, q1);
+    float me = (float)i;
+    float acc = 0.f;
+    for (int p = p0; p < p1; ++p)
+      for (int q = q0; q < q1; ++q)
+        if (ms[p * Q + q] == me) acc = __fadd_rn(acc, gs[p * Q + q]);
+    dp[i] = acc;
+  }
+}
+
+// LRN, one thread per (n, pixel) walking the channels with a 5-wide register
+// window (size == 5, the GoogLeNet / AlexNet setting): each input is read once.
+// Out-of-range window slots hold +0.0, which leaves the in-order sums unchanged.
+__global__ void lrn5_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
+                                float* __restrict__ scale, int N, int C, int HW, float a_n,
+                                float beta, float kk) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)N * HW) return;
+  int n = (int)(t / HW), hw = (int)(t - (int64_t)n * HW);
+  const float* xp = x + (int64_t)n * C * HW + hw;
+  float* yp = y + (int64_t)n * C * HW + hw;
+  float* sp = scale + (int64_t)n * C * HW + hw;
+  // window w0..w4 = sq[c-2 .. c+2]
+  float w0 = 0.f, w1 = 0.f, w2, w3, w4;
+  float xc = xp[0];
+  w2 = __fmul_rn(xc, xc);
+  float x1 = C > 1 ? xp[HW] : 0.f;
+  w3 = C > 1 ? __fmul_rn(x1, x1) : 0.f;
+  float x2 = C > 2 ? xp[2 * (int64_t)HW] : 0.f;
+  w4 = C > 2 ? __fmul_rn(x2, x2) : 0.f;
+  for (int c = 0; c < C; ++c) {
+    float acc = 0.f;
+    acc = __fadd_rn(acc, w0);
+    acc = __fadd_rn(acc, w1);
+    acc = __fadd_rn(acc, w2);
+    acc = __fadd_rn(acc, w3);
+    acc = __fadd_rn(acc, w4);
+    float sc = __fadd_rn(kk, __fmul_rn(a_n, acc));
+    sp[(int64_t)c * HW] = sc;
+    yp[(int64_t)c * HW] = __fmul_rn(xc, powf(sc, -beta));
+    // slide: next channel
+    float xn = x1;
+    x1 = x2;
+    x2 = (c + 3 < C) ? xp[(int64_t)(c + 3) * HW] : 0.f;
+    w0 = w1;
+    w1 = w2;
+    w2 = w3;
+    w3 = w4;
+    w4 = (c + 3 < C) ? __fmul_rn(x2, x2) : 0.f;
+    xc = xn;
+  }
+}
+
+__global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
+                                const float* __restrict__ scale, const float* __restrict__ dy,
+                                float* __restrict__ dx, int N, int C, int HW, float coef,
+                                float beta) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)N * HW) return;
+  int n = (int)(t / HW), hw = (int)(t - (int64_t)n * HW);
+  const int64_t base = (int64_t)n * C * HW + hw;
+  auto ratio = [&](int c) -> float {
+    int64_t j = base + (int64_t)c * HW;
+    return __fdiv_rn(__fmul_rn(dy[j], y[j]), scale[j]);
+  };
+  float r0 = 0.f, r1 = 0.f, r2 = ratio(0);
+  float r3 = C > 1 ? ratio(1) : 0.f;
+  float r4 = C > 2 ? ratio(2) : 0.f;
+  for (int c = 0; c < C; ++c) {
+    float acc = 0.f;
+    acc = __fadd_rn(acc, r0);
+    acc = __fadd_rn(acc, r1);
+    acc = __fadd_rn(acc, r2);
+    acc = __fadd_rn(acc, r3);
+    acc = __fadd_rn(acc, r4);
+    int64_t i = base + (int64_t)c * HW;
+    float a = __fmul_rn(dy[i], powf(scale[i], -beta));
+    float b = __fmul_rn(__fmul_rn(coef, x[i]), acc);
+    dx[i] = __fsub_rn(a, b);
+    r0 = r1;
+    r1 = r2;
+    r2 = r3;
+    r3 = r4;
+    r4 = (c + 3 < C) ? ratio(c + 3) : 0.f;
+  }
+}
+
+// bias gradient, stage 1: CTA (slice, channel) sums dy over its images and all
+// pixels (fixed tree) -> partial[channel][slice]; stage 2 adds the slices in
+// order.  Deterministic, and parallel over channels x image slices.
+__global__ void bias_partial_kernel(const float* __restrict__ dy, float* __restrict__ part,
+                                    int N, int K, int PQ, int slices) {
+  __shared__ float red[33];
+  const int s = blockIdx.x, c = blockIdx.y;
+  const int per = (N + slices - 1) / slices;
+  const int n0 = s * per, n1 = min(N, n0 + per);
+  float acc = 0.f;
+  if ((PQ & 3) == 0) {
+    const int pq4 = PQ >> 2;
+    for (int n = n0; n < n1; ++n) {
+      const float4* row = reinterpret_cast<const float4*>(dy + ((int64_t)n * K + c) * PQ);
+      for (int e = threadIdx.x; e < pq4; e += blockDim.x) {
+        float4 v = row[e];
+        acc += (v.x + v.y) + (v.z + v.w);
+      }
+    }
+  } else {
+    for (int n = n0; n < n1; ++n) {
+      const float* row = dy + ((int64_t)n * K + c) * PQ;
+      for (int e = threadIdx.x; e < PQ; e += blockDim.x) acc += row[e];
+    }
+  }
+  acc = block_reduce(acc, red, false);
+  if (threadIdx.x == 0) part[(int64_t)c * slices + s] = acc;
+}
+
+__global__ void bias_finish_kernel(const float* __restrict__ part, float* __restrict__ db, int K,
+                                   int slices) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  float acc = 0.f;
+  for (int s = 0; s < slices; ++s) acc += part[(int64_t)c * slices + s];
+  db[c] = acc;
+}
+
 // per-channel sum over (n, pq): one CTA per channel, fixed tree -> deterministic
 __global__ void channel_sum_kernel(const float* __restrict__ dy, float* __restrict__ db, int N,
                                    int K, int PQ) {
@@ -294,6 +475,19 @@ int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, i
                    int Q, int kernel, int stride, int pad, bf_stream_t s) {
   int64_t total = (int64_t)N * C * P * Q;
   if (total <= 0) return 0;
+  const int smem = H * W * 4;
+  if (smem <= kPlaneSmemMax) {
+    static bool attr = false;
+    if (!attr) {
+      BF_CUDA(cudaFuncSetAttribute(maxpool_fwd_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kPlaneSmemMax),
+              "maxpool smem attribute");
+      attr = true;
+    }
+    maxpool_fwd_plane<<<N * C, 256, smem, as_stream(s)>>>(x, y, mask, H, W, P, Q, kernel, stride,
+                                                          pad);
+    return check_launch("maxpool_forward");
+  }
   maxpool_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
       x, y, mask, total, H, W, P, Q, kernel, stride, pad);
   return check_launch("maxpool_forward");
@@ -303,6 +497,19 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
                    int P, int Q, int kernel, int stride, int pad, bf_stream_t s) {
   int64_t total = (int64_t)N * C * H * W;
   if (total <= 0) return 0;
+  const int smem = 2 * P * Q * 4;
+  if (smem <= kPlaneSmemMax) {
+    static bool attr = false;
+    if (!attr) {
+      BF_CUDA(cudaFuncSetAttribute(maxpool_bwd_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kPlaneSmemMax),
+              "maxpool smem attribute");
+      attr = true;
+    }
+    maxpool_bwd_plane<<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, kernel,
+                                                          stride, pad);
+    return check_launch("maxpool_backward");
+  }
   maxpool_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
       mask, dy, dx, total, H, W, P, Q, kernel, stride, pad);
   return check_launch("maxpool_backward");
@@ -333,6 +540,12 @@ int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int 
   if (total <= 0) return 0;
   int pre = (size - 1) / 2, post = size - 1 - pre;
   float a_n = alpha / (float)size;
+  if (size == 5) {
+    int64_t px = (int64_t)N * H * W;
+    lrn5_fwd_kernel<<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(x, y, scale, N, C, H * W,
+                                                                       a_n, beta, k);
+    return check_launch("lrn_forward");
+  }
   lrn_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
       x, y, scale, total, C, H * W, pre, post, a_n, beta, k);
   return check_launch("lrn_forward");
@@ -348,6 +561,12 @@ int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* 
   float coef = 2.0f * alpha;
   coef = coef * beta;
   coef = coef / (float)size;
+  if (size == 5) {
+    int64_t px = (int64_t)N * H * W;
+    lrn5_bwd_kernel<<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(x, y, scale, dy, dx, N, C,
+                                                                       H * W, coef, beta);
+    return check_launch("lrn_backward");
+  }
   lrn_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
       x, y, scale, dy, dx, total, C, H * W, pre, post, coef, beta);
   (void)k;
@@ -393,8 +612,18 @@ int bf_softmax_xent(const float* logits, const float* labels, float* loss, float
   return check_launch("softmax_xent(mean)");
 }
 
-int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, bf_stream_t s) {
+int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, float* workspace,
+                       int64_t ws_bytes, bf_stream_t s) {
   if (K <= 0) return 0;
+  int slices = (4 * sm_count_current() + K - 1) / K;
+  if (slices > N) slices = N;
+  if (slices > 1 && workspace && (int64_t)K * slices * 4 <= ws_bytes) {
+    bias_partial_kernel<<<dim3(slices, K), 256, 0, as_stream(s)>>>(dy, workspace, N, K, PQ,
+                                                                   slices);
+    if (int rc = check_launch("conv2d_backward_bias")) return rc;
+    bias_finish_kernel<<<(K + 127) / 128, 128, 0, as_stream(s)>>>(workspace, db, K, slices);
+    return check_launch("conv2d_backward_bias");
+  }
   channel_sum_kernel<<<K, 512, 0, as_stream(s)>>>(dy, db, N, K, PQ);
   return check_launch("conv2d_backward_bias");
 }

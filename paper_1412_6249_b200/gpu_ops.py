@@ -112,7 +112,7 @@ def _conv_bwd_parts(ctx, attrs, x, w, dy, dx, dw, db):
     if dw is not None:
         lib("bf_conv2d_bwd_weight", x.ptr, dy.ptr, dw.ptr, *g, *_ws(ctx), ctx.stream)
     if db is not None:
-        lib("bf_conv2d_bwd_bias", dy.ptr, db.ptr, g[0], g[4], g[7] * g[8], ctx.stream)
+        lib("bf_conv2d_bwd_bias", dy.ptr, db.ptr, g[0], g[4], g[7] * g[8], *_ws(ctx), ctx.stream)
     if dx is not None:
         lib("bf_conv2d_bwd_data", w.ptr, dy.ptr, dx.ptr, *g, *_ws(ctx), ctx.stream)
 
@@ -139,7 +139,7 @@ def _conv_bwd_bias(ctx, op):
     (dy,) = _ins(ctx, op)
     (db,) = _outs(ctx, op)
     n, k, p, q = dy.shape
-    _L()("bf_conv2d_bwd_bias", dy.ptr, db.ptr, n, k, p * q, ctx.stream)
+    _L()("bf_conv2d_bwd_bias", dy.ptr, db.ptr, n, k, p * q, *_ws(ctx), ctx.stream)
 
 
 # ---------------------------------------------------------------------------
