@@ -324,6 +324,90 @@ __global__ void maxpool_bwd_plane(const float* __restrict__ mask, const float* _
   }
 }
 
+// 3x3 windows (every GoogLeNet / NIN max-pool), stride S in {1, 2}: warps walk
+// output rows, lanes walk output columns (no per-element division), the window
+// is unrolled with clipped taps read as -inf (strict '>' never picks them).
+template <int S>
+__global__ void maxpool3_fwd_plane(const float* __restrict__ x, float* __restrict__ y,
+                                   float* __restrict__ mask, int H, int W, int P, int Q,
+                                   int pad) {
+  extern __shared__ float plane[];
+  const int64_t pl = blockIdx.x;
+  const float* xp = x + pl * (int64_t)H * W;
+  for (int i = threadIdx.x; i < H * W; i += blockDim.x) plane[i] = xp[i];
+  __syncthreads();
+  float* yp = y + pl * (int64_t)P * Q;
+  float* mp = mask + pl * (int64_t)P * Q;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int ph = warp; ph < P; ph += nw) {
+    const int hs = ph * S - pad;
+    for (int pw = lane; pw < Q; pw += 32) {
+      const int ws = pw * S - pad;
+      float best = -INFINITY;
+      int arg = -1;
+#pragma unroll
+      for (int dh = 0; dh < 3; ++dh) {
+        const int h = hs + dh;
+        const bool hv = (unsigned)h < (unsigned)H;
+#pragma unroll
+        for (int dw = 0; dw < 3; ++dw) {
+          const int w = ws + dw;
+          const bool ok = hv && (unsigned)w < (unsigned)W;
+          const float v = ok ? plane[h * W + w] : -INFINITY;
+          if (v > best) {
+            best = v;
+            arg = h * W + w;
+          }
+        }
+      }
+      yp[ph * Q + pw] = best;
+      mp[ph * Q + pw] = (float)arg;
+    }
+  }
+}
+
+template <int S>
+__global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
+                                   float* __restrict__ dx, int H, int W, int P, int Q, int pad) {
+  extern __shared__ float sm[];
+  float* ms = sm;
+  float* gs = sm + P * Q;
+  const int64_t pl = blockIdx.x;
+  const int PQ = P * Q;
+  for (int i = threadIdx.x; i < PQ; i += blockDim.x) {
+    ms[i] = mask[pl * PQ + i];
+    gs[i] = dy[pl * PQ + i];
+  }
+  __syncthreads();
+  float* dp = dx + pl * (int64_t)H * W;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int h = warp; h < H; h += nw) {
+    // output rows whose window covers h: p*S - pad <= h <= p*S - pad + 2
+    const int hp = h + pad;
+    const int p0 = hp < 3 ? 0 : (hp - 3) / S + 1;
+    const int p1 = min(hp / S + 1, P);
+    for (int w = lane; w < W; w += 32) {
+      const int wp = w + pad;
+      const int q0 = wp < 3 ? 0 : (wp - 3) / S + 1;
+      const int q1 = min(wp / S + 1, Q);
+      const float me = (float)(h * W + w);
+      float acc = 0.f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int p = p0 + a;
+        if (p < p1) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const int q = q0 + b;
+            if (q < q1 && ms[p * Q + q] == me) acc = __fadd_rn(acc, gs[p * Q + q]);
+          }
+        }
+      }
+      dp[h * W + w] = acc;
+    }
+  }
+}
+
 // LRN, one thread per (n, pixel) walking the channels with a 5-wide register
 // window (size == 5, the GoogLeNet / AlexNet setting): each input is read once.
 // Out-of-range window slots hold +0.0, which leaves the in-order sums unchanged.
@@ -482,7 +566,20 @@ int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, i
       BF_CUDA(cudaFuncSetAttribute(maxpool_fwd_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kPlaneSmemMax),
               "maxpool smem attribute");
+      BF_CUDA(cudaFuncSetAttribute(maxpool3_fwd_plane<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
+              "maxpool smem attribute");
+      BF_CUDA(cudaFuncSetAttribute(maxpool3_fwd_plane<2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
+              "maxpool smem attribute");
       attr = true;
+    }
+    if (kernel == 3 && (stride == 1 || stride == 2)) {
+      if (stride == 1)
+        maxpool3_fwd_plane<1><<<N * C, 256, smem, as_stream(s)>>>(x, y, mask, H, W, P, Q, pad);
+      else
+        maxpool3_fwd_plane<2><<<N * C, 256, smem, as_stream(s)>>>(x, y, mask, H, W, P, Q, pad);
+      return check_launch("maxpool_forward");
     }
     maxpool_fwd_plane<<<N * C, 256, smem, as_stream(s)>>>(x, y, mask, H, W, P, Q, kernel, stride,
                                                           pad);
@@ -504,7 +601,20 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
       BF_CUDA(cudaFuncSetAttribute(maxpool_bwd_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kPlaneSmemMax),
               "maxpool smem attribute");
+      BF_CUDA(cudaFuncSetAttribute(maxpool3_bwd_plane<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
+              "maxpool smem attribute");
+      BF_CUDA(cudaFuncSetAttribute(maxpool3_bwd_plane<2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
+              "maxpool smem attribute");
       attr = true;
+    }
+    if (kernel == 3 && (stride == 1 || stride == 2)) {
+      if (stride == 1)
+        maxpool3_bwd_plane<1><<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, pad);
+      else
+        maxpool3_bwd_plane<2><<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, pad);
+      return check_launch("maxpool_backward");
     }
     maxpool_bwd_plane<<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, kernel,
                                                           stride, pad);
