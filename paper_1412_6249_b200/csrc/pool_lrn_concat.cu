@@ -6,6 +6,8 @@
 // row-major order), so they need no atomics and reproduce the CPU oracle's
 // accumulation order bit for bit (oracle/kernels.py maxpool_backward /
 // avgpool_backward).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bf {
@@ -327,21 +329,28 @@ __global__ void maxpool_bwd_plane(const float* __restrict__ mask, const float* _
 // 3x3 windows (every GoogLeNet / NIN max-pool), stride S in {1, 2}: warps walk
 // output rows, lanes walk output columns (no per-element division), the window
 // is unrolled with clipped taps read as -inf (strict '>' never picks them).
-template <int S>
+// A CTA owns G consecutive (n, c) planes (G > 1 for small 14x14 / 7x7 planes);
+// a warp covers 32/CW rows x CW columns so narrow rows keep the lanes busy.
+template <int S, int CW>
 __global__ void maxpool3_fwd_plane(const float* __restrict__ x, float* __restrict__ y,
-                                   float* __restrict__ mask, int H, int W, int P, int Q,
-                                   int pad) {
-  extern __shared__ float plane[];
-  const int64_t pl = blockIdx.x;
-  const float* xp = x + pl * (int64_t)H * W;
-  for (int i = threadIdx.x; i < H * W; i += blockDim.x) plane[i] = xp[i];
+                                   float* __restrict__ mask, int planes, int G, int H, int W,
+                                   int P, int Q, int pad) {
+  extern __shared__ float plane_all[];
+  const int64_t pl0 = (int64_t)blockIdx.x * G;
+  const int g_here = (int)min<int64_t>(G, planes - pl0);
+  const float* xp0 = x + pl0 * (int64_t)H * W;
+  for (int i = threadIdx.x; i < g_here * H * W; i += blockDim.x) plane_all[i] = xp0[i];
   __syncthreads();
-  float* yp = y + pl * (int64_t)P * Q;
-  float* mp = mask + pl * (int64_t)P * Q;
+  constexpr int RPW = 32 / CW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int ph = warp; ph < P; ph += nw) {
+  const int roff = lane / CW, col = lane % CW;
+  for (int rr = warp * RPW + roff; rr < g_here * P; rr += nw * RPW) {
+    const int g = rr / P, ph = rr - g * P;
+    const float* plane = plane_all + g * H * W;
+    float* yp = y + (pl0 + g) * (int64_t)P * Q;
+    float* mp = mask + (pl0 + g) * (int64_t)P * Q;
     const int hs = ph * S - pad;
-    for (int pw = lane; pw < Q; pw += 32) {
+    for (int pw = col; pw < Q; pw += CW) {
       const int ws = pw * S - pad;
       float best = -INFINITY;
       int arg = -1;
@@ -366,27 +375,34 @@ __global__ void maxpool3_fwd_plane(const float* __restrict__ x, float* __restric
   }
 }
 
-template <int S>
+template <int S, int CW>
 __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
-                                   float* __restrict__ dx, int H, int W, int P, int Q, int pad) {
+                                   float* __restrict__ dx, int planes, int G, int H, int W, int P,
+                                   int Q, int pad) {
   extern __shared__ float sm[];
-  float* ms = sm;
-  float* gs = sm + P * Q;
-  const int64_t pl = blockIdx.x;
+  const int64_t pl0 = (int64_t)blockIdx.x * G;
+  const int g_here = (int)min<int64_t>(G, planes - pl0);
   const int PQ = P * Q;
-  for (int i = threadIdx.x; i < PQ; i += blockDim.x) {
-    ms[i] = mask[pl * PQ + i];
-    gs[i] = dy[pl * PQ + i];
+  float* ms_all = sm;
+  float* gs_all = sm + G * PQ;
+  for (int i = threadIdx.x; i < g_here * PQ; i += blockDim.x) {
+    ms_all[i] = mask[pl0 * PQ + i];
+    gs_all[i] = dy[pl0 * PQ + i];
   }
   __syncthreads();
-  float* dp = dx + pl * (int64_t)H * W;
+  constexpr int RPW = 32 / CW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int h = warp; h < H; h += nw) {
+  const int roff = lane / CW, col = lane % CW;
+  for (int rr = warp * RPW + roff; rr < g_here * H; rr += nw * RPW) {
+    const int g = rr / H, h = rr - g * H;
+    const float* ms = ms_all + g * PQ;
+    const float* gs = gs_all + g * PQ;
+    float* dp = dx + (pl0 + g) * (int64_t)H * W;
     // output rows whose window covers h: p*S - pad <= h <= p*S - pad + 2
     const int hp = h + pad;
     const int p0 = hp < 3 ? 0 : (hp - 3) / S + 1;
     const int p1 = min(hp / S + 1, P);
-    for (int w = lane; w < W; w += 32) {
+    for (int w = col; w < W; w += CW) {
       const int wp = w + pad;
       const int q0 = wp < 3 ? 0 : (wp - 3) / S + 1;
       const int q1 = min(wp / S + 1, Q);
@@ -566,19 +582,32 @@ int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, i
       BF_CUDA(cudaFuncSetAttribute(maxpool_fwd_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kPlaneSmemMax),
               "maxpool smem attribute");
-      BF_CUDA(cudaFuncSetAttribute(maxpool3_fwd_plane<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
-              "maxpool smem attribute");
-      BF_CUDA(cudaFuncSetAttribute(maxpool3_fwd_plane<2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
-              "maxpool smem attribute");
+      const void* fns[] = {(const void*)maxpool3_fwd_plane<1, 8>,
+                           (const void*)maxpool3_fwd_plane<1, 16>,
+                           (const void*)maxpool3_fwd_plane<1, 32>,
+                           (const void*)maxpool3_fwd_plane<2, 8>,
+                           (const void*)maxpool3_fwd_plane<2, 16>,
+                           (const void*)maxpool3_fwd_plane<2, 32>};
+      for (const void* f : fns)
+        BF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kPlaneSmemMax),
+                "maxpool smem attribute");
       attr = true;
     }
     if (kernel == 3 && (stride == 1 || stride == 2)) {
-      if (stride == 1)
-        maxpool3_fwd_plane<1><<<N * C, 256, smem, as_stream(s)>>>(x, y, mask, H, W, P, Q, pad);
-      else
-        maxpool3_fwd_plane<2><<<N * C, 256, smem, as_stream(s)>>>(x, y, mask, H, W, P, Q, pad);
+      const int planes = N * C;
+      const int G = std::max(1, std::min(16, 4096 / (H * W)));
+      const int blocks = (planes + G - 1) / G;
+      const int sm = G * H * W * 4;
+      const int cw = Q <= 8 ? 8 : (Q <= 16 ? 16 : 32);
+#define BF_MP3F(SS, CC) \
+  maxpool3_fwd_plane<SS, CC><<<blocks, 256, sm, as_stream(s)>>>(x, y, mask, planes, G, H, W, P, Q, pad)
+      if (stride == 1) {
+        if (cw == 8) BF_MP3F(1, 8); else if (cw == 16) BF_MP3F(1, 16); else BF_MP3F(1, 32);
+      } else {
+        if (cw == 8) BF_MP3F(2, 8); else if (cw == 16) BF_MP3F(2, 16); else BF_MP3F(2, 32);
+      }
+#undef BF_MP3F
       return check_launch("maxpool_forward");
     }
     maxpool_fwd_plane<<<N * C, 256, smem, as_stream(s)>>>(x, y, mask, H, W, P, Q, kernel, stride,
@@ -601,19 +630,32 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
       BF_CUDA(cudaFuncSetAttribute(maxpool_bwd_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kPlaneSmemMax),
               "maxpool smem attribute");
-      BF_CUDA(cudaFuncSetAttribute(maxpool3_bwd_plane<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
-              "maxpool smem attribute");
-      BF_CUDA(cudaFuncSetAttribute(maxpool3_bwd_plane<2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPlaneSmemMax),
-              "maxpool smem attribute");
+      const void* fns[] = {(const void*)maxpool3_bwd_plane<1, 8>,
+                           (const void*)maxpool3_bwd_plane<1, 16>,
+                           (const void*)maxpool3_bwd_plane<1, 32>,
+                           (const void*)maxpool3_bwd_plane<2, 8>,
+                           (const void*)maxpool3_bwd_plane<2, 16>,
+                           (const void*)maxpool3_bwd_plane<2, 32>};
+      for (const void* f : fns)
+        BF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kPlaneSmemMax),
+                "maxpool smem attribute");
       attr = true;
     }
     if (kernel == 3 && (stride == 1 || stride == 2)) {
-      if (stride == 1)
-        maxpool3_bwd_plane<1><<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, pad);
-      else
-        maxpool3_bwd_plane<2><<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, pad);
+      const int planes = N * C;
+      const int G = std::max(1, std::min(16, 4096 / (H * W)));
+      const int blocks = (planes + G - 1) / G;
+      const int sm = G * 2 * P * Q * 4;
+      const int cw = W <= 8 ? 8 : (W <= 16 ? 16 : 32);
+#define BF_MP3B(SS, CC) \
+  maxpool3_bwd_plane<SS, CC><<<blocks, 256, sm, as_stream(s)>>>(mask, dy, dx, planes, G, H, W, P, Q, pad)
+      if (stride == 1) {
+        if (cw == 8) BF_MP3B(1, 8); else if (cw == 16) BF_MP3B(1, 16); else BF_MP3B(1, 32);
+      } else {
+        if (cw == 8) BF_MP3B(2, 8); else if (cw == 16) BF_MP3B(2, 16); else BF_MP3B(2, 32);
+      }
+#undef BF_MP3B
       return check_launch("maxpool_backward");
     }
     maxpool_bwd_plane<<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, kernel,
