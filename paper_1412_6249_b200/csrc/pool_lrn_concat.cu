@@ -337,7 +337,7 @@ __global__ void maxpool3_fwd_plane(const float* __restrict__ x, float* __restric
                                    int P, int Q, int pad) {
   extern __shared__ float plane_all[];
   const int64_t pl0 = (int64_t)blockIdx.x * G;
-  const int g_here = (int)min<int64_t>(G, planes - pl0);
+  const int g_here = (int)(planes - pl0 < G ? planes - pl0 : G);
   const float* xp0 = x + pl0 * (int64_t)H * W;
   for (int i = threadIdx.x; i < g_here * H * W; i += blockDim.x) plane_all[i] = xp0[i];
   __syncthreads();
@@ -381,7 +381,7 @@ __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* 
                                    int Q, int pad) {
   extern __shared__ float sm[];
   const int64_t pl0 = (int64_t)blockIdx.x * G;
-  const int g_here = (int)min<int64_t>(G, planes - pl0);
+  const int g_here = (int)(planes - pl0 < G ? planes - pl0 : G);
   const int PQ = P * Q;
   float* ms_all = sm;
   float* gs_all = sm + G * PQ;
