@@ -153,6 +153,33 @@ struct Fast<LdDgradDY> {
   static bool ok(const LdDgradDY& l) { return l.g.K % 16 == 0 && l.g.stride == 1; }
 };
 
+// weight gradient, fast path: K = pixels ordered (n, p, q) with q padded to Qp
+// (Qp = 8 for Q <= 8, else a multiple of 16), so a 16-pixel chunk is one output
+// row segment (or two 8-wide rows): per element only compile-time offsets and
+// two bounds tests remain.
+struct WgradGeom {
+  int Pp, Qp;  // padded output rows / cols of the K ordering
+};
+__host__ inline WgradGeom wgrad_geom(const ConvShape& g) {
+  WgradGeom w;
+  w.Qp = g.Q <= 8 ? 8 : (g.Q + 15) / 16 * 16;
+  const int rpc = 16 / (w.Qp < 16 ? w.Qp : 16);
+  w.Pp = (g.P + rpc - 1) / rpc * rpc;
+  return w;
+}
+
+struct LdWgradDYPad {  // B(n = kout, k' = padded pixel) for the pack kernel
+  const float* dy;
+  int K, P, Q, Pp, Qp;
+  __device__ __forceinline__ float operator()(int ko, int k) const {
+    int per = Pp * Qp;
+    int n = k / per, rem = k - n * per;
+    int p = rem / Qp, q = rem - p * Qp;
+    if (p >= P || q >= Q) return 0.f;
+    return dy[(((int64_t)n * K + ko) * P + p) * Q + q];
+  }
+};
+
 // B views with the same (r, s, c) K order for the pack kernel
 struct LdFwdWPerm {  // B(n = kout, k' = (rs, c)) = w[kout][c][rs]
   const float* w;
@@ -324,7 +351,12 @@ constexpr int kKtabMax = 4096;  // k-table entries cached in shared memory per C
 
 struct Work {
   int M, N, K, BN, nst, nkb, kbps, splits, mtiles, ntiles, units, nacc, full_ktab;
+  int Pp, Qp;  // weight-gradient fast path: padded pixel grid of the K ordering
 };
+
+// MODE: 0 generic table gather, 1 channel-chunk fast path (fwd / dgrad),
+//       2 / 3 weight-gradient pixel-row fast path with 16- / 8-wide chunks
+enum { kGeneric = 0, kChannel = 1, kWgrad16 = 2, kWgrad8 = 3 };
 
 __device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& nt, int& sp) {
   sp = u % w.splits;
@@ -374,14 +406,41 @@ __device__ __forceinline__ void gather16_fast(const LA& la, const RowInfo* ktab,
   for (int j = 0; j < 16; ++j) v[j] = ldg_pred(p + j * stride, ok);
 }
 
+template <int CCW, class LA>
+__device__ __forceinline__ void gather16_wgrad(const LA& la, const Work& w, const RowInfo& ri,
+                                               int kk, const float* __restrict__ pa,
+                                               float (&v)[16]) {
+  const ConvShape& g = la.g;
+  const int per = w.Pp * w.Qp;
+  const int n = kk / per, rem = kk - n * per;
+  const int p0 = rem / w.Qp, q0 = rem - p0 * w.Qp;
+  const int st = g.stride;
+  const int ihb = p0 * st - g.pad + ri.h, iwb = q0 * st - g.pad + ri.w;
+  const int64_t off0 =
+      (int64_t)n * g.C * g.H * g.W + ri.off + (p0 * st - g.pad) * g.W + (q0 * st - g.pad);
+  const bool live = kk < w.K;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int jr = j / CCW, jc = j % CCW;
+    const int ih = ihb + jr * st, iw = iwb + jc * st;
+    const int ok = live && (p0 + jr < g.P) && (q0 + jc < g.Q) && (unsigned)ih < (unsigned)g.H &&
+                   (unsigned)iw < (unsigned)g.W;
+    v[j] = ldg_pred(pa + (ok ? off0 + (int64_t)jr * st * g.W + jc * st : 0), ok);
+  }
+}
+
 // the table/no-table choice is hoisted out of the unrolled loop so the
 // division-heavy fallback is never if-converted into the common path
-template <class SA, bool FAST, class LA>
+template <class SA, int MODE, class LA>
 __device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowInfo* ktab,
                                          const RowInfo& ri, int kbase, int kc0,
                                          const float* __restrict__ pa, unsigned hb, unsigned wb,
                                          float (&v)[16]) {
-  if (FAST)
+  if (MODE == kWgrad16)
+    gather16_wgrad<16>(la, w, ri, kbase + kc0, pa, v);
+  else if (MODE == kWgrad8)
+    gather16_wgrad<8>(la, w, ri, kbase + kc0, pa, v);
+  else if (MODE == kChannel)
     gather16_fast(la, ktab, ri, kbase, kc0, pa, hb, wb, v);
   else if (w.full_ktab)
     gather16_impl<SA, true>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
@@ -389,7 +448,7 @@ __device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowI
     gather16_impl<SA, false>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
 }
 
-template <class LA, class Epi, bool FAST>
+template <class LA, class Epi, int MODE>
 __global__ void __launch_bounds__(kAllThreads, 1)
     tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part) {
   using SA = Sep<LA>;
@@ -426,12 +485,12 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (FAST) {  // per 16-channel chunk: offset and filter tap, once per CTA
+  if (MODE == kChannel) {  // per 16-channel chunk: offset and filter tap, once per CTA
     ChunkInfo* ct = reinterpret_cast<ChunkInfo*>(ktab);
     for (int c = threadIdx.x; c < ktab_n / 16; c += kAllThreads)
       ct[c] = c * 16 < w.K ? Fast<LA>::chunk(la, c * 16)
                            : ChunkInfo{0, (short)kInvalid, (short)kInvalid};
-  } else if (w.full_ktab) {  // k -> gather offsets for the whole (padded) K extent, once per CTA
+  } else if (MODE == kGeneric && w.full_ktab) {  // k -> gather offsets, whole K, once per CTA
     for (int k = threadIdx.x; k < ktab_n; k += kAllThreads)
       ktab[k] = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
   }
@@ -455,7 +514,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       return m < w.M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
     };
     int u = blockIdx.x, i = 0, it = 0;
-    if (!FAST && !w.full_ktab) {
+    if (MODE == kGeneric && !w.full_ktab) {
       // K too long for a cached table (weight gradients: K = N*P*Q pixels):
       // the k-block's 32 gather offsets are computed per stage into a ring slot
       for (; u < w.units; u += gridDim.x) {
@@ -504,7 +563,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       int kb0 = sp * w.kbps;
       int nk = min(w.kbps, w.nkb - kb0);
       float v[16];
-      gather16<SA, FAST>(la, w, ktab, ri, kb0 * BK, kc0, pa, hb, wb, v);
+      gather16<SA, MODE>(la, w, ktab, ri, kb0 * BK, kc0, pa, hb, wb, v);
       while (true) {
         // next (unit, k-block) and its prefetch
         int u2 = u, i2 = i + 1;
@@ -524,7 +583,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           nk2 = min(w.kbps, w.nkb - kb02);
         }
 #if TC2_PREFETCH
-        if (more) gather16<SA, FAST>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
+        if (more) gather16<SA, MODE>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
 #endif
         // current k-block: split, publish to TMEM + kick off the B tile
         float big[16], small[16];
@@ -551,7 +610,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         ++it;
         if (!more) break;
 #if !TC2_PREFETCH
-        gather16<SA, FAST>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
+        gather16<SA, MODE>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
 #endif
         u = u2;
         i = i2;
@@ -656,12 +715,16 @@ inline int pick_bn(int N, int& ntiles) {
 
 template <class LA, class LB, class LBP, class Epi>
 int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, const Epi& epi,
-           float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
-  const bool fast = Fast<LA>::ok(la);
+           float* ws, int64_t ws_bytes, cudaStream_t st, const char* what, int mode = -1,
+           int Pp = 0, int Qp = 0) {
+  if (mode < 0) mode = Fast<LA>::ok(la) ? kChannel : kGeneric;
+  const bool fast = mode != kGeneric;
   Work w{};
   w.M = M;
   w.N = N;
   w.K = K;
+  w.Pp = Pp;
+  w.Qp = Qp;
   w.BN = pick_bn(N, w.ntiles);
   w.nkb = (K + BK - 1) / BK;
   w.mtiles = (M + BM - 1) / BM;
@@ -698,17 +761,20 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
 
   const int smem_cap = 227 * 1024;
   const int tail = 1024 + 16 * 8 + 64;
-  w.full_ktab = (fast || K <= kKtabMax) ? 1 : 0;
-  const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;
+  w.full_ktab = (mode == kChannel || (mode == kGeneric && K <= kKtabMax)) ? 1 : 0;
+  const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;  // as the kernel carves it
   w.nst = (int)std::min<int64_t>(STAGES, (smem_cap - tail - ktab_bytes) / stage_bytes);
   if (w.nst < 2) return -1;
   const int smem = tail + (int)(w.nst * stage_bytes) + ktab_bytes;
-  auto kern = fast ? tc2_kernel<LA, Epi, true> : tc2_kernel<LA, Epi, false>;
-  static bool configured[2] = {false, false};
-  if (!configured[fast]) {
+  auto kern = mode == kChannel ? tc2_kernel<LA, Epi, kChannel>
+             : mode == kWgrad16 ? tc2_kernel<LA, Epi, kWgrad16>
+             : mode == kWgrad8  ? tc2_kernel<LA, Epi, kWgrad8>
+                                : tc2_kernel<LA, Epi, kGeneric>;
+  static bool configured[4] = {false, false, false, false};
+  if (!configured[mode]) {
     BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap),
             "tc2 smem attribute");
-    configured[fast] = true;
+    configured[mode] = true;
   }
   // >= 120 KB of shared memory keeps one CTA (one 512-column TMEM allocation) per SM
   const int smem_req = std::max(smem, 120 << 10);
@@ -738,6 +804,13 @@ int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
                    const EpiT& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
                    const char* what) {
   if (M < 128 || K < 8) return -1;
+  const tc2::WgradGeom wg = tc2::wgrad_geom(la.g);
+  const int64_t kpad = (int64_t)la.g.N * wg.Pp * wg.Qp;
+  if (kpad < (int64_t)K * 2 && kpad < (1LL << 31)) {  // padding waste bounded: fast path
+    tc2::LdWgradDYPad lbp{lb.dy, la.g.K, la.g.P, la.g.Q, wg.Pp, wg.Qp};
+    return tc2::launch(la, lb, lbp, M, N, (int)kpad, epi, ws, ws_bytes, st, what,
+                       wg.Qp >= 16 ? tc2::kWgrad16 : tc2::kWgrad8, wg.Pp, wg.Qp);
+  }
   return tc2::launch(la, lb, lb, M, N, K, epi, ws, ws_bytes, st, what);
 }
 
