@@ -21,6 +21,7 @@
 // TMEM map (512 columns): [0, BN) fp32 accumulator; [256 + 64*s, +32) A_big
 // and [256 + 64*s + 32, +32) A_small of stage s (4 stages).
 #include <algorithm>
+#include <type_traits>
 
 #include "gemm_common.cuh"
 #include "gemm_engines.cuh"
@@ -737,7 +738,9 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned);
   const int64_t part_bytes = ws_bytes - pack_aligned;
 
-  if (fast)
+  if constexpr (std::is_same_v<LBP, LdWgradDYPad>) {
+    pack_dy_kernel<<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack);
+  } else if (fast)
     pack_b_kernel<LBP><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack);
   else
     pack_b_kernel<LB><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lb, N, K, w.BN, w.nkb, bpack);
@@ -748,7 +751,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   {
     int64_t tiles = (int64_t)w.mtiles * w.ntiles;
     if (tiles < sms) {
-      int64_t want = (sms + tiles - 1) / tiles;
+      int64_t want = sms / tiles;  // one wave: units <= SMs (ceil would leave a 2-unit tail)
       int64_t by_k = w.nkb / 4;
       int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
       w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
