@@ -324,6 +324,47 @@ __global__ void pack_b_kernel(LB lb, int N, int K, int BN, int nkb, uint8_t* __r
   }
 }
 
+
+// weight-gradient dY pack: a thread owns 4 consecutive padded pixels of one
+// row (Qp is a multiple of 8, so they never straddle rows): one decode and one
+// float4 load (or 4 scalar loads) per 16-byte chunk instead of per element
+__global__ void pack_dy_kernel(LdWgradDYPad lb, int N, int K, int BN, int nkb,
+                               uint8_t* __restrict__ out) {
+  const int tile = blockIdx.y, kb = blockIdx.x;
+  uint8_t* base = out + ((size_t)tile * nkb + kb) * 2 * BN * 128;
+  const int per = lb.Pp * lb.Qp;
+  const bool vec = (lb.Q & 3) == 0;
+  for (int i = threadIdx.x; i < BN * 8; i += blockDim.x) {
+    const int r = i >> 3, c = i & 7;
+    const int ko = tile * BN + r;
+    const int k0 = kb * BK + c * 4;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (ko < N && k0 < K) {
+      const int n = k0 / per, rem = k0 - n * per;
+      const int p = rem / lb.Qp, q = rem - p * lb.Qp;
+      if (p < lb.P) {
+        const float* src = lb.dy + (((int64_t)n * lb.K + ko) * lb.P + p) * lb.Q + q;
+        if (vec && q + 3 < lb.Q) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(src));
+          v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (q + j < lb.Q) v[j] = __ldg(src + j);
+        }
+      }
+    }
+    float4 bg, sm;
+    bg.x = to_tf32_rna(v[0]); sm.x = to_tf32_rna(v[0] - bg.x);
+    bg.y = to_tf32_rna(v[1]); sm.y = to_tf32_rna(v[1] - bg.y);
+    bg.z = to_tf32_rna(v[2]); sm.z = to_tf32_rna(v[2] - bg.z);
+    bg.w = to_tf32_rna(v[3]); sm.w = to_tf32_rna(v[3] - bg.w);
+    const uint32_t off = sw_off(r, c);
+    *reinterpret_cast<float4*>(base + off) = bg;
+    *reinterpret_cast<float4*>(base + BN * 128 + off) = sm;
+  }
+}
+
 // ---- persistent warp-specialised kernel ---------------------------------------------
 //
 // warps 0-7   : producers — A gather -> split -> tcgen05.st into the stage's TMEM
