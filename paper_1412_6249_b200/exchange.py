@@ -200,7 +200,7 @@ def setup_nccl(store, world: int, rank: int) -> None:
 
 
 def build_rank_sequence(net, world: int, rank: int, store, bucket_bytes: int = 4 << 20,
-                        nccl: bool = True):
+                        nccl: bool | None = None):
     """Full DP graph for ``world`` peers (server on device ``world``), lowered
     for ``rank``; arenas materialised in ``store``; NCCL set up when world > 1."""
     plan = ParallelPlan("data", peers=tuple(Location("local", k) for k in range(world)),
@@ -209,7 +209,9 @@ def build_rank_sequence(net, world: int, rank: int, store, bucket_bytes: int = 4
     xplan = plan_buckets(param_names(net), world, bucket_bytes)
     seq = lower_data_parallel(full, rank, xplan, net)
     materialize(store, xplan, rank)
-    if world > 1 and nccl:
+    if nccl is None:
+        nccl = world > 1
+    if nccl:  # world == 1 with nccl=True exercises the NCCL path on one GPU (tests)
         setup_nccl(store, world, rank)
     return seq, xplan
 

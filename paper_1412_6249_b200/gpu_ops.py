@@ -246,10 +246,10 @@ def _dp_exchange(ctx, op):
     world = int(op.attrs["world"])
     lr = float(op.attrs["lr"])
     lib = _L()
-    if world == 1:
+    comm = getattr(ctx.store, "_nccl", None)
+    if world == 1 and comm is None:  # single GPU: the exchange is the local update
         lib("bf_sgd_mean_update", w0, g0, o0, lr, 1, length, ctx.stream)
         return
-    comm = getattr(ctx.store, "_nccl", None)
     if comm is None:
         raise KernelError("dp_exchange: no NCCL communicator on this store "
                           "(exchange.setup_nccl)")

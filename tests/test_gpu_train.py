@@ -114,6 +114,42 @@ def test_lowered_exchange_world1_is_bitwise_the_server_graph(factory, iters):
         assert np.array_equal(st_cap.array(f"{pname}_p0"), st_ref.array(f"{pname}_p0")), pname
 
 
+def test_nccl_exchange_under_graph_capture_one_rank():
+    """The multi-GPU code path (NCCL reduce-scatter -> shard SGD -> all-gather
+    inside captured CUDA graphs), exercised with a 1-rank communicator on the
+    single GPU: bitwise equal to the local update."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1412_6249_b200.exchange import build_rank_sequence
+    from paper_1412_6249_b200.executor import CapturedSequence
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        net = cifar_convnet(batch=4, lr=0.01)
+        feed = SyntheticFeed.for_net(net, 3, spread=0.0)
+        results = []
+        for use_nccl in (False, True):
+            st = TensorStore("cuda:0")
+            seq, _ = build_rank_sequence(net, 1, 0, st, bucket_bytes=32 << 10, nccl=use_nccl)
+            assert (getattr(st, "_nccl", None) is not None) == use_nccl
+            init_params(net, st, 3, seq.layout)
+            feeder(feed, seq.layout)(0, st)
+            exe = CapturedSequence(seq, st)
+            exe.prepare()
+            for _ in range(3):
+                exe.step()
+            results.append({p: st.array(f"{p}_p0") for p, _ in net.param_shapes()})
+        for p in results[0]:
+            assert np.array_equal(results[0][p], results[1][p]), p
+    finally:
+        dist.destroy_process_group()
+
+
 def _oracle_iteration(seq, net, feed, seed):
     from oracle.serial import run_graph_serial
 
