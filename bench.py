@@ -46,6 +46,8 @@ def _args():
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--force-nccl", action="store_true",
+                    help="route the exchange through NCCL even on one GPU (plumbing test)")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="extra replays for an external profiler (ncu); no timing")
     return ap.parse_args()
@@ -223,7 +225,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    if world > 1 or args.force_nccl:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -232,7 +234,8 @@ def run_ours(args):
     store = TensorStore(dev)
     from paper_1412_6249_b200.exchange import build_rank_sequence
 
-    seq, exch = build_rank_sequence(net, world, rank, store)
+    seq, exch = build_rank_sequence(net, world, rank, store,
+                                    nccl=True if args.force_nccl else None)
     layout = seq.layout
     init_params(net, store, 7, layout)
     feed = SyntheticFeed.for_net(net, 7, peers=world, spread=0.0)
