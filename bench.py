@@ -184,7 +184,9 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cores = len(os.sched_getaffinity(0))
+    # one replica thread per core (numpy releases the GIL in its kernels), capped
+    # so the replicas' activations stay a few GB of host memory
+    cores = min(len(os.sched_getaffinity(0)), 32)
     sample = 2
     # warm-up steps are shorter than timed ones only by reuse of numpy buffers
     cpu_throughput(args.net, sample, cores, max(1, min(args.warmup, 1)))
