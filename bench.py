@@ -187,7 +187,7 @@ def run_reference(args):
     # one replica thread per core (numpy releases the GIL in its kernels), capped
     # so the replicas' activations stay a few GB of host memory
     cores = min(len(os.sched_getaffinity(0)), 32)
-    sample = 2
+    sample = 1
     # warm-up steps are shorter than timed ones only by reuse of numpy buffers
     cpu_throughput(args.net, sample, cores, max(1, min(args.warmup, 1)))
     value, times = cpu_throughput(args.net, sample, cores, args.steps)

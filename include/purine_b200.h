@@ -95,6 +95,12 @@ int bf_fc_bwd_bias(const float* dy, float* db, int n, int m, bf_stream_t stream)
 int bf_conv2d_fwd(const float* x, const float* w, const float* b, float* y,
                   int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                   int stride, int pad, float* workspace, int64_t ws_bytes, bf_stream_t stream);
+/* conv2d_forward followed by relu_forward (ops.py:359-364) in one kernel:
+   writes the pre-activation y (kept: relu_backward reads it) and relu(y) */
+int bf_conv2d_fwd_relu(const float* x, const float* w, const float* b, float* y, float* y_relu,
+                       int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                       int stride, int pad, float* workspace, int64_t ws_bytes,
+                       bf_stream_t stream);
 int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx,
                        int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                        int stride, int pad, float* workspace, int64_t ws_bytes,

@@ -48,11 +48,18 @@ int bf_set_gemm_engine(int engine) {
 int bf_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int N, int C, int H,
                   int W, int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
                   int64_t ws_bytes, bf_stream_t s) {
+  return bf_conv2d_fwd_relu(x, w, b, y, nullptr, N, C, H, W, K, R, S, P, Q, stride, pad, ws,
+                            ws_bytes, s);
+}
+
+int bf_conv2d_fwd_relu(const float* x, const float* w, const float* b, float* y, float* y_relu,
+                       int N, int C, int H, int W, int K, int R, int S, int P, int Q, int stride,
+                       int pad, float* ws, int64_t ws_bytes, bf_stream_t s) {
   if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
   ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
   LdFwdX la{x, g};
   LdRowK lb{w, (int64_t)C * R * S};
-  EpiNCHW epi{y, b, P * Q, K};
+  EpiNCHW epi{y, b, P * Q, K, y_relu};
   if (g_gemm_engine == 0) {
     int rc = tc2_conv_fwd(la, lb, N * P * Q, K, C * R * S, epi, ws, ws_bytes, as_stream(s),
                           "conv2d_forward");

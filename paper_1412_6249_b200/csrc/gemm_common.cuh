@@ -129,25 +129,36 @@ struct LdWgradDY {
 struct RowPtr {
   float* p;
   float bias_row;  // EpiT's per-row bias (0 if none)
+  int64_t relu_delta = 0;  // EpiNCHW: element offset of the fused ReLU output
 };
 
-// out[(img*Cout + n)*PQ + pq] = v (+ bias[n]);  m = img*PQ + pq
+// relu_forward's arithmetic (ops.py:359-364; elementwise.cu relu1)
+__device__ __forceinline__ float relu_value(float v) { return v > 0.f ? v : 0.f; }
+
+// out[(img*Cout + n)*PQ + pq] = v (+ bias[n]);  m = img*PQ + pq.
+// With relu_out set the epilogue also writes relu(v) there: the graph's
+// following relu_forward is fused away (dispatcher fusion plan).
 struct EpiNCHW {
   float* out;
   const float* bias;
   int PQ, Cout;
+  float* relu_out = nullptr;
   __device__ __forceinline__ void operator()(int m, int n, float v) const {
     int img = m / PQ, pq = m - img * PQ;
     if (bias) v = __fadd_rn(v, bias[n]);
-    out[((int64_t)img * Cout + n) * PQ + pq] = v;
+    const int64_t o = ((int64_t)img * Cout + n) * PQ + pq;
+    out[o] = v;
+    if (relu_out) relu_out[o] = relu_value(v);
   }
   __device__ __forceinline__ RowPtr row(int m) const {
     int img = m / PQ, pq = m - img * PQ;
-    return {out + (int64_t)img * Cout * PQ + pq, 0.f};
+    return {out + (int64_t)img * Cout * PQ + pq, 0.f, relu_out ? relu_out - out : 0};
   }
   __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
     if (bias) v = __fadd_rn(v, __ldg(bias + n));
-    r.p[(int64_t)n * PQ] = v;
+    float* p = r.p + (int64_t)n * PQ;
+    *p = v;
+    if (relu_out) p[r.relu_delta] = relu_value(v);
   }
 };
 

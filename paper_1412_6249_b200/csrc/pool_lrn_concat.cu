@@ -512,13 +512,25 @@ __global__ void bias_partial_kernel(const float* __restrict__ dy, float* __restr
   const int n0 = s * per, n1 = min(N, n0 + per);
   float acc = 0.f;
   if ((PQ & 3) == 0) {
+    // flattened (image, float4) index space, 4 independent loads per thread
+    // in flight per iteration
     const int pq4 = PQ >> 2;
-    for (int n = n0; n < n1; ++n) {
-      const float4* row = reinterpret_cast<const float4*>(dy + ((int64_t)n * K + c) * PQ);
-      for (int e = threadIdx.x; e < pq4; e += blockDim.x) {
-        float4 v = row[e];
-        acc += (v.x + v.y) + (v.z + v.w);
+    const int total = (n1 - n0) * pq4;
+    const int step = blockDim.x * 4;
+    for (int base = threadIdx.x; base < total; base += step) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < total) {
+          const int n = n0 + i / pq4, e = i - (i / pq4) * pq4;
+          v[u] = __ldg(reinterpret_cast<const float4*>(dy + ((int64_t)n * K + c) * PQ) + e);
+        } else {
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += (v[u].x + v[u].y) + (v[u].z + v[u].w);
     }
   } else {
     for (int n = n0; n < n1; ++n) {

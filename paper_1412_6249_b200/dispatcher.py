@@ -220,6 +220,7 @@ class RunContext:
     stream: int = 0
     workspace: object | None = None  # _Workspace: .data_ptr() / .numel(), lazily allocated
     lane: WorkerLane | None = None
+    fused: dict | None = None  # epilogue-fusion instructions for this operator (see _Plan)
 
 
 WORKSPACE_FLOATS = int(os.environ.get("PURINE_B200_WORKSPACE_MB", "1024")) << 18  # 1 GiB
@@ -316,6 +317,33 @@ class _Plan:
                     deps.append(p)
                     self.signals.add(p)
             self.waits[oid] = deps
+        # epilogue fusion: a relu_forward on the same stream directly after the
+        # conv2d_forward producing its input is computed by the conv epilogue
+        # (the relu operator is still dispatched, as a no-op, so dispatch order,
+        # readiness events and traces are unchanged; results are bit-identical)
+        self.fusion: dict[int, dict] = {}
+        self.fused_away: set[int] = set()
+        for oid, op in graph.operators.items():
+            if op.kind != "relu_forward":
+                continue
+            p = graph.producer_of(op.inputs[0])
+            if p is None or graph.operators[p].kind != "conv2d_forward":
+                continue
+            if self.slot[p] != self.slot[oid]:
+                continue
+            self.fusion[p] = {"relu_out": graph.tensors[op.outputs[0]].name}
+            self.fused_away.add(oid)
+
+
+FUSE_ENV = "PURINE_B200_FUSE"  # "0" disables epilogue fusion (A/B and debugging)
+
+
+def _fusion_enabled(registry) -> bool:
+    if os.environ.get(FUSE_ENV, "1") == "0":
+        return False
+    # only when both kinds run the product kernels (a user-registered kind is
+    # never bypassed)
+    return all(registry.get(k) is KINDS[k] for k in ("conv2d_forward", "relu_forward"))
 
 
 _PLAN_CACHE: dict[tuple[int, int], tuple[int, _Plan]] = {}
@@ -361,6 +389,7 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
     from . import _native
 
     failure = None
+    fuse = _fusion_enabled(registry)
     for oid in plan.order:
         op = graph.operators[oid]
         spec = registry.get(op.kind)
@@ -374,6 +403,7 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
         ctx.stream = stream.cuda_stream
         ctx.workspace = ws
         ctx.lane = lane_of(op)
+        ctx.fused = plan.fusion.get(oid) if fuse else None
         try:
             with torch.cuda.stream(stream):
                 if trace:
@@ -382,7 +412,11 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
                 delay = float(op.attrs.get("delay_s", 0.0) or 0.0)
                 if delay > 0:
                     _native.lib()("bf_delay_ns", int(delay * 1e9), ctx.stream)
-                spec.execute(ctx, op)
+                if not (fuse and oid in plan.fused_away):
+                    spec.execute(ctx, op)
+                else:  # computed by its producer's epilogue; still owns its output buffer
+                    t = graph.tensors[op.outputs[0]]
+                    store.ensure(t.name, t.shape)
                 if trace:
                     t_end = torch.cuda.Event(enable_timing=True, external=True)
                     t_end.record(stream)

@@ -102,6 +102,12 @@ def _geom(x, w, attrs):
 def _conv_fwd(ctx, op):
     x, w, b = _ins(ctx, op)
     (y,) = _outs(ctx, op)
+    fused = getattr(ctx, "fused", None)
+    if fused and "relu_out" in fused:  # the following relu_forward runs in this epilogue
+        yr = ctx.store.ensure(fused["relu_out"], y.shape)
+        _L()("bf_conv2d_fwd_relu", x.ptr, w.ptr, b.ptr, y.ptr, yr.ptr, *_geom(x, w, op.attrs),
+             *_ws(ctx), ctx.stream)
+        return
     _L()("bf_conv2d_fwd", x.ptr, w.ptr, b.ptr, y.ptr, *_geom(x, w, op.attrs), *_ws(ctx), ctx.stream)
 
 

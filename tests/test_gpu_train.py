@@ -114,6 +114,30 @@ def test_lowered_exchange_world1_is_bitwise_the_server_graph(factory, iters):
         assert np.array_equal(st_cap.array(f"{pname}_p0"), st_ref.array(f"{pname}_p0")), pname
 
 
+def test_epilogue_fusion_is_bitwise_neutral(monkeypatch):
+    """conv2d_forward + relu_forward fused in the conv epilogue produce exactly
+    the tensors of the unfused operators (every output of a GoogLeNet step)."""
+    net = googlenet(batch=2, lr=0.01)
+    seq = build_sgd_iteration(net)
+    feed = SyntheticFeed.for_net(net, 5, spread=0.0)
+    stores = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PURINE_B200_FUSE", flag)
+        st = TensorStore("cuda:0")
+        init_params(net, st, 5, seq.layout)
+        feeder(feed, seq.layout)(0, st)
+        from paper_1412_6249_b200 import run
+
+        run(seq.graphs[0], st)
+        stores.append(st)
+    g = seq.graphs[0]
+    fused = [op for op in g.operators.values() if op.kind == "relu_forward"]
+    assert fused
+    for t in g.tensors.values():
+        if stores[0].has(t.name):
+            assert np.array_equal(stores[0].array(t.name), stores[1].array(t.name)), t.name
+
+
 def test_nccl_exchange_under_graph_capture_one_rank():
     """The multi-GPU code path (NCCL reduce-scatter -> shard SGD -> all-gather
     inside captured CUDA graphs), exercised with a 1-rank communicator on the
