@@ -329,6 +329,44 @@ __global__ void maxpool_bwd_plane(const float* __restrict__ mask, const float* _
 // 3x3 windows (every GoogLeNet / NIN max-pool), stride S in {1, 2}: warps walk
 // output rows, lanes walk output columns (no per-element division), the window
 // is unrolled with clipped taps read as -inf (strict '>' never picks them).
+// global -> shared staging with 4 independent 16-byte loads in flight per
+// thread (the plain strided loop was latency-bound)
+__device__ __forceinline__ void stage_plane(float* __restrict__ dst, const float* __restrict__ src,
+                                            int n) {
+  if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (n & 3) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    const int n4 = n >> 2;
+    for (int base = threadIdx.x; base < n4; base += 4 * blockDim.x) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < n4) v[u] = __ldg(s4 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < n4) d4[i] = v[u];
+      }
+    }
+  } else {
+    for (int base = threadIdx.x; base < n; base += 4 * blockDim.x) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < n) v[u] = __ldg(src + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < n) dst[i] = v[u];
+      }
+    }
+  }
+}
+
 // A CTA owns G consecutive (n, c) planes (G > 1 for small 14x14 / 7x7 planes);
 // a warp covers 32/CW rows x CW columns so narrow rows keep the lanes busy.
 template <int S, int CW>
@@ -339,7 +377,7 @@ __global__ void maxpool3_fwd_plane(const float* __restrict__ x, float* __restric
   const int64_t pl0 = (int64_t)blockIdx.x * G;
   const int g_here = (int)(planes - pl0 < G ? planes - pl0 : G);
   const float* xp0 = x + pl0 * (int64_t)H * W;
-  for (int i = threadIdx.x; i < g_here * H * W; i += blockDim.x) plane_all[i] = xp0[i];
+  stage_plane(plane_all, xp0, g_here * H * W);
   __syncthreads();
   constexpr int RPW = 32 / CW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -385,10 +423,8 @@ __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* 
   const int PQ = P * Q;
   float* ms_all = sm;
   float* gs_all = sm + G * PQ;
-  for (int i = threadIdx.x; i < g_here * PQ; i += blockDim.x) {
-    ms_all[i] = mask[pl0 * PQ + i];
-    gs_all[i] = dy[pl0 * PQ + i];
-  }
+  stage_plane(ms_all, mask + pl0 * PQ, g_here * PQ);
+  stage_plane(gs_all, dy + pl0 * PQ, g_here * PQ);
   __syncthreads();
   constexpr int RPW = 32 / CW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
