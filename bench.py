@@ -48,6 +48,8 @@ def _args():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--force-nccl", action="store_true",
                     help="route the exchange through NCCL even on one GPU (plumbing test)")
+    ap.add_argument("--op-table", default=None,
+                    help="write the traced replay's per-operator device times (TSV) here")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="extra replays for an external profiler (ncu); no timing")
     return ap.parse_args()
@@ -313,6 +315,7 @@ def run_ours(args):
     per_kind: dict[str, float] = {}
     contraction_ms = contraction_flops = 0.0
     hbm_ms = hbm_bytes = 0.0
+    rows: dict[str, list] = {}
     for r in range(reps):
         par = texe.parity
         texe.step()
@@ -322,12 +325,19 @@ def run_ours(args):
         for gi, op, t in texe.op_times_ms(par):
             per_kind[op.kind] = per_kind.get(op.kind, 0.0) + t / (reps - 1)
             g = seq.graphs[gi]
+            row = rows.setdefault(op.name, [op.kind, 0.0, op_flops(g, op), op_bytes(g, op)])
+            row[1] += t / (reps - 1)
             if op.kind in CONTRACTION_KINDS:
                 contraction_ms += t / (reps - 1)
                 contraction_flops += op_flops(g, op) / (reps - 1)
             elif op.kind not in ("swap", "flatten_forward", "flatten_backward", "copy", "dp_exchange"):
                 hbm_ms += t / (reps - 1)
                 hbm_bytes += op_bytes(g, op) / (reps - 1)
+    if args.op_table and rank == 0:
+        with open(args.op_table, "w") as f:
+            f.write("op\tkind\tms\tgflop\tmbytes\n")
+            for name, (kind, t, fl, by) in sorted(rows.items(), key=lambda kv: -kv[1][1]):
+                f.write(f"{name}\t{kind}\t{t:.4f}\t{fl / 1e9:.3f}\t{by / 1e6:.2f}\n")
     peaks = _peaks()
     tpeak, basis = _tf32_peak(peaks)
     achieved = contraction_flops / (contraction_ms / 1e3) / 1e12 if contraction_ms else 0.0

@@ -45,7 +45,9 @@ int bf_sm_count(int device);
 int bf_has_tcgen05(void);
 /* total kernels launched by this library so far (process-wide counter) */
 long long bf_launch_count(void);
-/* select the GEMM engine: 0 = auto (tcgen05 where supported), 1 = SIMT fp32 */
+/* select the GEMM engine: 0 = auto (tcgen05 v2 > v1 where supported), 1 = SIMT fp32,
+   2 = tcgen05 v1 only, 3 = auto with the halo-staged engine v3 for stride-1 R x S convs
+   (opt-in: measured slower than v2 on GoogLeNet shapes) */
 int bf_set_gemm_engine(int engine);
 
 /* bind this library's CUDA runtime to `device` for the calling thread */
@@ -109,6 +111,13 @@ int bf_conv2d_bwd_weight(const float* x, const float* dy, float* dw,
                          int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                          int stride, int pad, float* workspace, int64_t ws_bytes,
                          bf_stream_t stream);
+/* conv2d_backward_weight + conv2d_backward_bias on the same dy (ops.py:332-352): the
+   bias sums are taken from the weight gradient's dY pass (no second read of dy);
+   db may be NULL */
+int bf_conv2d_bwd_weight_bias(const float* x, const float* dy, float* dw, float* db,
+                              int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                              int stride, int pad, float* workspace, int64_t ws_bytes,
+                              bf_stream_t stream);
 /* db[k] = sum over (n, p, q) of dy, deterministic order; workspace >= 4*K*slices bytes
    (optional: NULL falls back to one CTA per channel) */
 int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, float* workspace,

@@ -51,6 +51,7 @@ _SIGS = {
     "bf_conv2d_fwd_relu": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_data": [_p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_weight": [_p, _p, _p] + [_i] * 11 + [_p, _l, _p],
+    "bf_conv2d_bwd_weight_bias": [_p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_bias": [_p, _p, _i, _i, _i, _p, _l, _p],
     "bf_gemm_workspace_bytes": [_i] * 12,
     "bf_maxpool_fwd": [_p, _p, _p] + [_i] * 9 + [_p],

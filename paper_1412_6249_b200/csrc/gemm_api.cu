@@ -13,7 +13,7 @@ int g_gemm_engine = 0;
 template <class LA, class LB, class Epi>
 static int run_gemm(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, float* ws,
                     int64_t ws_bytes, cudaStream_t st, const char* what) {
-  if (g_gemm_engine == 0 || g_gemm_engine == 2) {
+  if (g_gemm_engine != 1) {
     int rc = tc_gemm(la, lb, M, N, K, epi, ws, ws_bytes, st, what);
     if (rc >= 0) return rc;
   }
@@ -39,8 +39,8 @@ using namespace bf;
 extern "C" {
 
 int bf_set_gemm_engine(int engine) {
-  BF_REQUIRE(engine >= 0 && engine <= 2,
-             "bf_set_gemm_engine: 0 (auto), 1 (simt), 2 (tcgen05 v1 only)");
+  BF_REQUIRE(engine >= 0 && engine <= 3,
+             "bf_set_gemm_engine: 0 (auto), 1 (simt), 2 (tcgen05 v1 only), 3 (auto + halo engine v3)");
   g_gemm_engine = engine;
   return 0;
 }
@@ -60,7 +60,11 @@ int bf_conv2d_fwd_relu(const float* x, const float* w, const float* b, float* y,
   LdFwdX la{x, g};
   LdRowK lb{w, (int64_t)C * R * S};
   EpiNCHW epi{y, b, P * Q, K, y_relu};
-  if (g_gemm_engine == 0) {
+  if (g_gemm_engine == 3) {
+    int rc = tc3_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
+    if (rc >= 0) return rc;
+  }
+  if (g_gemm_engine == 0 || g_gemm_engine == 3) {
     int rc = tc2_conv_fwd(la, lb, N * P * Q, K, C * R * S, epi, ws, ws_bytes, as_stream(s),
                           "conv2d_forward");
     if (rc >= 0) return rc;
@@ -77,7 +81,11 @@ int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx, int N, int C,
   LdDgradDY la{dy, g};
   LdDgradW lb{w, g};
   EpiNCHW epi{dx, nullptr, H * W, C};
-  if (g_gemm_engine == 0) {
+  if (g_gemm_engine == 3) {
+    int rc = tc3_conv_dgrad(g, dy, w, epi, ws, ws_bytes, as_stream(s), "conv2d_backward_data");
+    if (rc >= 0) return rc;
+  }
+  if (g_gemm_engine == 0 || g_gemm_engine == 3) {
     int rc = tc2_conv_dgrad(la, lb, N * H * W, C, K * R * S, epi, ws, ws_bytes, as_stream(s),
                             "conv2d_backward_data");
     if (rc >= 0) return rc;
@@ -89,18 +97,28 @@ int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx, int N, int C,
 int bf_conv2d_bwd_weight(const float* x, const float* dy, float* dw, int N, int C, int H, int W,
                          int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
                          int64_t ws_bytes, bf_stream_t s) {
+  return bf_conv2d_bwd_weight_bias(x, dy, dw, nullptr, N, C, H, W, K, R, S, P, Q, stride, pad,
+                                   ws, ws_bytes, s);
+}
+
+int bf_conv2d_bwd_weight_bias(const float* x, const float* dy, float* dw, float* db, int N,
+                              int C, int H, int W, int K, int R, int S, int P, int Q, int stride,
+                              int pad, float* ws, int64_t ws_bytes, bf_stream_t s) {
   if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
   ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
   LdWgradX la{x, g};
   LdWgradDY lb{dy, g};
   EpiT epi{dw, nullptr, (int64_t)C * R * S};
-  if (g_gemm_engine == 0) {
-    int rc = tc2_conv_wgrad(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
-                            "conv2d_backward_weight");
-    if (rc >= 0) return rc;
-  }
-  return run_gemm(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
+  int rc = -1;
+  bool db_done = false;
+  if (g_gemm_engine == 0 || g_gemm_engine == 3)
+    rc = tc2_conv_wgrad(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
+                        "conv2d_backward_weight", db, &db_done);
+  if (rc < 0)
+    rc = run_gemm(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
                   "conv2d_backward_weight");
+  if (rc != 0 || !db || db_done) return rc;
+  return bf_conv2d_bwd_bias(dy, db, N, K, P * Q, ws, ws_bytes, s);
 }
 
 int bf_fc_fwd(const float* x, const float* w, const float* b, float* y, int n, int d, int m,

@@ -21,10 +21,18 @@ int tc2_conv_fwd(const LdFwdX& la, const LdRowK& lb, int M, int N, int K, const 
 int tc2_conv_dgrad(const LdDgradDY& la, const LdDgradW& lb, int M, int N, int K,
                    const EpiNCHW& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
                    const char* what);
+// db != NULL: the bias gradient is fused into the dY pack when the fast path is
+// taken (*db_done = true); otherwise the caller computes it
 int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
                    const EpiT& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
-                   const char* what);
+                   const char* what, float* db = nullptr, bool* db_done = nullptr);
 
-extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only
+// tcgen05 engine v3 (gemm_tc3.cu): halo-staged stride-1 R x S convolutions
+int tc3_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNCHW& epi,
+                 float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+int tc3_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
+                   float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+
+extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in)
 
 }  // namespace bf

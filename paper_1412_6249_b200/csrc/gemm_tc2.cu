@@ -25,11 +25,11 @@
 
 #include "gemm_common.cuh"
 #include "gemm_engines.cuh"
+#include "tc_ptx.cuh"
 
 namespace bf {
 namespace tc2 {
 
-constexpr int BM = 128;
 constexpr int BK = 32;
 constexpr int STAGES = 4;
 constexpr int kProducerWarps = 8;
@@ -199,137 +199,13 @@ struct LdDgradWPerm {  // B(n = c, k' = (rs, ko)) = w[ko][c][rs]
   }
 };
 
-// ---- PTX helpers --------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(dst),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-// D[tmem] (+)= A[tmem] * B[smem desc]
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
-      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
-      "f"(v[15])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-__device__ __forceinline__ uint32_t tf32_idesc(int bn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(bn >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
-}
-// round to the nearest TF32 value (ties away from zero) in two integer ops:
-// add half a TF32 ulp to the magnitude bits, clear the 13 dropped bits
-__device__ __forceinline__ float to_tf32_rna(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-}
-__device__ __forceinline__ uint32_t sw_off(int r, int c) {
-  return (uint32_t)(r * 128 + (((c ^ r) & 7) << 4));
-}
-
-// ---- B pre-pack: [n_tile][k_block][big BN x 128B | small BN x 128B], swizzled ----
-
-template <class LB>
-__global__ void pack_b_kernel(LB lb, int N, int K, int BN, int nkb, uint8_t* __restrict__ out) {
-  const int tile = blockIdx.y, kb = blockIdx.x;
-  uint8_t* base = out + ((size_t)tile * nkb + kb) * 2 * BN * 128;
-  const int chunks = BN * 8;
-  for (int i = threadIdx.x; i < chunks; i += blockDim.x) {
-    int r = i >> 3, c = i & 7;
-    int n = tile * BN + r;
-    float4 bg, sm;
-    float v[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int k = kb * BK + c * 4 + j;
-      v[j] = (n < N && k < K) ? lb(n, k) : 0.f;
-    }
-    bg.x = to_tf32_rna(v[0]); sm.x = to_tf32_rna(v[0] - bg.x);
-    bg.y = to_tf32_rna(v[1]); sm.y = to_tf32_rna(v[1] - bg.y);
-    bg.z = to_tf32_rna(v[2]); sm.z = to_tf32_rna(v[2] - bg.z);
-    bg.w = to_tf32_rna(v[3]); sm.w = to_tf32_rna(v[3] - bg.w);
-    uint32_t off = sw_off(r, c);
-    *reinterpret_cast<float4*>(base + off) = bg;
-    *reinterpret_cast<float4*>(base + BN * 128 + off) = sm;
-  }
-}
-
+using namespace tcu;
 
 // weight-gradient dY pack: a thread owns 4 consecutive padded pixels of one
 // row (Qp is a multiple of 8, so they never straddle rows): one decode and one
 // float4 load (or 4 scalar loads) per 16-byte chunk instead of per element
 __global__ void pack_dy_kernel(LdWgradDYPad lb, int N, int K, int BN, int nkb,
-                               uint8_t* __restrict__ out) {
+                               uint8_t* __restrict__ out, float* __restrict__ bias_part) {
   const int tile = blockIdx.y, kb = blockIdx.x;
   uint8_t* base = out + ((size_t)tile * nkb + kb) * 2 * BN * 128;
   const int per = lb.Pp * lb.Qp;
@@ -362,7 +238,31 @@ __global__ void pack_dy_kernel(LdWgradDYPad lb, int N, int K, int BN, int nkb,
     const uint32_t off = sw_off(r, c);
     *reinterpret_cast<float4*>(base + off) = bg;
     *reinterpret_cast<float4*>(base + BN * 128 + off) = sm;
+    if (bias_part) {  // fused bias gradient: this k-block's 32-pixel sum per output channel
+      float acc = __fadd_rn(__fadd_rn(v[0], v[1]), __fadd_rn(v[2], v[3]));
+      acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+      acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+      acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+      if (c == 0 && ko < N) bias_part[(size_t)ko * nkb + kb] = acc;
+    }
   }
+}
+
+// db[ko] = sum over k-blocks of the pack kernel's partials, in a fixed order
+// (strided per thread, then a shared-memory tree): deterministic
+__global__ void bias_blocks_finish_kernel(const float* __restrict__ part, int nkb,
+                                          float* __restrict__ db) {
+  __shared__ float red[256];
+  const float* row = part + (size_t)blockIdx.x * nkb;
+  float acc = 0.f;
+  for (int kb = threadIdx.x; kb < nkb; kb += 256) acc = __fadd_rn(acc, __ldg(row + kb));
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = __fadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) db[blockIdx.x] = red[0];
 }
 
 // ---- persistent warp-specialised kernel ---------------------------------------------
@@ -758,7 +658,7 @@ inline int pick_bn(int N, int& ntiles) {
 template <class LA, class LB, class LBP, class Epi>
 int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, const Epi& epi,
            float* ws, int64_t ws_bytes, cudaStream_t st, const char* what, int mode = -1,
-           int Pp = 0, int Qp = 0) {
+           int Pp = 0, int Qp = 0, float* bias_out = nullptr) {
   if (mode < 0) mode = Fast<LA>::ok(la) ? kChannel : kGeneric;
   const bool fast = mode != kGeneric;
   Work w{};
@@ -776,11 +676,21 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   const int64_t pack_aligned = (pack_bytes + 1023) / 1024 * 1024;
   if (!ws || ws_bytes < pack_aligned) return -1;
   uint8_t* bpack = reinterpret_cast<uint8_t*>(ws);
-  float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned);
-  const int64_t part_bytes = ws_bytes - pack_aligned;
+  // fused bias gradient (weight-gradient pack only): per (channel, k-block) partials
+  const int64_t bias_bytes = bias_out ? ((int64_t)N * w.nkb * 4 + 1023) / 1024 * 1024 : 0;
+  if (ws_bytes < pack_aligned + bias_bytes) return -1;
+  float* bias_ws = bias_out ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned)
+                            : nullptr;
+  float* part_ws =
+      reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned + bias_bytes);
+  const int64_t part_bytes = ws_bytes - pack_aligned - bias_bytes;
 
   if constexpr (std::is_same_v<LBP, LdWgradDYPad>) {
-    pack_dy_kernel<<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack);
+    pack_dy_kernel<<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack, bias_ws);
+    if (bias_out) {
+      if (int rc = check_launch(what)) return rc;
+      bias_blocks_finish_kernel<<<N, 256, 0, st>>>(bias_ws, w.nkb, bias_out);
+    }
   } else if (fast)
     pack_b_kernel<LBP><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack);
   else
@@ -839,21 +749,24 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
 // conv forward / stride-1 data gradient through engine v2; -1 = not taken
 int tc2_conv_fwd(const LdFwdX& la, const LdRowK& lb, int M, int N, int K, const EpiNCHW& epi,
                  float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
-  if (M < 128 || K < 8) return -1;
+  if (K < 8) return -1;
   tc2::LdFwdWPerm lbp{lb.p, la.g.C, la.g.R * la.g.S};
   return tc2::launch(la, lb, lbp, M, N, K, epi, ws, ws_bytes, st, what);
 }
 
 int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
                    const EpiT& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
-                   const char* what) {
-  if (M < 128 || K < 8) return -1;
+                   const char* what, float* db, bool* db_done) {
+  if (db_done) *db_done = false;
+  if (K < 8) return -1;
   const tc2::WgradGeom wg = tc2::wgrad_geom(la.g);
   const int64_t kpad = (int64_t)la.g.N * wg.Pp * wg.Qp;
   if (kpad < (int64_t)K * 2 && kpad < (1LL << 31)) {  // padding waste bounded: fast path
     tc2::LdWgradDYPad lbp{lb.dy, la.g.K, la.g.P, la.g.Q, wg.Pp, wg.Qp};
-    return tc2::launch(la, lb, lbp, M, N, (int)kpad, epi, ws, ws_bytes, st, what,
-                       wg.Qp >= 16 ? tc2::kWgrad16 : tc2::kWgrad8, wg.Pp, wg.Qp);
+    const int rc = tc2::launch(la, lb, lbp, M, N, (int)kpad, epi, ws, ws_bytes, st, what,
+                               wg.Qp >= 16 ? tc2::kWgrad16 : tc2::kWgrad8, wg.Pp, wg.Qp, db);
+    if (rc == 0 && db_done) *db_done = db != nullptr;
+    return rc;
   }
   return tc2::launch(la, lb, lb, M, N, K, epi, ws, ws_bytes, st, what);
 }

@@ -333,6 +333,20 @@ class _Plan:
                 continue
             self.fusion[p] = {"relu_out": graph.tensors[op.outputs[0]].name}
             self.fused_away.add(oid)
+        # bias gradient: a conv2d_backward_bias on the same stream after the
+        # conv2d_backward_weight reading the same dy takes its sums from the
+        # weight gradient's pass over dy (within tolerance, not bit-identical to
+        # the stand-alone bias kernel: different summation blocking)
+        pos = {oid: i for i, oid in enumerate(self.order)}
+        for oid, op in graph.operators.items():
+            if op.kind != "conv2d_backward_bias":
+                continue
+            sib = [c for c, _ in graph.consumers_of(op.inputs[0])
+                   if graph.operators[c].kind == "conv2d_backward_weight"
+                   and self.slot[c] == self.slot[oid] and pos[c] < pos[oid] and c not in self.fusion]
+            if sib:
+                self.fusion[sib[0]] = {"db": graph.tensors[op.outputs[0]].name}
+                self.fused_away.add(oid)
 
 
 FUSE_ENV = "PURINE_B200_FUSE"  # "0" disables epilogue fusion (A/B and debugging)
@@ -343,7 +357,9 @@ def _fusion_enabled(registry) -> bool:
         return False
     # only when both kinds run the product kernels (a user-registered kind is
     # never bypassed)
-    return all(registry.get(k) is KINDS[k] for k in ("conv2d_forward", "relu_forward"))
+    return all(registry.get(k) is KINDS[k] for k in ("conv2d_forward", "relu_forward",
+                                                      "conv2d_backward_weight",
+                                                      "conv2d_backward_bias"))
 
 
 _PLAN_CACHE: dict[tuple[int, int], tuple[int, _Plan]] = {}

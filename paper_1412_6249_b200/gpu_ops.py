@@ -115,6 +115,9 @@ def _conv_bwd_parts(ctx, attrs, x, w, dy, dx, dw, db):
     g = _geom(x, w, attrs)
     lib = _L()
     # weight and bias first: they feed the parameter exchange; data last
+    if dw is not None and db is not None:  # one pass over dy for both
+        lib("bf_conv2d_bwd_weight_bias", x.ptr, dy.ptr, dw.ptr, db.ptr, *g, *_ws(ctx), ctx.stream)
+        dw = db = None
     if dw is not None:
         lib("bf_conv2d_bwd_weight", x.ptr, dy.ptr, dw.ptr, *g, *_ws(ctx), ctx.stream)
     if db is not None:
@@ -138,7 +141,11 @@ def _conv_bwd_data(ctx, op):
 def _conv_bwd_weight(ctx, op):
     x, w, dy = _ins(ctx, op)
     (dw,) = _outs(ctx, op)
-    _conv_bwd_parts(ctx, op.attrs, x, w, dy, None, dw, None)
+    fused = getattr(ctx, "fused", None)
+    db = None
+    if fused and "db" in fused:  # the sibling conv2d_backward_bias on the same dy
+        db = ctx.store.ensure(fused["db"], (w.shape[0],))
+    _conv_bwd_parts(ctx, op.attrs, x, w, dy, None, dw, db)
 
 
 def _conv_bwd_bias(ctx, op):

@@ -41,12 +41,28 @@ CONV_CASES = [
     (2, 160, 7, 7, 320, 3, 1, 1, False),          # inception 5a 3x3
     (1, 3, 224, 224, 96, 11, 4, 0, True),         # NIN conv1
     (2, 3, 13, 13, 8, 3, 2, 1, False),            # strided dgrad
+    (2, 96, 14, 14, 208, 3, 1, 1, False),         # inception 4a 3x3 (dgrad: 208 = 6.5 blocks)
+    (4, 48, 7, 7, 128, 5, 1, 2, False),           # inception 5b 5x5 (partial channel block)
 ]
 
 
+@pytest.fixture(params=[0, 3], ids=["auto", "halo-v3"])
+def gemm_engine(request):
+    """0 = default engine choice; 3 = also route stride-1 R x S convolutions
+    through the opt-in halo-staged engine v3 (gemm_tc3.cu)."""
+    from paper_1412_6249_b200 import _native
+
+    lib = _native.lib()
+    lib("bf_set_gemm_engine", request.param)
+    yield request.param
+    lib("bf_set_gemm_engine", 0)
+
+
 @pytest.mark.parametrize("case", CONV_CASES, ids=lambda c: "x".join(map(str, c[:7])))
-def test_conv_forward_backward(case):
+def test_conv_forward_backward(case, gemm_engine):
     n, c, h, w, k, r, s, p, fl = case
+    if gemm_engine == 3 and not (s == 1 and r > 1):
+        pytest.skip("engine v3 only takes stride-1 spatial filters")
     x = rnd(n, c, h, w)
     wt = rnd(k, c, r, r, scale=1.0 / np.sqrt(c * r * r))
     b = rnd(k)

@@ -114,9 +114,12 @@ def test_lowered_exchange_world1_is_bitwise_the_server_graph(factory, iters):
         assert np.array_equal(st_cap.array(f"{pname}_p0"), st_ref.array(f"{pname}_p0")), pname
 
 
-def test_epilogue_fusion_is_bitwise_neutral(monkeypatch):
+def test_epilogue_fusion_is_neutral(monkeypatch):
     """conv2d_forward + relu_forward fused in the conv epilogue produce exactly
-    the tensors of the unfused operators (every output of a GoogLeNet step)."""
+    the tensors of the unfused operators (every output of a GoogLeNet step);
+    the bias gradients summed inside the weight gradient's dY pass agree with
+    the stand-alone bias kernel at the contraction tolerance (different
+    summation blocking, so not bit for bit) and leave everything else exact."""
     net = googlenet(batch=2, lr=0.01)
     seq = build_sgd_iteration(net)
     feed = SyntheticFeed.for_net(net, 5, spread=0.0)
@@ -133,9 +136,20 @@ def test_epilogue_fusion_is_bitwise_neutral(monkeypatch):
     g = seq.graphs[0]
     fused = [op for op in g.operators.values() if op.kind == "relu_forward"]
     assert fused
+    bias_grads = {g.tensors[op.outputs[0]].name for op in g.operators.values()
+                  if op.kind == "conv2d_backward_bias"}
+    assert bias_grads
+    for op in g.operators.values():  # and the bias updates computed from them
+        if any(g.tensors[t].name in bias_grads for t in op.inputs):
+            bias_grads |= {g.tensors[t].name for t in op.outputs}
     for t in g.tensors.values():
-        if stores[0].has(t.name):
-            assert np.array_equal(stores[0].array(t.name), stores[1].array(t.name)), t.name
+        if not stores[0].has(t.name):
+            continue
+        a, b = stores[0].array(t.name), stores[1].array(t.name)
+        if t.name in bias_grads:
+            assert_close(b, a, rtol=RTOL, atol=ATOL * max(1.0, float(np.abs(a).max())), what=t.name)
+        else:
+            assert np.array_equal(a, b), t.name
 
 
 def test_nccl_exchange_under_graph_capture_one_rank():
