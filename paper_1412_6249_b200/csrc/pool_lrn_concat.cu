@@ -413,127 +413,311 @@ __global__ void maxpool3_fwd_plane(const float* __restrict__ x, float* __restric
   }
 }
 
+// (mask, dy) interleaved into float2 pairs while staging: one 8-byte shared
+// load per candidate window in the gather below
+__device__ __forceinline__ void stage_pairs(float2* __restrict__ dst, const float* __restrict__ m,
+                                            const float* __restrict__ g, int n) {
+  if ((((reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(g)) & 15) == 0) &&
+      (n & 3) == 0) {
+    const float4* m4 = reinterpret_cast<const float4*>(m);
+    const float4* g4 = reinterpret_cast<const float4*>(g);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    const int n4 = n >> 2;
+    for (int base = threadIdx.x; base < n4; base += 2 * blockDim.x) {
+      float4 mv[2], gv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < n4) {
+          mv[u] = __ldg(m4 + i);
+          gv[u] = __ldg(g4 + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = base + u * blockDim.x;
+        if (i < n4) {
+          d4[2 * i] = make_float4(mv[u].x, gv[u].x, mv[u].y, gv[u].y);
+          d4[2 * i + 1] = make_float4(mv[u].z, gv[u].z, mv[u].w, gv[u].w);
+        }
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = make_float2(__ldg(m + i), __ldg(g + i));
+  }
+}
+
+// Gather form (bit-exact with the oracle's raster-order scatter): pixel (h, w)
+// sums, in window raster order, dy of the windows whose argmax it is.  At most
+// ceil(3/S) windows cover it per axis; every candidate is evaluated branch-free
+// (clamped index, select of +0.0: acc starts at +0.0 and can never become
+// -0.0, so adding +0.0 is the identity).
 template <int S, int CW>
 __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
                                    float* __restrict__ dx, int planes, int G, int H, int W, int P,
                                    int Q, int pad) {
-  extern __shared__ float sm[];
+  extern __shared__ float2 pairs_all[];
   const int64_t pl0 = (int64_t)blockIdx.x * G;
   const int g_here = (int)(planes - pl0 < G ? planes - pl0 : G);
   const int PQ = P * Q;
-  float* ms_all = sm;
-  float* gs_all = sm + G * PQ;
-  stage_plane(ms_all, mask + pl0 * PQ, g_here * PQ);
-  stage_plane(gs_all, dy + pl0 * PQ, g_here * PQ);
+  stage_pairs(pairs_all, mask + pl0 * PQ, dy + pl0 * PQ, g_here * PQ);
   __syncthreads();
   constexpr int RPW = 32 / CW;
+  constexpr int NA = (3 + S - 1) / S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int roff = lane / CW, col = lane % CW;
   for (int rr = warp * RPW + roff; rr < g_here * H; rr += nw * RPW) {
     const int g = rr / H, h = rr - g * H;
-    const float* ms = ms_all + g * PQ;
-    const float* gs = gs_all + g * PQ;
-    float* dp = dx + (pl0 + g) * (int64_t)H * W;
+    const float2* pr = pairs_all + g * PQ;
+    float* dp = dx + (pl0 + g) * (int64_t)H * W + h * W;
     // output rows whose window covers h: p*S - pad <= h <= p*S - pad + 2
     const int hp = h + pad;
     const int p0 = hp < 3 ? 0 : (hp - 3) / S + 1;
     const int p1 = min(hp / S + 1, P);
+    int prow[NA];
+    bool pok[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      pok[a] = p0 + a < p1;
+      prow[a] = (pok[a] ? p0 + a : 0) * Q;
+    }
+    const int hw0 = h * W;
     for (int w = col; w < W; w += CW) {
       const int wp = w + pad;
       const int q0 = wp < 3 ? 0 : (wp - 3) / S + 1;
       const int q1 = min(wp / S + 1, Q);
-      const float me = (float)(h * W + w);
+      const float me = (float)(hw0 + w);
       float acc = 0.f;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int p = p0 + a;
-        if (p < p1) {
+      for (int a = 0; a < NA; ++a) {
 #pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            const int q = q0 + b;
-            if (q < q1 && ms[p * Q + q] == me) acc = __fadd_rn(acc, gs[p * Q + q]);
-          }
+        for (int b = 0; b < NA; ++b) {
+          const bool ok = pok[a] && q0 + b < q1;
+          const float2 mg = pr[prow[a] + (ok ? q0 + b : 0)];
+          acc = __fadd_rn(acc, (ok && mg.x == me) ? mg.y : 0.f);
         }
       }
-      dp[h * W + w] = acc;
+      dp[w] = acc;
     }
   }
 }
 
-// LRN, one thread per (n, pixel) walking the channels with a 5-wide register
-// window (size == 5, the GoogLeNet / AlexNet setting): each input is read once.
-// Out-of-range window slots hold +0.0, which leaves the in-order sums unchanged.
-__global__ void lrn5_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
-                                float* __restrict__ scale, int N, int C, int HW, float a_n,
-                                float beta, float kk) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)N * HW) return;
-  int n = (int)(t / HW), hw = (int)(t - (int64_t)n * HW);
-  const float* xp = x + (int64_t)n * C * HW + hw;
-  float* yp = y + (int64_t)n * C * HW + hw;
-  float* sp = scale + (int64_t)n * C * HW + hw;
-  // window w0..w4 = sq[c-2 .. c+2]
-  float w0 = 0.f, w1 = 0.f, w2, w3, w4;
-  float xc = xp[0];
-  w2 = __fmul_rn(xc, xc);
-  float x1 = C > 1 ? xp[HW] : 0.f;
-  w3 = C > 1 ? __fmul_rn(x1, x1) : 0.f;
-  float x2 = C > 2 ? xp[2 * (int64_t)HW] : 0.f;
-  w4 = C > 2 ? __fmul_rn(x2, x2) : 0.f;
-  for (int c = 0; c < C; ++c) {
-    float acc = 0.f;
-    acc = __fadd_rn(acc, w0);
-    acc = __fadd_rn(acc, w1);
-    acc = __fadd_rn(acc, w2);
-    acc = __fadd_rn(acc, w3);
-    acc = __fadd_rn(acc, w4);
-    float sc = __fadd_rn(kk, __fmul_rn(a_n, acc));
-    sp[(int64_t)c * HW] = sc;
-    yp[(int64_t)c * HW] = __fmul_rn(xc, powf(sc, -beta));
-    // slide: next channel
-    float xn = x1;
-    x1 = x2;
-    x2 = (c + 3 < C) ? xp[(int64_t)(c + 3) * HW] : 0.f;
-    w0 = w1;
-    w1 = w2;
-    w2 = w3;
-    w3 = w4;
-    w4 = (c + 3 < C) ? __fmul_rn(x2, x2) : 0.f;
-    xc = xn;
+// Stride-2 3x3 backward: a thread owns the 2x2 pixel block (h0, w0) = (2i - pad,
+// 2j - pad) + {0,1}^2.  On the padded grid an even row is the bottom row of
+// window i-1 and the top row of window i, an odd row the middle row of window
+// i (same for columns), so the block is covered by exactly the windows
+// (i-1, j-1), (i-1, j), (i, j-1), (i, j): one 8-byte shared load each and 9
+// argmax tests for 4 pixels, visited in window raster order (bit-exact).
+template <int CW>
+__global__ void maxpool3s2_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
+                                     float* __restrict__ dx, int planes, int G, int H, int W,
+                                     int P, int Q, int pad) {
+  extern __shared__ float2 pairs_all[];
+  const int64_t pl0 = (int64_t)blockIdx.x * G;
+  const int g_here = (int)(planes - pl0 < G ? planes - pl0 : G);
+  const int PQ = P * Q;
+  stage_pairs(pairs_all, mask + pl0 * PQ, dy + pl0 * PQ, g_here * PQ);
+  __syncthreads();
+  constexpr int RPW = 32 / CW;
+  const int BI = (H + pad + 1) / 2, BJ = (W + pad + 1) / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int roff = lane / CW, col = lane % CW;
+  for (int rr = warp * RPW + roff; rr < g_here * BI; rr += nw * RPW) {
+    const int g = rr / BI, i = rr - g * BI;
+    const float2* pr = pairs_all + g * PQ;
+    float* dp = dx + (pl0 + g) * (int64_t)H * W;
+    const int h0 = 2 * i - pad;
+    const bool r0 = h0 >= 0, r1 = h0 + 1 < H;  // block rows inside the plane
+    const bool pa = i - 1 >= 0 && i - 1 < P, pb = i < P;
+    const int rowa = (pa ? i - 1 : 0) * Q, rowb = (pb ? i : 0) * Q;
+    for (int j = col; j < BJ; j += CW) {
+      const int w0 = 2 * j - pad;
+      const bool qa = j - 1 >= 0 && j - 1 < Q, qb = j < Q;
+      const float2 wAA = pr[rowa + (qa ? j - 1 : 0)];
+      const float2 wAB = pr[rowa + (qb ? j : 0)];
+      const float2 wBA = pr[rowb + (qa ? j - 1 : 0)];
+      const float2 wBB = pr[rowb + (qb ? j : 0)];
+      const float e00 = (float)(h0 * W + w0);
+      const float e01 = e00 + 1.f, e10 = e00 + (float)W, e11 = e10 + 1.f;
+      float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+      // window (i-1, j-1): pixel (0,0)
+      a00 = __fadd_rn(a00, (pa && qa && wAA.x == e00) ? wAA.y : 0.f);
+      // window (i-1, j): pixels (0,0), (0,1)
+      a00 = __fadd_rn(a00, (pa && qb && wAB.x == e00) ? wAB.y : 0.f);
+      a01 = __fadd_rn(a01, (pa && qb && wAB.x == e01) ? wAB.y : 0.f);
+      // window (i, j-1): pixels (0,0), (1,0)
+      a00 = __fadd_rn(a00, (pb && qa && wBA.x == e00) ? wBA.y : 0.f);
+      a10 = __fadd_rn(a10, (pb && qa && wBA.x == e10) ? wBA.y : 0.f);
+      // window (i, j): all four
+      const bool bb = pb && qb;
+      a00 = __fadd_rn(a00, (bb && wBB.x == e00) ? wBB.y : 0.f);
+      a01 = __fadd_rn(a01, (bb && wBB.x == e01) ? wBB.y : 0.f);
+      a10 = __fadd_rn(a10, (bb && wBB.x == e10) ? wBB.y : 0.f);
+      a11 = __fadd_rn(a11, (bb && wBB.x == e11) ? wBB.y : 0.f);
+      const bool c0 = w0 >= 0, c1 = w0 + 1 < W;
+      if (r0) {
+        if (c0) dp[h0 * W + w0] = a00;
+        if (c1) dp[h0 * W + w0 + 1] = a01;
+      }
+      if (r1) {
+        if (c0) dp[(h0 + 1) * W + w0] = a10;
+        if (c1) dp[(h0 + 1) * W + w0 + 1] = a11;
+      }
+    }
   }
 }
 
+// LRN, one thread per (n, V consecutive pixels) walking the channels with a
+// 5-wide register window (size == 5, the GoogLeNet / AlexNet setting): every
+// input element is loaded exactly once (V = 4: 16-byte loads and stores).
+// Out-of-range window slots hold +0.0, which leaves the in-order sums unchanged.
+#ifndef LRN_VEC
+#define LRN_VEC 4
+#endif
+template <int V>
+struct Vec;
+template <>
+struct Vec<1> {
+  __device__ static void ld(const float* p, float (&v)[1]) { v[0] = __ldg(p); }
+  __device__ static void st(float* p, const float (&v)[1]) { *p = v[0]; }
+};
+template <>
+struct Vec<4> {
+  __device__ static void ld(const float* p, float (&v)[4]) {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  }
+  __device__ static void st(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+
+template <int V>
+__global__ void lrn5_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
+                                float* __restrict__ scale, int N, int C, int HW, float a_n,
+                                float beta, float kk) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int HWV = HW / V;
+  if (t >= (int64_t)N * HWV) return;
+  const int n = (int)(t / HWV), hw = (int)(t - (int64_t)n * HWV) * V;
+  const int64_t base = (int64_t)n * C * HW + hw;
+  // per lane: squares window w0..w4 = sq[c-2 .. c+2], inputs x0..x2 = x[c .. c+2]
+  float w[5][V], xs[3][V];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    if (j < C) Vec<V>::ld(x + base + (int64_t)j * HW, xs[j]);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (j >= C) xs[j][v] = 0.f;
+      w[2 + j][v] = j < C ? __fmul_rn(xs[j][v], xs[j][v]) : 0.f;
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) w[0][v] = w[1][v] = 0.f;
+  for (int c = 0; c < C; ++c) {
+    float xn[V];
+    const bool more = c + 3 < C;
+    if (more) Vec<V>::ld(x + base + (int64_t)(c + 3) * HW, xn);
+    float sc[V], yv[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float acc = 0.f;
+      acc = __fadd_rn(acc, w[0][v]);
+      acc = __fadd_rn(acc, w[1][v]);
+      acc = __fadd_rn(acc, w[2][v]);
+      acc = __fadd_rn(acc, w[3][v]);
+      acc = __fadd_rn(acc, w[4][v]);
+      sc[v] = __fadd_rn(kk, __fmul_rn(a_n, acc));
+      yv[v] = __fmul_rn(xs[0][v], powf(sc[v], -beta));
+    }
+    Vec<V>::st(scale + base + (int64_t)c * HW, sc);
+    Vec<V>::st(y + base + (int64_t)c * HW, yv);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      if (!more) xn[v] = 0.f;
+      w[0][v] = w[1][v];
+      w[1][v] = w[2][v];
+      w[2][v] = w[3][v];
+      w[3][v] = w[4][v];
+      w[4][v] = more ? __fmul_rn(xn[v], xn[v]) : 0.f;
+      xs[0][v] = xs[1][v];
+      xs[1][v] = xs[2][v];
+      xs[2][v] = xn[v];
+    }
+  }
+}
+
+// backward: x, y, scale and dy each loaded once (y as given: the operator's
+// contract, ops-level, takes the forward output as an input); the powf is
+// shared between the entering element's ratio and its later centre term.
+template <int V>
 __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                 const float* __restrict__ scale, const float* __restrict__ dy,
                                 float* __restrict__ dx, int N, int C, int HW, float coef,
                                 float beta) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= (int64_t)N * HW) return;
-  int n = (int)(t / HW), hw = (int)(t - (int64_t)n * HW);
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int HWV = HW / V;
+  if (t >= (int64_t)N * HWV) return;
+  const int n = (int)(t / HWV), hw = (int)(t - (int64_t)n * HWV) * V;
   const int64_t base = (int64_t)n * C * HW + hw;
-  auto ratio = [&](int c) -> float {
-    int64_t j = base + (int64_t)c * HW;
-    return __fdiv_rn(__fmul_rn(dy[j], y[j]), scale[j]);
+  // r[0..4] = ratio[c-2 .. c+2] = dy*y/scale;  for c..c+2 also x, dy, scale^-beta
+  float r[5][V], xs[3][V], ds[3][V], pw[3][V];
+  auto enter = [&](int j, float (&xv)[V], float (&dv)[V], float (&pv)[V], float (&rv)[V]) {
+    float sv[V], yv[V];
+    Vec<V>::ld(x + base + (int64_t)j * HW, xv);
+    Vec<V>::ld(y + base + (int64_t)j * HW, yv);
+    Vec<V>::ld(dy + base + (int64_t)j * HW, dv);
+    Vec<V>::ld(scale + base + (int64_t)j * HW, sv);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      pv[v] = powf(sv[v], -beta);
+      rv[v] = __fdiv_rn(__fmul_rn(dv[v], yv[v]), sv[v]);
+    }
   };
-  float r0 = 0.f, r1 = 0.f, r2 = ratio(0);
-  float r3 = C > 1 ? ratio(1) : 0.f;
-  float r4 = C > 2 ? ratio(2) : 0.f;
+#pragma unroll
+  for (int v = 0; v < V; ++v) r[0][v] = r[1][v] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    if (j < C) {
+      enter(j, xs[j], ds[j], pw[j], r[2 + j]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) xs[j][v] = ds[j][v] = pw[j][v] = r[2 + j][v] = 0.f;
+    }
+  }
   for (int c = 0; c < C; ++c) {
-    float acc = 0.f;
-    acc = __fadd_rn(acc, r0);
-    acc = __fadd_rn(acc, r1);
-    acc = __fadd_rn(acc, r2);
-    acc = __fadd_rn(acc, r3);
-    acc = __fadd_rn(acc, r4);
-    int64_t i = base + (int64_t)c * HW;
-    float a = __fmul_rn(dy[i], powf(scale[i], -beta));
-    float b = __fmul_rn(__fmul_rn(coef, x[i]), acc);
-    dx[i] = __fsub_rn(a, b);
-    r0 = r1;
-    r1 = r2;
-    r2 = r3;
-    r3 = r4;
-    r4 = (c + 3 < C) ? ratio(c + 3) : 0.f;
+    float out[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float acc = 0.f;
+      acc = __fadd_rn(acc, r[0][v]);
+      acc = __fadd_rn(acc, r[1][v]);
+      acc = __fadd_rn(acc, r[2][v]);
+      acc = __fadd_rn(acc, r[3][v]);
+      acc = __fadd_rn(acc, r[4][v]);
+      const float a = __fmul_rn(ds[0][v], pw[0][v]);
+      const float b = __fmul_rn(__fmul_rn(coef, xs[0][v]), acc);
+      out[v] = __fsub_rn(a, b);
+    }
+    Vec<V>::st(dx + base + (int64_t)c * HW, out);
+    float xn[V], dn[V], pn[V], rn[V];
+    if (c + 3 < C) {
+      enter(c + 3, xn, dn, pn, rn);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) xn[v] = dn[v] = pn[v] = rn[v] = 0.f;
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      r[0][v] = r[1][v];
+      r[1][v] = r[2][v];
+      r[2][v] = r[3][v];
+      r[3][v] = r[4][v];
+      r[4][v] = rn[v];
+      xs[0][v] = xs[1][v]; xs[1][v] = xs[2][v]; xs[2][v] = xn[v];
+      ds[0][v] = ds[1][v]; ds[1][v] = ds[2][v]; ds[2][v] = dn[v];
+      pw[0][v] = pw[1][v]; pw[1][v] = pw[2][v]; pw[2][v] = pn[v];
+    }
   }
 }
 
@@ -678,12 +862,12 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
       BF_CUDA(cudaFuncSetAttribute(maxpool_bwd_plane, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kPlaneSmemMax),
               "maxpool smem attribute");
-      const void* fns[] = {(const void*)maxpool3_bwd_plane<1, 8>,
+      const void* fns[] = {(const void*)maxpool3s2_bwd_plane<8>,
+                           (const void*)maxpool3s2_bwd_plane<16>,
+                           (const void*)maxpool3s2_bwd_plane<32>,
+                           (const void*)maxpool3_bwd_plane<1, 8>,
                            (const void*)maxpool3_bwd_plane<1, 16>,
-                           (const void*)maxpool3_bwd_plane<1, 32>,
-                           (const void*)maxpool3_bwd_plane<2, 8>,
-                           (const void*)maxpool3_bwd_plane<2, 16>,
-                           (const void*)maxpool3_bwd_plane<2, 32>};
+                           (const void*)maxpool3_bwd_plane<1, 32>};
       for (const void* f : fns)
         BF_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      kPlaneSmemMax),
@@ -701,7 +885,13 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
       if (stride == 1) {
         if (cw == 8) BF_MP3B(1, 8); else if (cw == 16) BF_MP3B(1, 16); else BF_MP3B(1, 32);
       } else {
-        if (cw == 8) BF_MP3B(2, 8); else if (cw == 16) BF_MP3B(2, 16); else BF_MP3B(2, 32);
+        const int bj = (W + pad + 1) / 2;
+        const int cw2 = bj <= 8 ? 8 : (bj <= 16 ? 16 : 32);
+#define BF_MP3B2(CC)                                                                            \
+  maxpool3s2_bwd_plane<CC><<<blocks, 256, sm, as_stream(s)>>>(mask, dy, dx, planes, G, H, W, P, \
+                                                              Q, pad)
+        if (cw2 == 8) BF_MP3B2(8); else if (cw2 == 16) BF_MP3B2(16); else BF_MP3B2(32);
+#undef BF_MP3B2
       }
 #undef BF_MP3B
       return check_launch("maxpool_backward");
@@ -742,8 +932,13 @@ int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int 
   float a_n = alpha / (float)size;
   if (size == 5) {
     int64_t px = (int64_t)N * H * W;
-    lrn5_fwd_kernel<<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(x, y, scale, N, C, H * W,
-                                                                       a_n, beta, k);
+    if (LRN_VEC == 4 && (H * W) % 4 == 0 && ((uintptr_t)x & 15) == 0 &&
+        ((uintptr_t)y & 15) == 0 && ((uintptr_t)scale & 15) == 0)
+      lrn5_fwd_kernel<4><<<(int)((px / 4 + 255) / 256), 256, 0, as_stream(s)>>>(
+          x, y, scale, N, C, H * W, a_n, beta, k);
+    else
+      lrn5_fwd_kernel<1><<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(x, y, scale, N, C,
+                                                                          H * W, a_n, beta, k);
     return check_launch("lrn_forward");
   }
   lrn_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
@@ -763,8 +958,14 @@ int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* 
   coef = coef / (float)size;
   if (size == 5) {
     int64_t px = (int64_t)N * H * W;
-    lrn5_bwd_kernel<<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(x, y, scale, dy, dx, N, C,
-                                                                       H * W, coef, beta);
+    if (LRN_VEC == 4 && (H * W) % 4 == 0 &&
+        (((uintptr_t)x | (uintptr_t)y | (uintptr_t)scale | (uintptr_t)dy | (uintptr_t)dx) & 15) ==
+            0)
+      lrn5_bwd_kernel<4><<<(int)((px / 4 + 255) / 256), 256, 0, as_stream(s)>>>(
+          x, y, scale, dy, dx, N, C, H * W, coef, beta);
+    else
+      lrn5_bwd_kernel<1><<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(
+          x, y, scale, dy, dx, N, C, H * W, coef, beta);
     return check_launch("lrn_backward");
   }
   lrn_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(

@@ -150,7 +150,10 @@ def test_sgd_momentum_aggregate_bitwise(golden_ops):
 
 @pytest.mark.parametrize("shape,k,s,p", [((2, 3, 9, 9), 3, 2, 0), ((2, 64, 112, 112), 3, 2, 0),
                                          ((2, 192, 28, 28), 3, 1, 1), ((2, 832, 14, 14), 3, 2, 0),
-                                         ((2, 4, 8, 8), 2, 2, 0), ((1, 96, 54, 54), 3, 2, 0)])
+                                         ((2, 4, 8, 8), 2, 2, 0), ((1, 96, 54, 54), 3, 2, 0),
+                                         ((2, 5, 11, 13), 3, 2, 1), ((2, 8, 14, 14), 3, 2, 1),
+                                         ((1, 2, 6, 7), 3, 2, 0), ((3, 7, 5, 5), 3, 1, 1),
+                                         ((2, 3, 6, 7), 3, 1, 0), ((2, 64, 7, 7), 3, 1, 1)])
 def test_maxpool_bitwise(shape, k, s, p):
     x = rnd(*shape)
     x[:, :, ::3, ::3] = 0.5  # plenty of ties
@@ -178,7 +181,7 @@ def test_avgpool_bitwise(shape, k, s, p):
     assert_bitwise(dx, O.avgpool_backward(x, dy, k, s, p))
 
 
-@pytest.mark.parametrize("shape", [(2, 64, 56, 56), (2, 7, 5, 5)])
+@pytest.mark.parametrize("shape", [(2, 64, 56, 56), (2, 7, 5, 5), (1, 2, 4, 4), (3, 4, 2, 2)])
 def test_lrn(shape):
     x = rnd(*shape, scale=3.0)
     y, sc = O.lrn_forward(x)

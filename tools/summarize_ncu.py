@@ -24,6 +24,9 @@ def family(name: str) -> str:
                  r"(?:\(int\))?(\d+)>", n)
     if m:
         return f"tc_gemm<{m.group(1)},{m.group(2)},{m.group(3)},BN={m.group(4)}>"
+    m = re.match(r"(?:bf::)?tc(\d)::tc\d_kernel<(?:bf::)?(\w+), (?:bf::)?(\w+)(?:, (?:\(int\))?(\d+))?>", n)
+    if m:
+        return f"tc{m.group(1)}<{m.group(2)},{m.group(3)}{',mode=' + m.group(4) if m.group(4) else ''}>"
     n = re.sub(r"\(.*", "", n)
     n = re.sub(r"<.*", "", n)
     return n
@@ -52,6 +55,11 @@ def launches(path):
     print("|---|---:|---:|---:|")
     for f, (c, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         print(f"| `{f}` | {c} | {ns / 1e6:.3f} | {ns / total:.1%} |")
+    if len(sys.argv) > 3:  # also the N longest single launches, in launch order index
+        top = sorted(enumerate(data), key=lambda kv: -kv[1][1])[:int(sys.argv[3])]
+        print("\n| launch # | kernel | us |\n|---:|---|---:|")
+        for i, (name, ns) in top:
+            print(f"| {i} | `{family(name)}` | {ns / 1e3:.1f} |")
 
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
