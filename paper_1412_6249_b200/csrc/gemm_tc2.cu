@@ -254,9 +254,17 @@ __global__ void bias_blocks_finish_kernel(const float* __restrict__ part, int nk
                                           float* __restrict__ db) {
   __shared__ float red[256];
   const float* row = part + (size_t)blockIdx.x * nkb;
-  float acc = 0.f;
-  for (int kb = threadIdx.x; kb < nkb; kb += 256) acc = __fadd_rn(acc, __ldg(row + kb));
-  red[threadIdx.x] = acc;
+  // four independent strided chains per thread (loads in flight), combined in a
+  // fixed order, then a fixed shared-memory tree
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int kb = threadIdx.x; kb < nkb; kb += 4 * 256) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = kb + u * 256;
+      if (k < nkb) acc[u] = __fadd_rn(acc[u], __ldg(row + k));
+    }
+  }
+  red[threadIdx.x] = __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
   __syncthreads();
   for (int s = 128; s > 0; s >>= 1) {
     if (threadIdx.x < s) red[threadIdx.x] = __fadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
@@ -692,9 +700,9 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
       bias_blocks_finish_kernel<<<N, 256, 0, st>>>(bias_ws, w.nkb, bias_out);
     }
   } else if (fast)
-    pack_b_kernel<LBP><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack);
+    launch_pack_b(lbp, N, K, w.BN, w.nkb, w.ntiles, bpack, st);
   else
-    pack_b_kernel<LB><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lb, N, K, w.BN, w.nkb, bpack);
+    launch_pack_b(lb, N, K, w.BN, w.nkb, w.ntiles, bpack, st);
   if (int rc = check_launch(what)) return rc;
 
   const int sms = sm_count_current();

@@ -2,9 +2,8 @@
 // (conv forward and data gradient, 3xTF32).
 //
 // Engine v2 (gemm_tc2.cu) gathers the im2col operand element by element: a
-// 3x3 layer loads, splits and stores every input value 9 times (25 for 5x5),
-// and ncu shows those producers, not the tensor pipe, setting the pace.  v3
-// removes the duplication with a padded-grid formulation:
+// 3x3 layer loads, splits and stores every input value 9 times (25 for 5x5).
+// v3 removes the duplication with a padded-grid formulation:
 //
 //  * Output pixels are enumerated on the zero-padded input grid
 //    (Hp = H + 2 pad, Wp = W + 2 pad): row o = (n*Hp + p)*Wp + q.  Filter tap
@@ -27,6 +26,13 @@
 // stride-1 convolution is the same operation on dY with pad' = R-1-pad and
 // the flipped, transposed filter (ops.py:300-343 restated by the oracle as
 // oracle/kernels.py conv2d_backward_data).
+//
+// Measured (GoogLeNet batch 128, tools/conv_bench.py): v3 is NOT faster than
+// v2.  The large 3x3 layers already run v2 at 150-180 TFLOP/s, close to the
+// 3xTF32 tensor ceiling, so removing gather work cannot help them; on the small
+// late layers the discarded border rows (up to 60% on 7x7 maps) and the
+// serial per-block staging cost more than they save.  v3 therefore stays
+// opt-in (bf_set_gemm_engine(3)) and covered by the GPU parity tests.
 #include <algorithm>
 
 #include "gemm_common.cuh"
@@ -341,8 +347,7 @@ int launch(const Halo& h, const LdHaloW& lbp, int Nout, const EpiNCHW& epi, floa
   const int64_t part_bytes = ws_bytes - pack_aligned;
   const int Mreal = h.N * h.P * h.Q;
 
-  pack_b_kernel<LdHaloW><<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, Nout, w.nkb * BK, w.BN,
-                                                                 w.nkb, bpack);
+  launch_pack_b(lbp, Nout, w.nkb * BK, w.BN, w.nkb, w.ntiles, bpack, st);
   if (int rc = check_launch(what)) return rc;
 
   const int sms = sm_count_current();

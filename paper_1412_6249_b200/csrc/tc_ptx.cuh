@@ -107,29 +107,38 @@ __device__ __forceinline__ uint32_t sw_off(int r, int c) {
 
 // ---- B pre-pack: [n_tile][k_block][big BN x 128B | small BN x 128B], swizzled ----
 
+// one thread per 16-byte chunk (row r of the tile, 4 consecutive k): grid
+// (k-blocks, n-tiles, BN/32) so even a small weight tensor spreads over
+// enough CTAs to be latency- rather than CTA-count-bound
 template <class LB>
 __global__ void pack_b_kernel(LB lb, int N, int K, int BN, int nkb, uint8_t* __restrict__ out) {
   const int tile = blockIdx.y, kb = blockIdx.x;
   uint8_t* base = out + ((size_t)tile * nkb + kb) * 2 * BN * 128;
-  const int chunks = BN * 8;
-  for (int i = threadIdx.x; i < chunks; i += blockDim.x) {
-    int r = i >> 3, c = i & 7;
-    int n = tile * BN + r;
-    float4 bg, sm;
-    float v[4];
+  const int i = blockIdx.z * blockDim.x + threadIdx.x;
+  if (i >= BN * 8) return;
+  const int r = i >> 3, c = i & 7;
+  const int n = tile * BN + r;
+  float v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int k = kb * 32 + c * 4 + j;
-      v[j] = (n < N && k < K) ? lb(n, k) : 0.f;
-    }
-    bg.x = to_tf32_rna(v[0]); sm.x = to_tf32_rna(v[0] - bg.x);
-    bg.y = to_tf32_rna(v[1]); sm.y = to_tf32_rna(v[1] - bg.y);
-    bg.z = to_tf32_rna(v[2]); sm.z = to_tf32_rna(v[2] - bg.z);
-    bg.w = to_tf32_rna(v[3]); sm.w = to_tf32_rna(v[3] - bg.w);
-    uint32_t off = sw_off(r, c);
-    *reinterpret_cast<float4*>(base + off) = bg;
-    *reinterpret_cast<float4*>(base + BN * 128 + off) = sm;
+  for (int j = 0; j < 4; ++j) {
+    const int k = kb * 32 + c * 4 + j;
+    v[j] = (n < N && k < K) ? lb(n, k) : 0.f;
   }
+  float4 bg, sm;
+  bg.x = to_tf32_rna(v[0]); sm.x = to_tf32_rna(v[0] - bg.x);
+  bg.y = to_tf32_rna(v[1]); sm.y = to_tf32_rna(v[1] - bg.y);
+  bg.z = to_tf32_rna(v[2]); sm.z = to_tf32_rna(v[2] - bg.z);
+  bg.w = to_tf32_rna(v[3]); sm.w = to_tf32_rna(v[3] - bg.w);
+  const uint32_t off = sw_off(r, c);
+  *reinterpret_cast<float4*>(base + off) = bg;
+  *reinterpret_cast<float4*>(base + BN * 128 + off) = sm;
+}
+
+template <class LB>
+inline void launch_pack_b(const LB& lb, int N, int K, int BN, int nkb, int ntiles, uint8_t* out,
+                          cudaStream_t st) {
+  pack_b_kernel<LB><<<dim3(nkb, ntiles, (BN * 8 + 255) / 256), 256, 0, st>>>(lb, N, K, BN, nkb,
+                                                                            out);
 }
 
 }  // namespace tcu
