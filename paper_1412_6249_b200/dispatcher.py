@@ -299,13 +299,15 @@ def _check_sources(graph: BiGraph, store: TensorStore) -> None:
 class _Plan:
     """Static per-(graph, lane cap) launch plan: order, lane slots, cross-stream edges."""
 
-    def __init__(self, graph: BiGraph, cap: int) -> None:
+    def __init__(self, graph: BiGraph, cap: int, branches: int = 1) -> None:
         self.order = serial_order(graph)
         lanes = sorted({lane_of(op) for op in graph.operators.values()})
         n = max(1, min(len(lanes), cap)) if lanes else 0
         self.slot_of_lane = {ln: i % n for i, ln in enumerate(lanes)} if n else {}
         self.slot = {oid: self.slot_of_lane[lane_of(op)] for oid, op in graph.operators.items()}
         self.n_slots = n
+        if branches > 1 and cap > 1 and n:
+            self._split_branches(graph, branches)
         # inputs produced by an op on a different slot -> that producer must record an event
         self.waits: dict[int, list[int]] = {}
         self.signals: set[int] = set()
@@ -348,6 +350,63 @@ class _Plan:
                 self.fusion[sib[0]] = {"db": graph.tensors[op.outputs[0]].name}
                 self.fused_away.add(oid)
 
+    def _split_branches(self, graph: BiGraph, branches: int) -> None:
+        """Event-driven device concurrency inside a lane: the lane's operators
+        are spread over up to ``branches`` CUDA streams by greedy chain
+        decomposition in serial order (an operator continues the stream whose
+        last operator produced one of its inputs, else takes a new or the
+        least recently used stream), so independent Inception branches run
+        concurrently; every cross-stream input becomes an event wait (``waits``).
+        Host dispatch order is unchanged.  Lanes carrying collectives or copies
+        keep one stream (NCCL calls must stay ordered per communicator)."""
+        serial_kinds = {"dp_exchange", "copy", "swap"}
+        keep = {self.slot[oid] for oid, op in graph.operators.items() if op.kind in serial_kinds}
+        subs: dict[int, list[int]] = {}
+        last_op: dict[int, int] = {}
+        last_use: dict[int, int] = {}
+        done: set[int] = set()
+        for i, oid in enumerate(self.order):
+            base = self.slot[oid]
+            if base in keep:
+                continue
+            pool = subs.setdefault(base, [base])
+            chosen = None
+            op = graph.operators[oid]
+            if op.kind == "conv2d_backward_bias":  # stays with its weight gradient (fusion)
+                for c, _ in graph.consumers_of(op.inputs[0]):
+                    if graph.operators[c].kind == "conv2d_backward_weight" and c in done:
+                        chosen = self.slot[c]
+            for tid in (op.inputs if chosen is None else ()):
+                p = graph.producer_of(tid)
+                if p is not None and self.slot.get(p) in pool and last_op.get(self.slot[p]) == p:
+                    chosen = self.slot[p]
+                    break
+            if chosen is None:
+                if len(pool) < branches and all(s in last_op for s in pool):
+                    chosen = self.n_slots
+                    self.n_slots += 1
+                    pool.append(chosen)
+                else:
+                    chosen = min(pool, key=lambda s: last_use.get(s, -1))
+            self.slot[oid] = chosen
+            last_op[chosen] = oid
+            last_use[chosen] = i
+            done.add(oid)
+
+
+BRANCH_ENV = "PURINE_B200_BRANCH_STREAMS"  # device streams per compute lane (1 = lane-exclusive)
+
+
+def _branch_streams() -> int:
+    raw = os.environ.get(BRANCH_ENV, "4")
+    try:
+        k = int(raw)
+    except ValueError:
+        raise DispatchError(f"{BRANCH_ENV} must be an integer, got {raw!r}") from None
+    if k < 1:
+        raise DispatchError(f"{BRANCH_ENV} must be >= 1, got {k}")
+    return k
+
 
 FUSE_ENV = "PURINE_B200_FUSE"  # "0" disables epilogue fusion (A/B and debugging)
 
@@ -362,16 +421,17 @@ def _fusion_enabled(registry) -> bool:
                                                       "conv2d_backward_bias"))
 
 
-_PLAN_CACHE: dict[tuple[int, int], tuple[int, _Plan]] = {}
+_PLAN_CACHE: dict[tuple[int, int, int], tuple[int, _Plan]] = {}
 
 
 def _plan(graph: BiGraph, cap: int) -> _Plan:
-    key = (id(graph), cap)
+    branches = _branch_streams()
+    key = (id(graph), cap, branches)
     stamp = len(graph.insertion_order) * 1_000_003 + len(graph.tensors)
     hit = _PLAN_CACHE.get(key)
     if hit is not None and hit[0] == stamp:
         return hit[1]
-    p = _Plan(graph, cap)
+    p = _Plan(graph, cap, branches)
     _PLAN_CACHE[key] = (stamp, p)
     return p
 
