@@ -41,6 +41,9 @@ int bf_version(void);
 const char* bf_last_error(void);
 /* number of SMs of `device` (grid sizing is done in multiples of it) */
 int bf_sm_count(int device);
+/* leave n SMs free of persistent GEMM CTAs (for NCCL kernels overlapping the
+   backward pass; exchange.py sets it when a communicator exists) */
+int bf_set_sm_reserve(int n);
 /* 1 if the library was compiled with the tcgen05 GEMM path */
 int bf_has_tcgen05(void);
 /* total kernels launched by this library so far (process-wide counter) */

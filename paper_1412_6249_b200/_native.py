@@ -32,6 +32,7 @@ _SIGS = {
     "bf_has_tcgen05": [],
     "bf_launch_count": [],
     "bf_set_gemm_engine": [_i],
+    "bf_set_sm_reserve": [_i],
     "bf_set_device": [_i],
     "bf_delay_ns": [_l, _p],
     "bf_relu_fwd": [_p, _p, _l, _p],

@@ -47,6 +47,7 @@ inline int check_launch(const char* what, int n = 1) {
   } while (0)
 
 int sm_count_current();
+int gemm_sm_budget();  // SM count minus bf_set_sm_reserve()
 
 // grid for a grid-stride elementwise kernel: multiple of the SM count
 inline int elementwise_grid(int64_t work_items, int threads) {

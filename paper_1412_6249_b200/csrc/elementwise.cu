@@ -24,6 +24,15 @@ static std::atomic<long long> g_launches{0};
 
 void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+static std::atomic<int> g_sm_reserve{0};
+
+// SMs the persistent GEMMs leave free for concurrently running collectives
+int gemm_sm_budget() {
+  const int sms = sm_count_current();
+  const int r = g_sm_reserve.load(std::memory_order_relaxed);
+  return sms - r >= 1 ? sms - r : 1;
+}
+
 int sm_count_current() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -176,6 +185,12 @@ int bf_sm_count(int device) {
     return -1;
   }
   return v;
+}
+
+int bf_set_sm_reserve(int n) {
+  BF_REQUIRE(n >= 0 && n < sm_count_current(), "bf_set_sm_reserve: 0 <= n < SM count");
+  g_sm_reserve.store(n, std::memory_order_relaxed);
+  return 0;
 }
 
 int bf_set_device(int device) {

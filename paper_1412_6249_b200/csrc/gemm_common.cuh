@@ -214,7 +214,7 @@ enum GemmOp { kConvFwd = 0, kConvDgrad = 1, kConvWgrad = 2, kFcFwd = 3, kFcDgrad
 inline int choose_splits(int64_t M, int64_t N, int64_t K, int bm, int bn, int64_t min_k,
                          int64_t ws_bytes) {
   int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
-  int64_t want = (2LL * sm_count_current() + tiles - 1) / tiles;
+  int64_t want = (2LL * gemm_sm_budget() + tiles - 1) / tiles;
   int64_t by_k = K / min_k;
   if (want > by_k) want = by_k;
   if (want > 64) want = 64;

@@ -705,7 +705,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
     launch_pack_b(lb, N, K, w.BN, w.nkb, w.ntiles, bpack, st);
   if (int rc = check_launch(what)) return rc;
 
-  const int sms = sm_count_current();
+  const int sms = gemm_sm_budget();
   w.splits = 1;
   {
     int64_t tiles = (int64_t)w.mtiles * w.ntiles;

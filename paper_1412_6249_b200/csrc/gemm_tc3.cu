@@ -350,7 +350,7 @@ int launch(const Halo& h, const LdHaloW& lbp, int Nout, const EpiNCHW& epi, floa
   launch_pack_b(lbp, Nout, w.nkb * BK, w.BN, w.nkb, w.ntiles, bpack, st);
   if (int rc = check_launch(what)) return rc;
 
-  const int sms = sm_count_current();
+  const int sms = gemm_sm_budget();
   w.splits = 1;
   const int64_t tiles = (int64_t)w.mtiles * w.ntiles;
   if (tiles < sms) {  // one wave: split the channel blocks

@@ -18,10 +18,17 @@ deadlock even when lanes share a stream, and every rank enqueues collectives
 in the same order.  Streams run concurrently, giving the reference's
 lane-level overlap (compute lanes vs. copy lanes) on the GPU.
 
+Inside a compute lane, independent operators (Inception branches; weight vs.
+data gradients) are further spread over up to ``PURINE_B200_BRANCH_STREAMS``
+(default 4) streams by greedy chain decomposition, with event waits on every
+cross-stream input: an operator starts when its inputs' events fire.  Lanes
+that carry collectives keep one stream, created at high priority so the block
+scheduler starts exchange CTAs ahead of queued compute CTAs.
+
 Lane cap: ``max_workers`` / ``BIFLOW_LANES`` bounds the number of streams;
 sorted lanes map round-robin onto them exactly as lanes map onto worker
 threads in the reference (dispatcher.py:261-267).  ``1`` is the fully serial
-mode: one stream, device execution order == dispatch order.
+mode: one stream (no branch streams), device execution order == dispatch order.
 
 Timing: with ``trace=True`` each operator is bracketed by CUDA events on its
 stream; `TraceRecord` start/end are ns since the sequence's zero event, so
@@ -253,8 +260,17 @@ class _Lanes:
         self.device = store.device
         self.streams: list[torch.cuda.Stream] = []
         self.workspaces: list[_Workspace] = []
+        self.high: dict[int, tuple[torch.cuda.Stream, _Workspace]] = {}
 
-    def get(self, idx: int) -> tuple[torch.cuda.Stream, _Workspace]:
+    def get(self, idx: int, high: bool = False) -> tuple[torch.cuda.Stream, _Workspace]:
+        """Stream + workspace of slot ``idx``; ``high`` selects a separate
+        high-priority stream (the exchange lane: the block scheduler then
+        starts its collective / update CTAs ahead of queued compute CTAs)."""
+        if high:
+            if idx not in self.high:
+                self.high[idx] = (torch.cuda.Stream(device=self.device, priority=-1),
+                                  _Workspace(self.device))
+            return self.high[idx]
         while len(self.streams) <= idx:
             self.streams.append(torch.cuda.Stream(device=self.device))
             self.workspaces.append(_Workspace(self.device))
@@ -306,6 +322,9 @@ class _Plan:
         self.slot_of_lane = {ln: i % n for i, ln in enumerate(lanes)} if n else {}
         self.slot = {oid: self.slot_of_lane[lane_of(op)] for oid, op in graph.operators.items()}
         self.n_slots = n
+        # slots running the parameter exchange get a high-priority stream
+        self.high_priority = {self.slot[oid] for oid, op in graph.operators.items()
+                              if op.kind == "dp_exchange"}
         if branches > 1 and cap > 1 and n:
             self._split_branches(graph, branches)
         # inputs produced by an op on a different slot -> that producer must record an event
@@ -456,7 +475,7 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
     cur = torch.cuda.current_stream(store.device)
     fork = torch.cuda.Event()
     fork.record(cur)
-    slots = [pool.get(i) for i in range(plan.n_slots)]
+    slots = [pool.get(i, i in plan.high_priority) for i in range(plan.n_slots)]
     for s, _ in slots:
         s.wait_event(fork)
     done_ev: dict[int, torch.cuda.Event] = {}

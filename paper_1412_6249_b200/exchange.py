@@ -31,6 +31,8 @@ parity is tolerance-based.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 from math import prod
 
@@ -194,6 +196,13 @@ def setup_nccl(store, world: int, rank: int) -> None:
     comm = ctypes.c_void_p()
     lib("bf_set_device", store.device.index or 0)
     lib("bf_nccl_init", ctypes.byref(comm), world, rank, ctypes.cast(uid, ctypes.c_void_p))
+    # the exchange lane's stream is high-priority (dispatcher), which keeps
+    # small-bucket collectives at their unloaded latency under a GEMM load
+    # (tools/exchange_sweep.py --overlap); optionally also keep SMs free of
+    # persistent GEMM CTAs
+    reserve = int(os.environ.get("PURINE_B200_SM_RESERVE", "0"))
+    if reserve:
+        lib("bf_set_sm_reserve", reserve)
     store._nccl = comm.value
     store._nccl_rank = rank
     store._nccl_world = world

@@ -108,6 +108,21 @@ class CapturedSequence:
                 out.append((gi, g.operators[oid], a.elapsed_time(b)))
         return out
 
+    def op_intervals_ns(self, parity: int) -> list[tuple[int, object, int, int]]:
+        """(graph index, operator, start ns, end ns) of the last replay of
+        ``parity``, relative to the first operator start of graph 0 (needs
+        ``trace=True``; call after synchronising)."""
+        base = None
+        out = []
+        for gi, recs in enumerate(self.timing[parity]):
+            g = self.seq.graphs[gi]
+            for oid, a, b in recs:
+                if base is None:
+                    base = a
+                s = int(round(base.elapsed_time(a) * 1e6))
+                out.append((gi, g.operators[oid], s, s + int(round(a.elapsed_time(b) * 1e6))))
+        return out
+
     def step(self, after_graph=None, iteration: int = 0) -> None:
         if not self.ready:
             raise DispatchError("CapturedSequence.step() before prepare()")

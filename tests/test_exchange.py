@@ -114,3 +114,20 @@ def test_gloo_two_ranks_match_aggregate_mean_sgd():
         got = np.asarray(out[r])
         assert np.array_equal(got, out[0])  # every rank holds identical parameters
         assert np.allclose(got, want, rtol=1e-6, atol=1e-7)
+
+
+def test_exchange_sweep_sizes_and_bandwidth_math():
+    """BASELINE config 5 sweep (tools/exchange_sweep.py): 17 message sizes from
+    4 KB to 256 MB; busbw = algbw * 2(N-1)/N for reduce-scatter + all-gather."""
+    import importlib.util
+    from pathlib import Path
+
+    spec = importlib.util.spec_from_file_location(
+        "exchange_sweep", Path(__file__).resolve().parent.parent / "tools" / "exchange_sweep.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    s = mod.sizes(4, 256)
+    assert len(s) == 17 and s[0] == 4096 and s[-1] == 256 << 20
+    alg, bus = mod.bus_bw(1 << 30, 0.5, 8)
+    assert abs(alg - 2.147483648) < 1e-9 and abs(bus - alg * 14 / 8) < 1e-9
+    assert mod.bus_bw(1000, 1e-6, 1) == (1.0, 1.0)
