@@ -18,8 +18,18 @@
 //  * N tile = the whole output-channel extent up to 256 (rounded to 32), so
 //    A is gathered once per output pixel tile.
 //
-// TMEM map (512 columns): [0, BN) fp32 accumulator; [256 + 64*s, +32) A_big
-// and [256 + 64*s + 32, +32) A_small of stage s (4 stages).
+// TMEM map (512 columns): nacc fp32 accumulators of BN columns at BN*b, then
+// the A ring from abase = 64-aligned end of the accumulators: stage s holds
+// A_big in [abase + 64*s, +32) and A_small in [abase + 64*s + 32, +32).  The
+// ring is as deep as the columns allow (4..7 stages): a stage is recycled only
+// after its MMAs complete and the commit reaches the producers (~2000 cycles),
+// so narrow tiles (BN <= 64, 384 tensor cycles per stage) need more than 4.
+//
+// MMA issue: tools/mma_probe.cu measured tcgen05.mma kind::tf32 at N/2 cycles
+// per instruction (1190 TFLOP/s at N >= 128) but an issue floor of ~45 cycles
+// per instruction even in straight-line code, and 110-150 cycles when each
+// instruction recomputes its descriptors and predicate; the issuer therefore
+// uses precomputed descriptor bases and literal accumulate flags.
 #include <algorithm>
 #include <type_traits>
 
@@ -31,12 +41,11 @@ namespace bf {
 namespace tc2 {
 
 constexpr int BK = 32;
-constexpr int STAGES = 4;
+constexpr int STAGES = 8;  // A-ring capacity (barrier arrays); the depth used is w.nst
 constexpr int kProducerWarps = 8;
 constexpr int kProducers = kProducerWarps * 32;
 constexpr int kInvalid = -30000;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAColBase = 256;
 
 struct __align__(8) RowInfo {
   int off;
@@ -291,16 +300,24 @@ __global__ void bias_blocks_finish_kernel(const float* __restrict__ part, int nk
 #ifndef TC2_EPI_WARPS
 #define TC2_EPI_WARPS 8
 #endif
+#ifndef TC2_TRUNC_SPLIT
+#define TC2_TRUNC_SPLIT 1
+#endif
 #ifndef TC2_PREFETCH
 #define TC2_PREFETCH 1
 #endif
 constexpr int kEpiWarps = TC2_EPI_WARPS;
 constexpr int kMmaWarp = kProducerWarps;
-constexpr int kAllThreads = (kProducerWarps + 1 + kEpiWarps) * 32;
+constexpr int kBWarp = kProducerWarps + 1 + kEpiWarps;  // B-tile loader (TMA issue)
+constexpr int kAllThreads = (kBWarp + 1) * 32;
+constexpr int kBStagesMax = 8;  // B ring depth, independent of the 4-stage TMEM A ring
 constexpr int kKtabMax = 4096;  // k-table entries cached in shared memory per CTA
 
 struct Work {
   int M, N, K, BN, nst, nkb, kbps, splits, mtiles, ntiles, units, nacc, full_ktab;
+  int nbst;   // B ring stages
+  int abase;  // first TMEM column of the A ring
+  int accs;   // TMEM column stride between the accumulator buffers
   int Pp, Qp;  // weight-gradient fast path: padded pixel grid of the K ordering
 };
 
@@ -379,6 +396,22 @@ __device__ __forceinline__ void gather16_wgrad(const LA& la, const Work& w, cons
   }
 }
 
+// A operand split for 3xTF32.  The tensor core reads a kind::tf32 operand's
+// fp32 bit pattern and ignores the 13 low mantissa bits, so the truncated
+// value trunc(x) is implicit: big = x as is, small = x - trunc(x) (exact in
+// fp32; its own low bits are dropped by the MMA in turn).  |x - big - small| <=
+// 2^-20 |x| (vs 2^-22 with round-to-nearest splitting, which costs 3 more
+// integer ops per element on the producers' critical path).
+__device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
+#if TC2_TRUNC_SPLIT
+  big = x;
+  small = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+#else
+  big = to_tf32_rna(x);
+  small = to_tf32_rna(x - big);
+#endif
+}
+
 // the table/no-table choice is hoisted out of the unrolled loop so the
 // division-heavy fallback is never if-converted into the common path
 template <class SA, int MODE, class LA>
@@ -409,10 +442,12 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   const int stage_bytes = 2 * BN * 128;
   uint8_t* tiles = base;
   const int ktab_n = w.full_ktab ? w.nkb * BK : STAGES * BK;
-  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nst * stage_bytes);
+  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nbst * stage_bytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + ktab_n);
   uint64_t* empty = full + STAGES;
-  uint64_t* acc_full = empty + STAGES;
+  uint64_t* bfull = empty + STAGES;
+  uint64_t* bempty = bfull + kBStagesMax;
+  uint64_t* acc_full = bempty + kBStagesMax;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -428,6 +463,10 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], kProducers);
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kBStagesMax; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -488,17 +527,10 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           float big[16], small[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            big[j] = to_tf32_rna(v[j]);
-            small[j] = to_tf32_rna(v[j] - big[j]);
+            split_tf32(v[j], big[j], small[j]);
           }
           mbar_wait(&empty[stage], phase ^ 1);
-          if (t == 0) {
-            mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-            bulk_g2s(smem_u32(tiles + stage * stage_bytes),
-                     bpack + ((size_t)nt * w.nkb + kb0 + i2) * stage_bytes,
-                     (uint32_t)stage_bytes, &full[stage]);
-          }
-          const uint32_t acol = kAColBase + stage * 64 + kc0;
+          const uint32_t acol = w.abase + stage * 64 + kc0;
           tmem_st16(lane_addr + acol, big);
           tmem_st16(lane_addr + acol + 32, small);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -507,6 +539,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         }
       }
     } else if (u < w.units) {
+      int pstage = 0;
+      uint32_t pphase = 0;
       RowInfo ri = row_of(u);
       int mt, nt, sp;
       unit_coords(w, u, mt, nt, sp);
@@ -539,19 +573,16 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         float big[16], small[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          big[j] = to_tf32_rna(v[j]);
-          small[j] = to_tf32_rna(v[j] - big[j]);
+          split_tf32(v[j], big[j], small[j]);
         }
-        const int stage = it % w.nst;
-        const uint32_t phase = (it / w.nst) & 1;
+        const int stage = pstage;
+        const uint32_t phase = pphase;
+        if (++pstage == w.nst) {
+          pstage = 0;
+          pphase ^= 1;
+        }
         mbar_wait(&empty[stage], phase ^ 1);
-        if (t == 0) {
-          mbar_expect_tx(&full[stage], (uint32_t)stage_bytes);
-          bulk_g2s(smem_u32(tiles + stage * stage_bytes),
-                   bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
-                   &full[stage]);
-        }
-        const uint32_t acol = kAColBase + stage * 64 + kc0;
+        const uint32_t acol = w.abase + stage * 64 + kc0;
         tmem_st16(lane_addr + acol, big);
         tmem_st16(lane_addr + acol + 32, small);
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -576,6 +607,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     // ======================= MMA issuer =======================
     if (lane == 0) {
       const uint32_t idesc = tf32_idesc(BN);
+      const uint64_t dtiles = sw128_desc(smem_u32(tiles));  // B stage 0, big image, k-step 0
+      const uint64_t dsmall = (uint64_t)((BN * 128) >> 4);   // big -> small image
       int it = 0, local = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
         int mt, nt, sp;
@@ -585,26 +618,60 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         const uint32_t use = local / w.nacc;
         mbar_wait(&acc_empty[b], (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t dacc = tmem + (uint32_t)(b * 128);
+        const uint32_t dacc = tmem + (uint32_t)(b * w.accs);
         for (int i = 0; i < nk; ++i, ++it) {
-          const int stage = it % w.nst;
+          // (stage, phase) from the k-block counter: running counters here made
+          // ptxas emit an illegal uniform-register sequence for tcgen05.mma
+          const int stage = it % w.nst, bst = it % w.nbst;
           const uint32_t phase = (it / w.nst) & 1;
+          mbar_wait(&bfull[bst], (it / w.nbst) & 1);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t bb = smem_u32(tiles + stage * stage_bytes);
-          const uint32_t bs = bb + BN * 128;
-          const uint32_t ab = tmem + kAColBase + stage * 64;
+          // descriptor start-address field = smem byte address >> 4 (bits 0-13)
+          const uint64_t db = dtiles + (uint64_t)((bst * stage_bytes) >> 4);
+          const uint64_t ds = db + dsmall;
+          const uint32_t ab = tmem + w.abase + stage * 64;
+          // 3xTF32 per k-step of 8: small*big + big*small + big*big
+          if (i == 0)
+            mma_ts_flag<0>(dacc, ab + 32, db, idesc);
+          else
+            mma_ts_flag<1>(dacc, ab + 32, db, idesc);
+          mma_ts_flag<1>(dacc, ab, ds, idesc);
+          mma_ts_flag<1>(dacc, ab, db, idesc);
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint64_t dbb = sw128_desc(bb + ks * 32), dbs = sw128_desc(bs + ks * 32);
-            const uint32_t a_big = ab + ks * 8, a_small = ab + 32 + ks * 8;
-            mma_ts(dacc, a_small, dbb, idesc, (i > 0 || ks > 0) ? 1u : 0u);
-            mma_ts(dacc, a_big, dbs, idesc, 1u);
-            mma_ts(dacc, a_big, dbb, idesc, 1u);
+          for (int ks = 1; ks < BK / 8; ++ks) {
+            const uint64_t k2 = (uint64_t)((ks * 32) >> 4);
+            mma_ts_flag<1>(dacc, ab + 32 + ks * 8, db + k2, idesc);
+            mma_ts_flag<1>(dacc, ab + ks * 8, ds + k2, idesc);
+            mma_ts_flag<1>(dacc, ab + ks * 8, db + k2, idesc);
           }
           tc_commit(&empty[stage]);
+          tc_commit(&bempty[bst]);
         }
         tc_commit(&acc_full[b]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == kBWarp) {
+    // ======================= B loader =======================
+    // streams the pre-packed B tiles of every (unit, k-block) into the B ring
+    // as far ahead as the ring allows: the TMA latency leaves the per-stage
+    // critical path of the producers
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
+        int mt, nt, sp;
+        unit_coords(w, u, mt, nt, sp);
+        const int kb0 = sp * w.kbps;
+        const int nk = min(w.kbps, w.nkb - kb0);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int bst = it % w.nbst;
+          mbar_wait(&bempty[bst], ((it / w.nbst) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bfull[bst], (uint32_t)stage_bytes);
+          bulk_g2s(smem_u32(tiles + bst * stage_bytes),
+                   bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
+                   &bfull[bst]);
+        }
       }
     }
     __syncwarp();
@@ -624,7 +691,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       const int m = mt * BM + q * 32 + lane;
       const int n0 = nt * BN;
       const int cols = kEpiWarps == 8 ? BN / 2 : BN;
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 128);
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * w.accs);
       const bool live = m < w.M;
       const RowPtr rp = live ? (w.splits > 1 ? part.row(sp, m) : epi.row(m)) : RowPtr{nullptr, 0.f};
 #pragma unroll 1
@@ -679,6 +746,9 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.nkb = (K + BK - 1) / BK;
   w.mtiles = (M + BM - 1) / BM;
   w.nacc = w.BN <= 128 ? 2 : 1;
+  w.accs = w.BN;  // multiple of 32
+  w.abase = (w.nacc * w.BN + 63) / 64 * 64;
+  w.nst = std::min<int>(7, (512 - w.abase) / 64);
   const int64_t stage_bytes = 2LL * w.BN * 128;
   const int64_t pack_bytes = (int64_t)w.ntiles * w.nkb * stage_bytes;
   const int64_t pack_aligned = (pack_bytes + 1023) / 1024 * 1024;
@@ -722,12 +792,12 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.units = w.mtiles * w.ntiles * w.splits;
 
   const int smem_cap = 227 * 1024;
-  const int tail = 1024 + 16 * 8 + 64;
+  const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
   w.full_ktab = (mode == kChannel || (mode == kGeneric && K <= kKtabMax)) ? 1 : 0;
   const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;  // as the kernel carves it
-  w.nst = (int)std::min<int64_t>(STAGES, (smem_cap - tail - ktab_bytes) / stage_bytes);
-  if (w.nst < 2) return -1;
-  const int smem = tail + (int)(w.nst * stage_bytes) + ktab_bytes;
+  w.nbst = (int)std::min<int64_t>(kBStagesMax, (smem_cap - tail - ktab_bytes) / stage_bytes);
+  if (w.nbst < 2) return -1;
+  const int smem = tail + (int)(w.nbst * stage_bytes) + ktab_bytes;
   auto kern = mode == kChannel ? tc2_kernel<LA, Epi, kChannel>
              : mode == kWgrad16 ? tc2_kernel<LA, Epi, kWgrad16>
              : mode == kWgrad8  ? tc2_kernel<LA, Epi, kWgrad8>

@@ -23,6 +23,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// arrive (count 1) and add the expected transaction bytes in one step
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -60,6 +66,14 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
+}
+// same with a compile-time accumulate flag (no per-instruction predicate setup)
+template <int ACC>
+__device__ __forceinline__ void mma_ts_flag(uint32_t d, uint32_t a, uint64_t bdesc,
+                                            uint32_t idesc) {
+  asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, %4;" ::"r"(d), "r"(a),
+               "l"(bdesc), "r"(idesc), "n"(ACC)
+               : "memory");
 }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
