@@ -109,9 +109,13 @@ def lib() -> _Lib:
                         f"CUDA kernel library not built: {LIB_PATH} is missing "
                         "(run `python -m paper_1412_6249_b200._build`); there is no CPU fallback")
                 try:
-                    _lib = _Lib(C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL))
+                    loaded_lib = _Lib(C.CDLL(str(LIB_PATH), mode=C.RTLD_GLOBAL))
                 except OSError as exc:
                     raise KernelError(f"cannot load {LIB_PATH}: {exc}") from None
+                # A/B switch for the contraction engines (bf_set_gemm_engine)
+                if os.environ.get("PURINE_B200_GEMM_ENGINE"):
+                    loaded_lib("bf_set_gemm_engine", int(os.environ["PURINE_B200_GEMM_ENGINE"]))
+                _lib = loaded_lib
     return _lib
 
 

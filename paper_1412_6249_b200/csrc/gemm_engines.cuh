@@ -33,6 +33,12 @@ int tc3_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNC
 int tc3_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
                    float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 
-extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in)
+// tcgen05 engine v4 (gemm_tc4.cu): TMA-fed 1x1 convolutions (MN-major activation operand)
+int tc4_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNCHW& epi,
+                 float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
+                   float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+
+extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in), 4 auto without v4
 
 }  // namespace bf

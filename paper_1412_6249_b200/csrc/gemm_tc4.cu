@@ -1,0 +1,418 @@
+// tcgen05 engine v4: TMA-fed 1x1 convolutions (forward and data gradient), 3xTF32.
+//
+// A 1x1 stride-1 convolution is, per image, a plain GEMM on the NCHW tensors:
+//   fwd   y[n][k][p] = sum_c w[k][c] x[n][c][p]      (ops.py:281-297)
+//   dgrad dx[n][c][p] = sum_k w[k][c] dy[n][k][p]    (ops.py:332-343)
+// With the output pixel as the MMA M index, the activation operand is
+// "MN-major" in memory (pixels contiguous, channels strided) -- a layout the
+// tensor core reads directly for kind::tf32 (instruction descriptor bit 15;
+// shared-memory layout "128B swizzle, 32B atoms", see mn_sw128_32b_desc).
+// So nothing is gathered: a TMA warp streams 128-pixel x 32-channel boxes
+// straight from x (or dy) into 128B-swizzled shared memory, and the weights
+// come pre-packed (tc_ptx.cuh pack_b_kernel) by bulk copy, as in engine v2.
+//
+// 3xTF32 split of the activation: the tensor core ignores the 13 low mantissa
+// bits of a kind::tf32 operand, so the raw TMA tile IS the "big" operand;
+// four "split" warps only compute small = x - trunc(x) (exact) into a second
+// tile: one 16-byte load, four AND + four FADD and one 16-byte store per four
+// elements.  MMAs per k-step of 8: small*big + big*small + big*big, both
+// operands from shared memory.
+//
+// Warp roles (14 warps, 4 per SM sub-partition -> up to 128 registers):
+//   warp 0        TMA / bulk-copy issuer (one thread)
+//   warps 1-4     split warps
+//   warp 5        MMA issuer (one thread) + TMEM allocator
+//   warps 6-13    epilogue: TMEM -> registers -> NCHW global stores (fused
+//                 bias / ReLU exactly as engine v2's EpiNCHW)
+// Tiles never straddle images (the TMA box is per image; pixels past the
+// image end are zero-filled and their rows discarded).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "gemm_common.cuh"
+#include "gemm_engines.cuh"
+#include "tc_ptx.cuh"
+
+namespace bf {
+namespace tc4 {
+
+using namespace tcu;
+
+constexpr int BK = 32;
+constexpr int kMaxStages = 6;
+constexpr int kTmaWarp = 0, kSplitWarp0 = 1, kSplitWarps = 4, kMmaWarp = 5, kEpiWarp0 = 6;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kABytes = BM * BK * 4;  // one raw activation tile (16 KB)
+
+struct Work {
+  int PQ, tiles_img, N_img, Nout, K, BN, ntiles, nkb, kbps, splits, units, nst, nacc;
+  int stage_bytes, b_bytes;
+};
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// MN-major tf32 operand: the only smem layout the tensor core accepts is
+// "128B swizzle with 32B atomicity" (descriptor layout type 1; TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes it): 128-byte K rows of 32
+// MN-elements whose 32-byte granules are permuted by row, 4-row (512 B) atoms.
+// 32-element MN chunks (one TMA box each) 4 KB apart = LBO; 4-row K groups
+// 512 B apart = SBO.  Verified bit-exactly by tools/mn_probe.cu.
+__device__ __forceinline__ uint64_t mn_sw128_32b_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(4096 >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;
+  return d;
+}
+
+template <int ACC>
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, %4;" ::"r"(d), "l"(a),
+               "l"(b), "r"(idesc), "n"(ACC)
+               : "memory");
+}
+
+__device__ __forceinline__ void unit_coords(const Work& w, int u, int& img, int& pt, int& nt,
+                                            int& sp) {
+  sp = u % w.splits;
+  int r = u / w.splits;
+  nt = r % w.ntiles;
+  r /= w.ntiles;
+  pt = r % w.tiles_img;
+  img = r / w.tiles_img;
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc4_kernel(const __grid_constant__ CUtensorMap amap, Work w, const uint8_t* __restrict__ bpack,
+               Epi epi, EpiPartial part) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int BN = w.BN;
+  // stage s: [A raw | A small | B big | B small]
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(base + w.nst * w.stage_bytes);
+  uint64_t* split_full = raw_full + kMaxStages;
+  uint64_t* empty = split_full + kMaxStages;
+  uint64_t* acc_full = empty + kMaxStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&raw_full[s], 1);
+      mbar_init(&split_full[s], kSplitWarps * 32);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kEpiWarps * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kTmaWarp) {
+    // ======================= TMA issue =======================
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
+        int img, pt, nt, sp;
+        unit_coords(w, u, img, pt, nt, sp);
+        const int kb0 = sp * w.kbps, nk = min(w.kbps, w.nkb - kb0);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % w.nst;
+          mbar_wait(&empty[s], ((it / w.nst) & 1) ^ 1);
+          mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(kABytes + w.b_bytes));
+          uint8_t* st = base + s * w.stage_bytes;
+          const int kc = (kb0 + i) * BK;
+#pragma unroll
+          for (int j = 0; j < BM / 32; ++j)
+            tma_load_3d(smem_u32(st + j * 4096), &amap, pt * BM + j * 32, kc, img, &raw_full[s]);
+          bulk_g2s(smem_u32(st + 2 * kABytes),
+                   bpack + ((size_t)nt * w.nkb + kb0 + i) * w.b_bytes, (uint32_t)w.b_bytes,
+                   &raw_full[s]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kSplitWarp0 && warp < kSplitWarp0 + kSplitWarps) {
+    // ======================= split: small = x - trunc(x) =======================
+    const int t = threadIdx.x - kSplitWarp0 * 32;
+    int it = 0;
+    for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
+      int img, pt, nt, sp;
+      unit_coords(w, u, img, pt, nt, sp);
+      const int nk = min(w.kbps, w.nkb - sp * w.kbps);
+      for (int i = 0; i < nk; ++i, ++it) {
+        const int s = it % w.nst;
+        mbar_wait(&raw_full[s], (it / w.nst) & 1);
+        const float4* src = reinterpret_cast<const float4*>(base + s * w.stage_bytes);
+        float4* dst = reinterpret_cast<float4*>(base + s * w.stage_bytes + kABytes);
+#pragma unroll
+        for (int q = 0; q < kABytes / 16 / (kSplitWarps * 32); ++q) {
+          const float4 v = src[q * kSplitWarps * 32 + t];
+          float4 r;
+          r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+          r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+          r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+          r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          dst[q * kSplitWarps * 32 + t] = r;
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&split_full[s]);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ======================= MMA issue =======================
+    if (lane == 0) {
+      // A MN-major (bit 15), B K-major; M = 128, N = BN
+      const uint32_t idesc = tf32_idesc(BN) | (1u << 15);
+      int it = 0, local = 0;
+      for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
+        int img, pt, nt, sp;
+        unit_coords(w, u, img, pt, nt, sp);
+        const int nk = min(w.kbps, w.nkb - sp * w.kbps);
+        const int b = local % w.nacc;
+        const uint32_t use = local / w.nacc;
+        mbar_wait(&acc_empty[b], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dacc = tmem + (uint32_t)(b * BN);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int s = it % w.nst;
+          mbar_wait(&split_full[s], (it / w.nst) & 1);
+          tc_fence_after();
+          const uint32_t st = smem_u32(base + s * w.stage_bytes);
+          const uint64_t abig = mn_sw128_32b_desc(st), asmall = mn_sw128_32b_desc(st + kABytes);
+          const uint64_t bbig = sw128_desc(st + 2 * kABytes);
+          const uint64_t bsmall = sw128_desc(st + 2 * kABytes + BN * 128);
+          // k-step ks (8 K rows): A start + 1 KB (two 4-row atoms), B start + 32 B
+          if (i == 0)
+            mma_ss<0>(dacc, asmall, bbig, idesc);
+          else
+            mma_ss<1>(dacc, asmall, bbig, idesc);
+          mma_ss<1>(dacc, abig, bsmall, idesc);
+          mma_ss<1>(dacc, abig, bbig, idesc);
+#pragma unroll
+          for (int ks = 1; ks < BK / 8; ++ks) {
+            const uint64_t ak = (uint64_t)((ks * 1024) >> 4), bk = (uint64_t)((ks * 32) >> 4);
+            mma_ss<1>(dacc, asmall + ak, bbig + bk, idesc);
+            mma_ss<1>(dacc, abig + ak, bsmall + bk, idesc);
+            mma_ss<1>(dacc, abig + ak, bbig + bk, idesc);
+          }
+          tc_commit(&empty[s]);
+        }
+        tc_commit(&acc_full[b]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ======================= epilogue =======================
+    const int ew = warp - kEpiWarp0;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    int local = 0;
+    for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
+      int img, pt, nt, sp;
+      unit_coords(w, u, img, pt, nt, sp);
+      const int b = local % w.nacc;
+      const uint32_t use = local / w.nacc;
+      mbar_wait(&acc_full[b], use & 1);
+      tc_fence_after();
+      const int pix = pt * BM + q * 32 + lane;
+      const bool live = pix < w.PQ;
+      const int m = img * w.PQ + pix;
+      const int n0 = nt * BN;
+      const int cols = BN / 2;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
+      const RowPtr rp = live ? (w.splits > 1 ? part.row(sp, m) : epi.row(m)) : RowPtr{nullptr, 0.f};
+#pragma unroll 1
+      for (int c0 = half * cols; c0 < half * cols + cols; c0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(taddr + (uint32_t)c0, v);
+        if (live) {
+          const int nlim = w.Nout - (n0 + c0);
+          if (w.splits > 1) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nlim) part.store(rp, n0 + c0 + j, __uint_as_float(v[j]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nlim) epi.store(rp, n0 + c0 + j, __uint_as_float(v[j]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [imgs][rows][PQ] fp32 activation viewed 3-D, box {32 pixels, 32 rows, 1}, 128B swizzle
+// with 32B atomicity (the MN-major tf32 layout, see mn_sw128_32b_desc)
+static bool make_act_map(CUtensorMap* map, const float* p, int PQ, int rows, int imgs) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)PQ, (cuuint64_t)rows, (cuuint64_t)imgs};
+  cuuint64_t strides[2] = {(cuuint64_t)PQ * 4, (cuuint64_t)PQ * rows * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)BK, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline int pick_bn(int N, int& ntiles) {
+  ntiles = (N + 255) / 256;
+  int per = (N + ntiles - 1) / ntiles;
+  return (per + 31) / 32 * 32;
+}
+
+// act: [imgs][K][PQ]; B(n, k) via lbp (pre-packed); D[m = img*PQ + pix][n] -> epi
+template <class LBP>
+int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, const EpiNCHW& epi,
+           float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
+  if (PQ % 4 || (reinterpret_cast<uintptr_t>(act) & 15) || K < 8) return -1;
+  CUtensorMap amap;
+  if (!make_act_map(&amap, act, PQ, K, imgs)) return -1;
+  Work w{};
+  w.PQ = PQ;
+  w.tiles_img = (PQ + BM - 1) / BM;
+  w.N_img = imgs;
+  w.Nout = Nout;
+  w.K = K;
+  w.BN = pick_bn(Nout, w.ntiles);
+  w.nkb = (K + BK - 1) / BK;
+  w.nacc = 2;
+  w.b_bytes = 2 * w.BN * 128;
+  w.stage_bytes = 2 * kABytes + w.b_bytes;
+  const int smem_cap = 227 * 1024;
+  const int tail = 1024 + (3 * kMaxStages + 4) * 8 + 64;
+  w.nst = std::min(kMaxStages, (smem_cap - tail) / w.stage_bytes);
+  if (w.nst < 2) return -1;
+  const int64_t pack_bytes = (int64_t)w.ntiles * w.nkb * w.b_bytes;
+  const int64_t pack_aligned = (pack_bytes + 1023) / 1024 * 1024;
+  if (!ws || ws_bytes < pack_aligned) return -1;
+  uint8_t* bpack = reinterpret_cast<uint8_t*>(ws);
+  float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned);
+  const int64_t part_bytes = ws_bytes - pack_aligned;
+  const int M = imgs * PQ;
+
+  launch_pack_b(lbp, Nout, K, w.BN, w.nkb, w.ntiles, bpack, st);
+  if (int rc = check_launch(what)) return rc;
+
+  const int sms = gemm_sm_budget();
+  w.splits = 1;
+  const int64_t tiles = (int64_t)imgs * w.tiles_img * w.ntiles;
+  if (tiles < sms) {
+    const int64_t want = sms / tiles;
+    const int64_t by_k = w.nkb / 2;
+    const int64_t by_ws = part_bytes / ((int64_t)M * Nout * 4);
+    w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
+                                                  std::min<int64_t>(by_ws, 64)));
+  }
+  w.kbps = (w.nkb + w.splits - 1) / w.splits;
+  w.splits = (w.nkb + w.kbps - 1) / w.kbps;
+  w.units = (int)(tiles * w.splits);
+
+  static bool configured = false;
+  if (!configured) {
+    BF_CUDA(cudaFuncSetAttribute(tc4_kernel<EpiNCHW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_cap),
+            "tc4 smem attribute");
+    configured = true;
+  }
+  const int smem = std::max(tail + w.nst * w.stage_bytes, 120 << 10);
+  const int grid = std::min(w.units, sms);
+  EpiPartial part{part_ws, M, Nout};
+  tc4_kernel<EpiNCHW><<<grid, kThreads, smem, st>>>(amap, w, bpack, epi, part);
+  if (int rc = check_launch(what)) return rc;
+  if (w.splits > 1) {
+    splitk_reduce_kernel<EpiNCHW><<<elementwise_grid((int64_t)M * Nout, 256), 256, 0, st>>>(
+        part_ws, w.splits, M, Nout, epi);
+    return check_launch(what);
+  }
+  return 0;
+}
+
+struct LdW1x1 {  // fwd: B(n = kout, k = c) = w[kout][c]
+  const float* w;
+  int C;
+  __device__ __forceinline__ float operator()(int n, int k) const {
+    return w[(int64_t)n * C + k];
+  }
+};
+struct LdW1x1T {  // dgrad: B(n = c, k = kout) = w[kout][c]
+  const float* w;
+  int C;
+  __device__ __forceinline__ float operator()(int n, int k) const {
+    return w[(int64_t)k * C + n];
+  }
+};
+
+}  // namespace tc4
+
+static bool tc4_eligible(const ConvShape& g) {
+  return g.R == 1 && g.S == 1 && g.stride == 1 && g.pad == 0 && g.P == g.H && g.Q == g.W &&
+         (g.H * g.W) % 4 == 0;
+}
+
+int tc4_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNCHW& epi,
+                 float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
+  if (!tc4_eligible(g)) return -1;
+  return tc4::launch(x, g.N, g.C, g.H * g.W, g.K, tc4::LdW1x1{w, g.C}, epi, ws, ws_bytes, st,
+                     what);
+}
+
+int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
+                   float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
+  if (!tc4_eligible(g)) return -1;
+  return tc4::launch(dy, g.N, g.K, g.H * g.W, g.C, tc4::LdW1x1T{w, g.C}, epi, ws, ws_bytes, st,
+                     what);
+}
+
+}  // namespace bf

@@ -43,13 +43,18 @@ CONV_CASES = [
     (2, 3, 13, 13, 8, 3, 2, 1, False),            # strided dgrad
     (2, 96, 14, 14, 208, 3, 1, 1, False),         # inception 4a 3x3 (dgrad: 208 = 6.5 blocks)
     (4, 48, 7, 7, 128, 5, 1, 2, False),           # inception 5b 5x5 (partial channel block)
+    (3, 480, 14, 14, 208, 1, 1, 0, False),        # 1x1, two pixel tiles per image
+    (2, 20, 6, 6, 40, 1, 1, 0, False),            # 1x1, partial channel block, tiny image
+    (2, 256, 28, 28, 384, 1, 1, 0, False),        # 1x1, two output-channel tiles
 ]
 
 
-@pytest.fixture(params=[0, 3], ids=["auto", "halo-v3"])
+@pytest.fixture(params=[0, 3, 4], ids=["auto", "halo-v3", "no-tma-1x1"])
 def gemm_engine(request):
-    """0 = default engine choice; 3 = also route stride-1 R x S convolutions
-    through the opt-in halo-staged engine v3 (gemm_tc3.cu)."""
+    """0 = default engine choice (1x1 convolutions through the TMA-fed engine
+    v4, gemm_tc4.cu); 3 = also route stride-1 R x S convolutions through the
+    opt-in halo-staged engine v3 (gemm_tc3.cu); 4 = 1x1 convolutions through
+    the gathering engine v2 instead of v4."""
     from paper_1412_6249_b200 import _native
 
     lib = _native.lib()
@@ -63,6 +68,8 @@ def test_conv_forward_backward(case, gemm_engine):
     n, c, h, w, k, r, s, p, fl = case
     if gemm_engine == 3 and not (s == 1 and r > 1):
         pytest.skip("engine v3 only takes stride-1 spatial filters")
+    if gemm_engine == 4 and r != 1:
+        pytest.skip("engine switch 4 only changes 1x1 convolutions")
     x = rnd(n, c, h, w)
     wt = rnd(k, c, r, r, scale=1.0 / np.sqrt(c * r * r))
     b = rnd(k)
