@@ -595,26 +595,33 @@ struct Vec<4> {
 template <int V>
 __global__ void lrn5_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
                                 float* __restrict__ scale, int N, int C, int HW, float a_n,
-                                float beta, float kk) {
+                                float beta, float kk, int CH) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int HWV = HW / V;
   if (t >= (int64_t)N * HWV) return;
   const int n = (int)(t / HWV), hw = (int)(t - (int64_t)n * HWV) * V;
   const int64_t base = (int64_t)n * C * HW + hw;
+  // this thread's channel chunk [c0, c1); the window starts 2 channels earlier
+  const int c0 = blockIdx.y * CH, c1 = min(C, c0 + CH);
   // per lane: squares window w0..w4 = sq[c-2 .. c+2], inputs x0..x2 = x[c .. c+2]
   float w[5][V], xs[3][V];
 #pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    if (j < C) Vec<V>::ld(x + base + (int64_t)j * HW, xs[j]);
+  for (int j = -2; j < 3; ++j) {
+    const int c = c0 + j;
+    float xv[V];
+    if (c >= 0 && c < C) {
+      Vec<V>::ld(x + base + (int64_t)c * HW, xv);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) xv[v] = 0.f;
+    }
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      if (j >= C) xs[j][v] = 0.f;
-      w[2 + j][v] = j < C ? __fmul_rn(xs[j][v], xs[j][v]) : 0.f;
+      w[2 + j][v] = (c >= 0 && c < C) ? __fmul_rn(xv[v], xv[v]) : 0.f;
+      if (j >= 0) xs[j][v] = xv[v];
     }
   }
-#pragma unroll
-  for (int v = 0; v < V; ++v) w[0][v] = w[1][v] = 0.f;
-  for (int c = 0; c < C; ++c) {
+  for (int c = c0; c < c1; ++c) {
     float xn[V];
     const bool more = c + 3 < C;
     if (more) Vec<V>::ld(x + base + (int64_t)(c + 3) * HW, xn);
@@ -654,12 +661,13 @@ template <int V>
 __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                 const float* __restrict__ scale, const float* __restrict__ dy,
                                 float* __restrict__ dx, int N, int C, int HW, float coef,
-                                float beta) {
+                                float beta, int CH) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int HWV = HW / V;
   if (t >= (int64_t)N * HWV) return;
   const int n = (int)(t / HWV), hw = (int)(t - (int64_t)n * HWV) * V;
   const int64_t base = (int64_t)n * C * HW + hw;
+  const int c0 = blockIdx.y * CH, c1 = min(C, c0 + CH);
   // r[0..4] = ratio[c-2 .. c+2] = dy*y/scale;  for c..c+2 also x, dy, scale^-beta
   float r[5][V], xs[3][V], ds[3][V], pw[3][V];
   auto enter = [&](int j, float (&xv)[V], float (&dv)[V], float (&pv)[V], float (&rv)[V]) {
@@ -674,18 +682,32 @@ __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __rest
       rv[v] = __fdiv_rn(__fmul_rn(dv[v], yv[v]), sv[v]);
     }
   };
+  // halo channels c0-2, c0-1: only their ratios
 #pragma unroll
-  for (int v = 0; v < V; ++v) r[0][v] = r[1][v] = 0.f;
+  for (int j = 0; j < 2; ++j) {
+    const int c = c0 - 2 + j;
+    if (c >= 0) {
+      float sv[V], yv[V], dv[V];
+      Vec<V>::ld(y + base + (int64_t)c * HW, yv);
+      Vec<V>::ld(dy + base + (int64_t)c * HW, dv);
+      Vec<V>::ld(scale + base + (int64_t)c * HW, sv);
+#pragma unroll
+      for (int v = 0; v < V; ++v) r[j][v] = __fdiv_rn(__fmul_rn(dv[v], yv[v]), sv[v]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < V; ++v) r[j][v] = 0.f;
+    }
+  }
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
-    if (j < C) {
-      enter(j, xs[j], ds[j], pw[j], r[2 + j]);
+    if (c0 + j < C) {
+      enter(c0 + j, xs[j], ds[j], pw[j], r[2 + j]);
     } else {
 #pragma unroll
       for (int v = 0; v < V; ++v) xs[j][v] = ds[j][v] = pw[j][v] = r[2 + j][v] = 0.f;
     }
   }
-  for (int c = 0; c < C; ++c) {
+  for (int c = c0; c < c1; ++c) {
     float out[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -719,6 +741,15 @@ __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __rest
       pw[0][v] = pw[1][v]; pw[1][v] = pw[2][v]; pw[2][v] = pn[v];
     }
   }
+}
+
+// channel chunk for the LRN walkers: enough (pixel group, chunk) threads to
+// fill the GPU several times over; each chunk re-reads a 2-channel halo
+static int lrn_chunk(int64_t pixel_threads, int C) {
+  const int64_t want = (int64_t)sm_count_current() * 2048 * 2;
+  int chunks = (int)std::min<int64_t>(std::max<int64_t>(1, want / std::max<int64_t>(1, pixel_threads)),
+                                      (C + 15) / 16);
+  return (C + chunks - 1) / chunks;
 }
 
 // bias gradient, stage 1: CTA (slice, channel) sums dy over its images and all
@@ -934,11 +965,15 @@ int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int 
     int64_t px = (int64_t)N * H * W;
     if (LRN_VEC == 4 && (H * W) % 4 == 0 && ((uintptr_t)x & 15) == 0 &&
         ((uintptr_t)y & 15) == 0 && ((uintptr_t)scale & 15) == 0)
-      lrn5_fwd_kernel<4><<<(int)((px / 4 + 255) / 256), 256, 0, as_stream(s)>>>(
-          x, y, scale, N, C, H * W, a_n, beta, k);
-    else
-      lrn5_fwd_kernel<1><<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(x, y, scale, N, C,
-                                                                          H * W, a_n, beta, k);
+    {
+      const int ch = lrn_chunk(px / 4, C);
+      lrn5_fwd_kernel<4><<<dim3((unsigned)((px / 4 + 255) / 256), (C + ch - 1) / ch), 256, 0,
+                           as_stream(s)>>>(x, y, scale, N, C, H * W, a_n, beta, k, ch);
+    } else {
+      const int ch = lrn_chunk(px, C);
+      lrn5_fwd_kernel<1><<<dim3((unsigned)((px + 255) / 256), (C + ch - 1) / ch), 256, 0,
+                           as_stream(s)>>>(x, y, scale, N, C, H * W, a_n, beta, k, ch);
+    }
     return check_launch("lrn_forward");
   }
   lrn_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
@@ -961,11 +996,15 @@ int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* 
     if (LRN_VEC == 4 && (H * W) % 4 == 0 &&
         (((uintptr_t)x | (uintptr_t)y | (uintptr_t)scale | (uintptr_t)dy | (uintptr_t)dx) & 15) ==
             0)
-      lrn5_bwd_kernel<4><<<(int)((px / 4 + 255) / 256), 256, 0, as_stream(s)>>>(
-          x, y, scale, dy, dx, N, C, H * W, coef, beta);
-    else
-      lrn5_bwd_kernel<1><<<(int)((px + 255) / 256), 256, 0, as_stream(s)>>>(
-          x, y, scale, dy, dx, N, C, H * W, coef, beta);
+    {
+      const int ch = lrn_chunk(px / 4, C);
+      lrn5_bwd_kernel<4><<<dim3((unsigned)((px / 4 + 255) / 256), (C + ch - 1) / ch), 256, 0,
+                           as_stream(s)>>>(x, y, scale, dy, dx, N, C, H * W, coef, beta, ch);
+    } else {
+      const int ch = lrn_chunk(px, C);
+      lrn5_bwd_kernel<1><<<dim3((unsigned)((px + 255) / 256), (C + ch - 1) / ch), 256, 0,
+                           as_stream(s)>>>(x, y, scale, dy, dx, N, C, H * W, coef, beta, ch);
+    }
     return check_launch("lrn_backward");
   }
   lrn_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(

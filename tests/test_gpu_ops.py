@@ -188,7 +188,8 @@ def test_avgpool_bitwise(shape, k, s, p):
     assert_bitwise(dx, O.avgpool_backward(x, dy, k, s, p))
 
 
-@pytest.mark.parametrize("shape", [(2, 64, 56, 56), (2, 7, 5, 5), (1, 2, 4, 4), (3, 4, 2, 2)])
+@pytest.mark.parametrize("shape", [(2, 64, 56, 56), (2, 7, 5, 5), (1, 2, 4, 4), (3, 4, 2, 2),
+                                   (1, 40, 6, 6), (2, 37, 3, 5)])
 def test_lrn(shape):
     x = rnd(*shape, scale=3.0)
     y, sc = O.lrn_forward(x)
