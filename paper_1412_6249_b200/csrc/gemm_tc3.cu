@@ -357,7 +357,7 @@ int launch(const Halo& h, const LdHaloW& lbp, int Nout, const EpiNCHW& epi, floa
     const int64_t want = sms / tiles;
     const int64_t by_ws = part_bytes / ((int64_t)Mreal * Nout * 4);
     w.splits = (int)std::max<int64_t>(1, std::min(std::min<int64_t>(want, h.ncb),
-                                                  std::min<int64_t>(by_ws, 64)));
+                                                  std::min<int64_t>(by_ws, 256)));
   }
   w.cbps = (h.ncb + w.splits - 1) / w.splits;
   w.splits = (h.ncb + w.cbps - 1) / w.cbps;

@@ -353,7 +353,7 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
     const int64_t by_k = w.nkb / 2;
     const int64_t by_ws = part_bytes / ((int64_t)M * Nout * 4);
     w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                  std::min<int64_t>(by_ws, 64)));
+                                                  std::min<int64_t>(by_ws, 256)));
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
   w.splits = (w.nkb + w.kbps - 1) / w.kbps;

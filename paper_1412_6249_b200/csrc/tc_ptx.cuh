@@ -155,5 +155,30 @@ inline void launch_pack_b(const LB& lb, int N, int K, int BN, int nkb, int ntile
                                                                             out);
 }
 
+// db[ko] = sum over k-blocks of the per-block partials (weight-gradient engines), in a fixed order
+// (strided per thread, then a shared-memory tree): deterministic
+static __global__ void bias_blocks_finish_kernel(const float* __restrict__ part, int nkb,
+                                          float* __restrict__ db) {
+  __shared__ float red[256];
+  const float* row = part + (size_t)blockIdx.x * nkb;
+  // four independent strided chains per thread (loads in flight), combined in a
+  // fixed order, then a fixed shared-memory tree
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int kb = threadIdx.x; kb < nkb; kb += 4 * 256) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = kb + u * 256;
+      if (k < nkb) acc[u] = __fadd_rn(acc[u], __ldg(row + k));
+    }
+  }
+  red[threadIdx.x] = __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = __fadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) db[blockIdx.x] = red[0];
+}
+
 }  // namespace tcu
 }  // namespace bf
