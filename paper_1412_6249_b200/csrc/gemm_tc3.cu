@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ======================= MMA issuer (as engine v2) =======================
-    if (lane == 0) {
+    // whole warp walks the schedule; one elected lane issues (see gemm_tc2.cu)
+    {
       const uint32_t idesc = tf32_idesc(BN);
       int it = 0, local = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
@@ -243,20 +244,23 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           const uint32_t bb = smem_u32(tiles + stage * stage_bytes);
           const uint32_t bs = bb + BN * 128;
           const uint32_t ab = tmem + kAColBase + stage * 64;
+          if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < BK / 8; ++ks) {
-            const uint64_t dbb = sw128_desc(bb + ks * 32), dbs = sw128_desc(bs + ks * 32);
-            const uint32_t a_big = ab + ks * 8, a_small = ab + 32 + ks * 8;
-            mma_ts(dacc, a_small, dbb, idesc, (i > 0 || ks > 0) ? 1u : 0u);
-            mma_ts(dacc, a_big, dbs, idesc, 1u);
-            mma_ts(dacc, a_big, dbb, idesc, 1u);
+            for (int ks = 0; ks < BK / 8; ++ks) {
+              const uint64_t dbb = sw128_desc(bb + ks * 32), dbs = sw128_desc(bs + ks * 32);
+              const uint32_t a_big = ab + ks * 8, a_small = ab + 32 + ks * 8;
+              mma_ts(dacc, a_small, dbb, idesc, (i > 0 || ks > 0) ? 1u : 0u);
+              mma_ts(dacc, a_big, dbs, idesc, 1u);
+              mma_ts(dacc, a_big, dbb, idesc, 1u);
+            }
+            tc_commit(&empty[stage]);
           }
-          tc_commit(&empty[stage]);
+          __syncwarp();
         }
-        tc_commit(&acc_full[b]);
+        if (elect_one()) tc_commit(&acc_full[b]);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else {
     // ======================= epilogue =======================
     const int ew = warp - kMmaWarp - 1;

@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == kMmaWarp) {
     // ======================= MMA issue =======================
-    if (lane == 0) {
+    // whole warp walks the schedule; one elected lane issues (see gemm_tc2.cu)
+    {
       // A MN-major (bit 15), B K-major; M = 128, N = BN
       const uint32_t idesc = tf32_idesc(BN) | (1u << 15);
       int it = 0, local = 0;
@@ -209,26 +210,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t abig = mn_sw128_32b_desc(st), asmall = mn_sw128_32b_desc(st + kABytes);
           const uint64_t bbig = sw128_desc(st + 2 * kABytes);
           const uint64_t bsmall = sw128_desc(st + 2 * kABytes + BN * 128);
-          // k-step ks (8 K rows): A start + 1 KB (two 4-row atoms), B start + 32 B
-          if (i == 0)
-            mma_ss<0>(dacc, asmall, bbig, idesc);
-          else
-            mma_ss<1>(dacc, asmall, bbig, idesc);
-          mma_ss<1>(dacc, abig, bsmall, idesc);
-          mma_ss<1>(dacc, abig, bbig, idesc);
+          if (elect_one()) {
+            // k-step ks (8 K rows): A start + 1 KB (two 4-row atoms), B start + 32 B
+            if (i == 0)
+              mma_ss<0>(dacc, asmall, bbig, idesc);
+            else
+              mma_ss<1>(dacc, asmall, bbig, idesc);
+            mma_ss<1>(dacc, abig, bsmall, idesc);
+            mma_ss<1>(dacc, abig, bbig, idesc);
 #pragma unroll
-          for (int ks = 1; ks < BK / 8; ++ks) {
-            const uint64_t ak = (uint64_t)((ks * 1024) >> 4), bk = (uint64_t)((ks * 32) >> 4);
-            mma_ss<1>(dacc, asmall + ak, bbig + bk, idesc);
-            mma_ss<1>(dacc, abig + ak, bsmall + bk, idesc);
-            mma_ss<1>(dacc, abig + ak, bbig + bk, idesc);
+            for (int ks = 1; ks < BK / 8; ++ks) {
+              const uint64_t ak = (uint64_t)((ks * 1024) >> 4), bk = (uint64_t)((ks * 32) >> 4);
+              mma_ss<1>(dacc, asmall + ak, bbig + bk, idesc);
+              mma_ss<1>(dacc, abig + ak, bsmall + bk, idesc);
+              mma_ss<1>(dacc, abig + ak, bbig + bk, idesc);
+            }
+            tc_commit(&empty[s]);
           }
-          tc_commit(&empty[s]);
+          __syncwarp();
         }
-        tc_commit(&acc_full[b]);
+        if (elect_one()) tc_commit(&acc_full[b]);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else {
     // ======================= epilogue =======================
     const int ew = warp - kEpiWarp0;
