@@ -30,21 +30,13 @@
 // per instruction even in straight-line code, and 110-150 cycles when each
 // instruction recomputes its descriptors and predicate; the issuer therefore
 // uses precomputed descriptor bases and literal accumulate flags.
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include <algorithm>
-#include <cstring>
 #include <type_traits>
 
 #include "gemm_common.cuh"
 #include "gemm_engines.cuh"
 #include "tc_ptx.cuh"
 
-#ifndef TC2_WGRAD_TMA
-#define TC2_WGRAD_TMA 0  // 1: weight-gradient dy tiles by TMA + in-kernel split instead of
-                          // the dY pack (measured slower: the split sits on the critical path)
-#endif
 
 namespace bf {
 namespace tc2 {
@@ -182,9 +174,6 @@ struct WgradGeom {
 __host__ inline WgradGeom wgrad_geom(const ConvShape& g) {
   WgradGeom w;
   w.Qp = g.Q <= 8 ? 8 : (g.Q + 15) / 16 * 16;
-  // rows of >= 32 columns padded to a multiple of 32 when dy can then be read
-  // by TMA (one box per k-block, no dY pack): conv1's 112 -> 128
-  if (TC2_WGRAD_TMA && g.Q > 16 && g.Q % 4 == 0) w.Qp = (g.Q + 31) / 32 * 32;
   const int rpc = 16 / (w.Qp < 16 ? w.Qp : 16);
   w.Pp = (g.P + rpc - 1) / rpc * rpc;
   return w;
@@ -303,8 +292,6 @@ constexpr int kKtabMax = 4096;  // k-table entries cached in shared memory per C
 struct Work {
   int M, N, K, BN, nst, nkb, kbps, splits, mtiles, ntiles, units, nacc, full_ktab;
   int nbst;   // B ring stages
-  int btma;   // weight gradient: B_big by TMA straight from dy, B_small split in-kernel
-  int bq, bp; // its box: bq padded columns x bp rows per 32-pixel k-block
   int abase;  // first TMEM column of the A ring
   int accs;   // TMEM column stride between the accumulator buffers
   int Pp, Qp;  // weight-gradient fast path: padded pixel grid of the K ordering
@@ -422,8 +409,7 @@ __device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowI
 
 template <class LA, class Epi, int MODE>
 __global__ void __launch_bounds__(kAllThreads, 1)
-    tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part,
-               const __grid_constant__ CUtensorMap ymap, float* __restrict__ bias_part) {
+    tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part) {
   using SA = Sep<LA>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -437,8 +423,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* bfull = empty + STAGES;
   uint64_t* bempty = bfull + kBStagesMax;
-  uint64_t* bsplit = bempty + kBStagesMax;  // btma: small part written (epilogue warps)
-  uint64_t* acc_full = bsplit + kBStagesMax;
+  uint64_t* acc_full = bempty + kBStagesMax;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -458,7 +443,6 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     for (int s = 0; s < kBStagesMax; ++s) {
       mbar_init(&bfull[s], 1);
       mbar_init(&bempty[s], 1);
-      mbar_init(&bsplit[s], kEpiWarps * 32);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -605,7 +589,6 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       const uint32_t idesc = tf32_idesc(BN);
       const uint64_t dtiles = sw128_desc(smem_u32(tiles));  // B stage 0, big image, k-step 0
       const uint64_t dsmall = (uint64_t)((BN * 128) >> 4);   // big -> small image
-      uint64_t* bready = w.btma ? bsplit : bfull;  // B stage complete (split in-kernel or not)
       int it = 0, local = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
         int mt, nt, sp;
@@ -619,7 +602,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         for (int i = 0; i < nk; ++i, ++it) {
           const int stage = it % w.nst, bst = it % w.nbst;
           const uint32_t phase = (it / w.nst) & 1;
-          mbar_wait(&bready[bst], (it / w.nbst) & 1);
+          mbar_wait(&bfull[bst], (it / w.nbst) & 1);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           // descriptor start-address field = smem byte address >> 4 (bits 0-13)
@@ -665,24 +648,10 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         for (int i = 0; i < nk; ++i, ++it) {
           const int bst = it % w.nbst;
           mbar_wait(&bempty[bst], ((it / w.nbst) & 1) ^ 1);
-          if (w.btma) {
-            // k-block kb = 32 consecutive padded pixels (n, p0.., q0..): one box of dy
-            const int kk = (kb0 + i) * BK, per = w.Pp * w.Qp;
-            const int n = kk / per, rem = kk - n * per;
-            const int p0 = rem / w.Qp, q0 = rem - p0 * w.Qp;
-            mbar_arrive_expect_tx(&bfull[bst], (uint32_t)(BN * 128));
-            asm volatile(
-                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(tiles + bst * stage_bytes)),
-                "l"(reinterpret_cast<uint64_t>(&ymap)), "r"(q0), "r"(p0), "r"(nt * BN), "r"(n),
-                "r"(smem_u32(&bfull[bst]))
-                : "memory");
-          } else {
-            mbar_arrive_expect_tx(&bfull[bst], (uint32_t)stage_bytes);
-            bulk_g2s(smem_u32(tiles + bst * stage_bytes),
-                     bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
-                     &bfull[bst]);
-          }
+          mbar_arrive_expect_tx(&bfull[bst], (uint32_t)stage_bytes);
+          bulk_g2s(smem_u32(tiles + bst * stage_bytes),
+                   bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
+                   &bfull[bst]);
         }
       }
     }
@@ -691,7 +660,6 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     // ======================= epilogue =======================
     const int ew = warp - kMmaWarp - 1;  // 0..kEpiWarps-1
     const int q = warp & 3;
-    int bit = 0;  // B-ring position (btma)
     const int half = kEpiWarps == 8 ? (ew >> 2) : 0;
     int local = 0;
     for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
@@ -699,38 +667,6 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       unit_coords(w, u, mt, nt, sp);
       const int b = local % w.nacc;
       const uint32_t use = local / w.nacc;
-      if (w.btma) {
-        // the unit's dy tiles: small = dy - trunc(dy) beside the TMA'd raw tile
-        // (one 128-byte row = 32 padded pixels of output channel k per thread) and,
-        // for m-tile 0, that row's sum: the fused bias gradient's block partial
-        const int et = threadIdx.x - (kMmaWarp + 1) * 32;
-        const int kb0 = sp * w.kbps, nk = min(w.kbps, w.nkb - kb0);
-        for (int i = 0; i < nk; ++i, ++bit) {
-          const int bst = bit % w.nbst;
-          mbar_wait(&bfull[bst], (bit / w.nbst) & 1);
-          uint8_t* st = tiles + bst * stage_bytes;
-          for (int r = et; r < BN; r += kEpiWarps * 32) {
-            const float4* src = reinterpret_cast<const float4*>(st + r * 128);
-            float4* dst = reinterpret_cast<float4*>(st + BN * 128 + r * 128);
-            float sum = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 v = src[j];
-              float4 o;
-              o.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-              o.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-              o.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-              o.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-              dst[j] = o;
-              sum = __fadd_rn(sum, __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
-            }
-            const int k = nt * BN + r;
-            if (bias_part && mt == 0 && k < w.N) bias_part[(size_t)k * w.nkb + kb0 + i] = sum;
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&bsplit[bst]);
-        }
-      }
       mbar_wait(&acc_full[b], use & 1);
       tc_fence_after();
       const int m = mt * BM + q * 32 + lane;
@@ -775,29 +711,6 @@ inline int pick_bn(int N, int& ntiles) {
   return (per + 31) / 32 * 32;
 }
 
-// dy [N][K][P][Q] as a 4-D TMA map, box {32 columns, 1 row, BN channels, 1 image}
-// with 128B swizzle: exactly the K-major B image (row k = 32 padded pixels)
-static bool make_dy_map(CUtensorMap* map, const float* dy, int Q, int P, int K, int imgs, int BN) {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return false;
-    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  if (reinterpret_cast<uintptr_t>(dy) & 15) return false;
-  cuuint64_t dims[4] = {(cuuint64_t)Q, (cuuint64_t)P, (cuuint64_t)K, (cuuint64_t)imgs};
-  cuuint64_t strides[3] = {(cuuint64_t)Q * 4, (cuuint64_t)P * Q * 4, (cuuint64_t)K * P * Q * 4};
-  cuuint32_t box[4] = {32, 1, (cuuint32_t)BN, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(dy), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <class LA, class LB, class LBP, class Epi>
 int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, const Epi& epi,
            float* ws, int64_t ws_bytes, cudaStream_t st, const char* what, int mode = -1,
@@ -831,16 +744,8 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
       reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + pack_aligned + bias_bytes);
   const int64_t part_bytes = ws_bytes - pack_aligned - bias_bytes;
 
-  CUtensorMap ymap;
-  memset(&ymap, 0, sizeof(ymap));
   if constexpr (std::is_same_v<LBP, LdWgradDYPad>) {
-    // dy's big TF32 part straight from HBM by TMA when a 32-pixel k-block is
-    // one box (padded rows of >= 32 columns, 16-byte row stride); else pre-pack
-    w.btma = TC2_WGRAD_TMA && lbp.Qp % 32 == 0 && lbp.Q % 4 == 0 &&
-             make_dy_map(&ymap, lbp.dy, lbp.Q, lbp.P, lbp.K, K / (lbp.Pp * lbp.Qp), w.BN);
-    if (!w.btma)
-      pack_dy_kernel<<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack,
-                                                            bias_ws);
+    pack_dy_kernel<<<dim3(w.nkb, w.ntiles), 256, 0, st>>>(lbp, N, K, w.BN, w.nkb, bpack, bias_ws);
   } else if (fast)
     launch_pack_b(lbp, N, K, w.BN, w.nkb, w.ntiles, bpack, st);
   else
@@ -864,7 +769,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.units = w.mtiles * w.ntiles * w.splits;
 
   const int smem_cap = 227 * 1024;
-  const int tail = 1024 + (2 * STAGES + 3 * kBStagesMax + 4) * 8 + 64;
+  const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
   w.full_ktab = (mode == kChannel || (mode == kGeneric && K <= kKtabMax)) ? 1 : 0;
   const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;  // as the kernel carves it
   w.nbst = (int)std::min<int64_t>(kBStagesMax, (smem_cap - tail - ktab_bytes) / stage_bytes);
@@ -884,20 +789,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   const int smem_req = std::max(smem, 120 << 10);
   const int grid = std::min(w.units, sms);
   EpiPartial part{part_ws, M, N};
-  float* bp = w.btma ? bias_ws : nullptr;
-  // direct launches (the tensor-map parameter is __grid_constant__)
-  if (mode == kChannel)
-    tc2_kernel<LA, Epi, kChannel><<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part,
-                                                                        ymap, bp);
-  else if (mode == kWgrad16)
-    tc2_kernel<LA, Epi, kWgrad16><<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part,
-                                                                        ymap, bp);
-  else if (mode == kWgrad8)
-    tc2_kernel<LA, Epi, kWgrad8><<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part,
-                                                                       ymap, bp);
-  else
-    tc2_kernel<LA, Epi, kGeneric><<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part,
-                                                                        ymap, bp);
+  kern<<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
     splitk_reduce_kernel<Epi><<<elementwise_grid((int64_t)M * N, 256), 256, 0, st>>>(
