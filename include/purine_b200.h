@@ -65,6 +65,10 @@ int bf_delay_ns(int64_t ns, bf_stream_t stream);
 int bf_relu_fwd(const float* x, float* y, int64_t n, bf_stream_t stream);
 /* relu_backward, ops.py:367-376 (dy where x > 0) */
 int bf_relu_bwd(const float* x, const float* dy, float* dx, int64_t n, bf_stream_t stream);
+/* relu_backward with dy = channels [c0, c0 + C) of a concatenated [N][ctot][HW]
+   gradient (the concat_backward copy is elided); x, dx are [N][C][HW] */
+int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, float* dx, int N,
+                      int C, int64_t HW, bf_stream_t stream);
 /* sgd_update, ops.py:428-437: out = w - f32(lr)*g, product rounded first */
 int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t n,
                   bf_stream_t stream);
@@ -107,6 +111,14 @@ int bf_conv2d_fwd_relu(const float* x, const float* w, const float* b, float* y,
                        int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                        int stride, int pad, float* workspace, int64_t ws_bytes,
                        bf_stream_t stream);
+/* the same with relu(y) written into channels [relu_c0, relu_c0 + K) of a
+   [N][relu_ctot][P][Q] tensor: the graph's following concat_forward copy
+   (ops: concat) is elided */
+int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, float* y,
+                             float* relu_cat, int relu_c0, int relu_ctot,
+                             int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                             int stride, int pad, float* workspace, int64_t ws_bytes,
+                             bf_stream_t stream);
 int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx,
                        int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                        int stride, int pad, float* workspace, int64_t ws_bytes,

@@ -37,6 +37,7 @@ _SIGS = {
     "bf_delay_ns": [_l, _p],
     "bf_relu_fwd": [_p, _p, _l, _p],
     "bf_relu_bwd": [_p, _p, _p, _l, _p],
+    "bf_relu_bwd_slice": [_p, _p, _i, _i, _p, _i, _i, _l, _p],
     "bf_sgd_update": [_p, _p, _p, _f, _l, _p],
     "bf_sgd_momentum": [_p, _p, _p, _p, _p, _f, _f, _l, _p],
     "bf_sgd_mean_update": [_p, _p, _p, _f, _i, _l, _p],
@@ -50,6 +51,7 @@ _SIGS = {
     "bf_fc_bwd_bias": [_p, _p, _i, _i, _p],
     "bf_conv2d_fwd": [_p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_fwd_relu": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
+    "bf_conv2d_fwd_relu_slice": [_p, _p, _p, _p, _p, _i, _i] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_data": [_p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_weight": [_p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_weight_bias": [_p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],

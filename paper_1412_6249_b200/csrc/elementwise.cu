@@ -88,6 +88,30 @@ __global__ void relu_bwd_s(const float* __restrict__ x, const float* __restrict_
     dx[i] = relu_g(x[i], dy[i]);
 }
 
+// relu_backward with dy read as a channel slice of a concatenated gradient
+// (the graph's concat_backward copy is elided): image n of dx/x covers
+// `run` = C*HW contiguous elements, its dy run starts at n*dy_img + dy_off
+__global__ void relu_bwd_slice_v4(const float4* __restrict__ x, const float4* __restrict__ dy,
+                                  float4* __restrict__ dx, int64_t run4, int64_t dy_img4,
+                                  int64_t dy_off4, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t img = i / run4, r = i - img * run4;
+    float4 a = x[i], g = dy[img * dy_img4 + dy_off4 + r];
+    dx[i] = make_float4(relu_g(a.x, g.x), relu_g(a.y, g.y), relu_g(a.z, g.z), relu_g(a.w, g.w));
+  }
+}
+
+__global__ void relu_bwd_slice_s(const float* __restrict__ x, const float* __restrict__ dy,
+                                 float* __restrict__ dx, int64_t run, int64_t dy_img,
+                                 int64_t dy_off, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t img = i / run, r = i - img * run;
+    dx[i] = relu_g(x[i], dy[img * dy_img + dy_off + r]);
+  }
+}
+
 __global__ void sgd_kernel(const float* __restrict__ w, const float* __restrict__ g,
                            float* __restrict__ out, float lr, int64_t n) {
   int64_t n4 = n >> 2;
@@ -225,6 +249,24 @@ int bf_relu_bwd(const float* x, const float* dy, float* dx, int64_t n, bf_stream
   if (n4 * 4 < n) relu_bwd_s<<<elementwise_grid(n - n4 * 4, kThreads), kThreads, 0, st>>>(
       x, dy, dx, n4 * 4, n);
   return check_launch("relu_backward", (n4 > 0) + (n4 * 4 < n));
+}
+
+int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, float* dx, int N,
+                      int C, int64_t HW, bf_stream_t s) {
+  BF_REQUIRE(N >= 0 && C >= 0 && c0 >= 0 && c0 + C <= ctot, "relu_backward(slice): bad channels");
+  const int64_t run = (int64_t)C * HW, n = run * N;
+  if (n <= 0) return 0;
+  cudaStream_t st = as_stream(s);
+  if (aligned16(x) && aligned16(dy_cat) && aligned16(dx) && run % 4 == 0 && HW % 4 == 0) {
+    relu_bwd_slice_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
+        reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy_cat),
+        reinterpret_cast<float4*>(dx), run / 4, (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4,
+        n / 4);
+  } else {
+    relu_bwd_slice_s<<<elementwise_grid(n, kThreads), kThreads, 0, st>>>(
+        x, dy_cat, dx, run, (int64_t)ctot * HW, (int64_t)c0 * HW, n);
+  }
+  return check_launch("relu_backward");
 }
 
 int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t n,

@@ -56,11 +56,21 @@ int bf_conv2d_fwd(const float* x, const float* w, const float* b, float* y, int 
 int bf_conv2d_fwd_relu(const float* x, const float* w, const float* b, float* y, float* y_relu,
                        int N, int C, int H, int W, int K, int R, int S, int P, int Q, int stride,
                        int pad, float* ws, int64_t ws_bytes, bf_stream_t s) {
+  return bf_conv2d_fwd_relu_slice(x, w, b, y, y_relu, 0, K, N, C, H, W, K, R, S, P, Q, stride,
+                                  pad, ws, ws_bytes, s);
+}
+
+int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, float* y,
+                             float* relu_cat, int relu_c0, int relu_ctot, int N, int C, int H,
+                             int W, int K, int R, int S, int P, int Q, int stride, int pad,
+                             float* ws, int64_t ws_bytes, bf_stream_t s) {
   if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
+  BF_REQUIRE(!relu_cat || (relu_c0 >= 0 && relu_c0 + K <= relu_ctot),
+             "conv2d_forward(+relu slice): bad channel range");
   ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
   LdFwdX la{x, g};
   LdRowK lb{w, (int64_t)C * R * S};
-  EpiNCHW epi{y, b, P * Q, K, y_relu};
+  EpiNCHW epi{y, b, P * Q, K, relu_cat, (int64_t)relu_ctot * P * Q, relu_c0};
   if (g_gemm_engine == 0 || g_gemm_engine == 3) {
     int rc = tc4_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
     if (rc >= 0) return rc;

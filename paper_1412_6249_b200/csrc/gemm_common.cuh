@@ -143,16 +143,25 @@ struct EpiNCHW {
   const float* bias;
   int PQ, Cout;
   float* relu_out = nullptr;
+  // relu_out layout: image stride (elements) and first channel, so the ReLU
+  // can land directly in a channel slice of a concatenated tensor
+  int64_t relu_img = 0;  // 0: same layout as out
+  int relu_c0 = 0;
   __device__ __forceinline__ void operator()(int m, int n, float v) const {
     int img = m / PQ, pq = m - img * PQ;
     if (bias) v = __fadd_rn(v, bias[n]);
     const int64_t o = ((int64_t)img * Cout + n) * PQ + pq;
     out[o] = v;
-    if (relu_out) relu_out[o] = relu_value(v);
+    if (relu_out) relu_out[relu_index(img, pq) + (int64_t)n * PQ] = relu_value(v);
+  }
+  __device__ __forceinline__ int64_t relu_index(int img, int pq) const {
+    return (relu_img ? (int64_t)img * relu_img : (int64_t)img * Cout * PQ) +
+           (int64_t)relu_c0 * PQ + pq;
   }
   __device__ __forceinline__ RowPtr row(int m) const {
     int img = m / PQ, pq = m - img * PQ;
-    return {out + (int64_t)img * Cout * PQ + pq, 0.f, relu_out ? relu_out - out : 0};
+    float* base = out + (int64_t)img * Cout * PQ + pq;
+    return {base, 0.f, relu_out ? (relu_out + relu_index(img, pq)) - base : 0};
   }
   __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
     if (bias) v = __fadd_rn(v, __ldg(bias + n));

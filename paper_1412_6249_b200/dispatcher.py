@@ -368,6 +368,45 @@ class _Plan:
             if sib:
                 self.fusion[sib[0]] = {"db": graph.tensors[op.outputs[0]].name}
                 self.fused_away.add(oid)
+        # concat elision (Inception): when every part of a concat_forward is a
+        # fused conv+ReLU output consumed by nothing else, each conv epilogue
+        # writes its ReLU straight into its channel slice of the concat output;
+        # when every part of a concat_backward feeds exactly one relu_backward,
+        # each relu_backward reads its slice of the concatenated gradient.  The
+        # concat operators become no-ops and their per-branch tensors are never
+        # materialised (``elided``); every other tensor is bit-identical.
+        self.elided: set[str] = set()
+        relu_src = {f["relu_out"]: p for p, f in self.fusion.items() if "relu_out" in f}
+        for oid, op in graph.operators.items():
+            if op.kind == "concat_forward":
+                parts = [graph.tensors[t] for t in op.inputs]
+                convs = [relu_src.get(t.name) for t in parts]
+                if any(c is None for c in convs) or any(
+                        len(graph.consumers_of(t)) != 1 for t in op.inputs):
+                    continue
+                out = graph.tensors[op.outputs[0]]
+                c0 = 0
+                for conv, t in zip(convs, parts):
+                    self.fusion[conv]["relu_slice"] = (out.name, out.shape, c0)
+                    self.elided.add(t.name)
+                    c0 += t.shape[1]
+                self.fused_away.add(oid)
+            elif op.kind == "concat_backward":
+                dy = graph.tensors[op.inputs[0]]
+                users = []
+                for t in op.outputs:
+                    cons = graph.consumers_of(t)
+                    ok = (len(cons) == 1 and graph.operators[cons[0][0]].kind == "relu_backward"
+                          and graph.operators[cons[0][0]].inputs[1] == t)
+                    users.append(cons[0][0] if ok else None)
+                if any(u is None for u in users):
+                    continue
+                c0 = 0
+                for u, t in zip(users, op.outputs):
+                    self.fusion[u] = {"dy_slice": (dy.name, c0, dy.shape[1])}
+                    self.elided.add(graph.tensors[t].name)
+                    c0 += graph.tensors[t].shape[1]
+                self.fused_away.add(oid)
 
     def _split_branches(self, graph: BiGraph, branches: int) -> None:
         """Event-driven device concurrency inside a lane: the lane's operators
@@ -437,7 +476,8 @@ def _fusion_enabled(registry) -> bool:
     # never bypassed)
     return all(registry.get(k) is KINDS[k] for k in ("conv2d_forward", "relu_forward",
                                                       "conv2d_backward_weight",
-                                                      "conv2d_backward_bias"))
+                                                      "conv2d_backward_bias", "concat_forward",
+                                                      "concat_backward", "relu_backward"))
 
 
 _PLAN_CACHE: dict[tuple[int, int, int], tuple[int, _Plan]] = {}
@@ -509,9 +549,10 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
                     _native.lib()("bf_delay_ns", int(delay * 1e9), ctx.stream)
                 if not (fuse and oid in plan.fused_away):
                     spec.execute(ctx, op)
-                else:  # computed by its producer's epilogue; still owns its output buffer
-                    t = graph.tensors[op.outputs[0]]
-                    store.ensure(t.name, t.shape)
+                else:  # computed by a neighbour (see _Plan); still owns its output buffers
+                    for tid in op.outputs:
+                        t = graph.tensors[tid]
+                        store.ensure(t.name, t.shape)
                 if trace:
                     t_end = torch.cuda.Event(enable_timing=True, external=True)
                     t_end.record(stream)

@@ -103,6 +103,12 @@ def _conv_fwd(ctx, op):
     x, w, b = _ins(ctx, op)
     (y,) = _outs(ctx, op)
     fused = getattr(ctx, "fused", None)
+    if fused and "relu_slice" in fused:  # ReLU straight into its slice of the concat output
+        name, shape, c0 = fused["relu_slice"]
+        cat = ctx.store.ensure(name, shape)
+        _L()("bf_conv2d_fwd_relu_slice", x.ptr, w.ptr, b.ptr, y.ptr, cat.ptr, c0, shape[1],
+             *_geom(x, w, op.attrs), *_ws(ctx), ctx.stream)
+        return
     if fused and "relu_out" in fused:  # the following relu_forward runs in this epilogue
         yr = ctx.store.ensure(fused["relu_out"], y.shape)
         _L()("bf_conv2d_fwd_relu", x.ptr, w.ptr, b.ptr, y.ptr, yr.ptr, *_geom(x, w, op.attrs),
@@ -166,6 +172,16 @@ def _relu_fwd(ctx, op):
 
 
 def _relu_bwd(ctx, op):
+    fused = getattr(ctx, "fused", None)
+    if fused and "dy_slice" in fused:  # dy = a channel slice of the concatenated gradient
+        name, c0, ctot = fused["dy_slice"]
+        x = ctx.store.get(ctx.graph.tensors[op.inputs[0]].name)
+        (dx,) = _outs(ctx, op)
+        cat = ctx.store.get(name)
+        n, c = x.shape[0], x.shape[1]
+        _L()("bf_relu_bwd_slice", x.ptr, cat.ptr, c0, ctot, dx.ptr, n, c, x.numel // (n * c),
+             ctx.stream)
+        return
     x, dy = _ins(ctx, op)
     (dx,) = _outs(ctx, op)
     _L()("bf_relu_bwd", x.ptr, dy.ptr, dx.ptr, x.numel, ctx.stream)
