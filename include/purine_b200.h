@@ -69,6 +69,11 @@ int bf_relu_bwd(const float* x, const float* dy, float* dx, int64_t n, bf_stream
    gradient (the concat_backward copy is elided); x, dx are [N][C][HW] */
 int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, float* dx, int N,
                       int C, int64_t HW, bf_stream_t stream);
+/* the same with dy = channels [c0, c0 + C) of the rank-ordered sum of k
+   concatenated gradients (parts: HOST array of k <= 32 device pointers): the
+   aggregate(sum) -> concat_backward pair is elided */
+int bf_relu_bwd_slice_sum(const float* x, const float* const* parts, int k, int c0, int ctot,
+                          float* dx, int N, int C, int64_t HW, bf_stream_t stream);
 /* sgd_update, ops.py:428-437: out = w - f32(lr)*g, product rounded first */
 int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t n,
                   bf_stream_t stream);

@@ -158,6 +158,28 @@ struct Parts {
   const float* p[32];
 };
 
+__global__ void aggregate_v4(Parts parts, int k, float4* __restrict__ out, int64_t n4, int mean) {
+  const float fk = (float)k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(parts.p[0])[i];
+    for (int j = 1; j < k; ++j) {
+      const float4 v = reinterpret_cast<const float4*>(parts.p[j])[i];
+      acc.x = __fadd_rn(acc.x, v.x);
+      acc.y = __fadd_rn(acc.y, v.y);
+      acc.z = __fadd_rn(acc.z, v.z);
+      acc.w = __fadd_rn(acc.w, v.w);
+    }
+    if (mean) {
+      acc.x = __fdiv_rn(acc.x, fk);
+      acc.y = __fdiv_rn(acc.y, fk);
+      acc.z = __fdiv_rn(acc.z, fk);
+      acc.w = __fdiv_rn(acc.w, fk);
+    }
+    out[i] = acc;
+  }
+}
+
 __global__ void aggregate_kernel(Parts parts, int k, float* __restrict__ out, int64_t n,
                                  int mean) {
   float fk = (float)k;
@@ -251,6 +273,65 @@ int bf_relu_bwd(const float* x, const float* dy, float* dx, int64_t n, bf_stream
   return check_launch("relu_backward", (n4 > 0) + (n4 * 4 < n));
 }
 
+// relu_backward whose dy is the channel slice of a rank-ordered SUM of k
+// concatenated gradients: the graph's aggregate(sum) -> concat_backward pair is
+// elided (ops.py:440-457 order: ((p0 + p1) + p2) + ...)
+__global__ void relu_bwd_slice_sum_v4(const float4* __restrict__ x, Parts parts, int k,
+                                      float4* __restrict__ dx, int64_t run4, int64_t dy_img4,
+                                      int64_t dy_off4, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t img = i / run4, r = i - img * run4;
+    const int64_t j = img * dy_img4 + dy_off4 + r;
+    float4 g = reinterpret_cast<const float4*>(parts.p[0])[j];
+    for (int q = 1; q < k; ++q) {
+      const float4 v = reinterpret_cast<const float4*>(parts.p[q])[j];
+      g.x = __fadd_rn(g.x, v.x);
+      g.y = __fadd_rn(g.y, v.y);
+      g.z = __fadd_rn(g.z, v.z);
+      g.w = __fadd_rn(g.w, v.w);
+    }
+    const float4 a = x[i];
+    dx[i] = make_float4(relu_g(a.x, g.x), relu_g(a.y, g.y), relu_g(a.z, g.z), relu_g(a.w, g.w));
+  }
+}
+
+__global__ void relu_bwd_slice_sum_s(const float* __restrict__ x, Parts parts, int k,
+                                     float* __restrict__ dx, int64_t run, int64_t dy_img,
+                                     int64_t dy_off, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t img = i / run, r = i - img * run;
+    const int64_t j = img * dy_img + dy_off + r;
+    float g = parts.p[0][j];
+    for (int q = 1; q < k; ++q) g = __fadd_rn(g, parts.p[q][j]);
+    dx[i] = relu_g(x[i], g);
+  }
+}
+
+int bf_relu_bwd_slice_sum(const float* x, const float* const* parts, int k, int c0, int ctot,
+                          float* dx, int N, int C, int64_t HW, bf_stream_t s) {
+  BF_REQUIRE(k >= 1 && k <= 32, "relu_backward(slice sum): 1 <= k <= 32 parts, got %d", k);
+  BF_REQUIRE(N >= 0 && C >= 0 && c0 >= 0 && c0 + C <= ctot, "relu_backward(slice): bad channels");
+  const int64_t run = (int64_t)C * HW, n = run * N;
+  if (n <= 0) return 0;
+  cudaStream_t st = as_stream(s);
+  Parts p;
+  bool vec = aligned16(x) && aligned16(dx) && run % 4 == 0 && HW % 4 == 0;
+  for (int i = 0; i < k; ++i) {
+    p.p[i] = parts[i];
+    vec = vec && aligned16(parts[i]);
+  }
+  if (vec)
+    relu_bwd_slice_sum_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
+        reinterpret_cast<const float4*>(x), p, k, reinterpret_cast<float4*>(dx), run / 4,
+        (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4, n / 4);
+  else
+    relu_bwd_slice_sum_s<<<elementwise_grid(n, kThreads), kThreads, 0, st>>>(
+        x, p, k, dx, run, (int64_t)ctot * HW, (int64_t)c0 * HW, n);
+  return check_launch("relu_backward");
+}
+
 int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, float* dx, int N,
                       int C, int64_t HW, bf_stream_t s) {
   BF_REQUIRE(N >= 0 && C >= 0 && c0 >= 0 && c0 + C <= ctot, "relu_backward(slice): bad channels");
@@ -302,9 +383,17 @@ int bf_aggregate(const float* const* parts, int k, float* out, int64_t n, int me
   BF_REQUIRE(k >= 1 && k <= 32, "aggregate: 1 <= k <= 32 inputs supported, got %d", k);
   if (n <= 0) return 0;
   Parts p;
-  for (int i = 0; i < k; ++i) p.p[i] = parts[i];
-  aggregate_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(p, k, out, n,
-                                                                                 mean);
+  bool vec = aligned16(out) && n % 4 == 0;
+  for (int i = 0; i < k; ++i) {
+    p.p[i] = parts[i];
+    vec = vec && aligned16(parts[i]);
+  }
+  if (vec)
+    aggregate_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, as_stream(s)>>>(
+        p, k, reinterpret_cast<float4*>(out), n / 4, mean);
+  else
+    aggregate_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(p, k, out, n,
+                                                                                   mean);
   return check_launch("aggregate");
 }
 

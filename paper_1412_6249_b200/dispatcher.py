@@ -401,9 +401,21 @@ class _Plan:
                     users.append(cons[0][0] if ok else None)
                 if any(u is None for u in users):
                     continue
+                # a rank-ordered sum feeding only this concat_backward (the gradient
+                # of an Inception module's input) is folded in as well
+                agg = graph.producer_of(op.inputs[0])
+                parts = None
+                if (agg is not None and graph.operators[agg].kind == "aggregate"
+                        and graph.operators[agg].attrs.get("mode", "mean") == "sum"
+                        and len(graph.consumers_of(op.inputs[0])) == 1
+                        and len(graph.operators[agg].inputs) <= 32):
+                    parts = [graph.tensors[t].name for t in graph.operators[agg].inputs]
+                    self.fused_away.add(agg)
+                    self.elided.add(dy.name)
                 c0 = 0
                 for u, t in zip(users, op.outputs):
-                    self.fusion[u] = {"dy_slice": (dy.name, c0, dy.shape[1])}
+                    self.fusion[u] = ({"dy_parts": (parts, c0, dy.shape[1])} if parts else
+                                      {"dy_slice": (dy.name, c0, dy.shape[1])})
                     self.elided.add(graph.tensors[t].name)
                     c0 += graph.tensors[t].shape[1]
                 self.fused_away.add(oid)
@@ -477,7 +489,8 @@ def _fusion_enabled(registry) -> bool:
     return all(registry.get(k) is KINDS[k] for k in ("conv2d_forward", "relu_forward",
                                                       "conv2d_backward_weight",
                                                       "conv2d_backward_bias", "concat_forward",
-                                                      "concat_backward", "relu_backward"))
+                                                      "concat_backward", "relu_backward",
+                                                      "aggregate"))
 
 
 _PLAN_CACHE: dict[tuple[int, int, int], tuple[int, _Plan]] = {}

@@ -173,6 +173,15 @@ def _relu_fwd(ctx, op):
 
 def _relu_bwd(ctx, op):
     fused = getattr(ctx, "fused", None)
+    if fused and "dy_parts" in fused:  # dy = slice of the (elided) sum of concatenated grads
+        names, c0, ctot = fused["dy_parts"]
+        x = ctx.store.get(ctx.graph.tensors[op.inputs[0]].name)
+        (dx,) = _outs(ctx, op)
+        parts = _native.ptr_array([ctx.store.get(nm).ptr for nm in names])
+        n, c = x.shape[0], x.shape[1]
+        _L()("bf_relu_bwd_slice_sum", x.ptr, parts, len(names), c0, ctot, dx.ptr, n, c,
+             x.numel // (n * c), ctx.stream)
+        return
     if fused and "dy_slice" in fused:  # dy = a channel slice of the concatenated gradient
         name, c0, ctot = fused["dy_slice"]
         x = ctx.store.get(ctx.graph.tensors[op.inputs[0]].name)
