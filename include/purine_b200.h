@@ -128,6 +128,11 @@ int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx,
                        int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                        int stride, int pad, float* workspace, int64_t ws_bytes,
                        bf_stream_t stream);
+/* data gradient with relu_backward folded into the epilogue (relu_x laid out as dx) */
+int bf_conv2d_bwd_data_relu(const float* w, const float* dy, float* dx, const float* relu_x,
+                            int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                            int stride, int pad, float* workspace, int64_t ws_bytes,
+                            bf_stream_t stream);
 int bf_conv2d_bwd_weight(const float* x, const float* dy, float* dw,
                          int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                          int stride, int pad, float* workspace, int64_t ws_bytes,
@@ -152,6 +157,11 @@ int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, i
                    int P, int Q, int kernel, int stride, int pad, bf_stream_t stream);
 int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, int H, int W,
                    int P, int Q, int kernel, int stride, int pad, bf_stream_t stream);
+/* the same with relu_backward folded in: dx = (relu_x > 0 ? dx : 0), relu_x laid
+   out as dx (the graph's following relu_backward and its dy tensor are elided) */
+int bf_maxpool_bwd_relu(const float* mask, const float* dy, float* dx, const float* relu_x,
+                        int N, int C, int H, int W, int P, int Q, int kernel, int stride, int pad,
+                        bf_stream_t stream);
 int bf_avgpool_fwd(const float* x, float* y, int N, int C, int H, int W, int P, int Q,
                    int kernel, int stride, int pad, bf_stream_t stream);
 int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P, int Q,
@@ -163,6 +173,10 @@ int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int 
 int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* dy, float* dx,
                int N, int C, int H, int W, int size, float alpha, float beta, float k,
                bf_stream_t stream);
+
+int bf_lrn_bwd_relu(const float* x, const float* y, const float* scale, const float* dy,
+                    float* dx, const float* relu_x, int N, int C, int H, int W, int size,
+                    float alpha, float beta, float k, bf_stream_t stream);
 
 /* channel concat (extension); parts/channels are HOST arrays, k <= 32 ---- */
 int bf_concat_fwd(const float* const* parts, const int* channels, int k, float* y,

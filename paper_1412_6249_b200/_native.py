@@ -54,16 +54,19 @@ _SIGS = {
     "bf_conv2d_fwd_relu": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_fwd_relu_slice": [_p, _p, _p, _p, _p, _i, _i] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_data": [_p, _p, _p] + [_i] * 11 + [_p, _l, _p],
+    "bf_conv2d_bwd_data_relu": [_p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_weight": [_p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_weight_bias": [_p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_bias": [_p, _p, _i, _i, _i, _p, _l, _p],
     "bf_gemm_workspace_bytes": [_i] * 12,
     "bf_maxpool_fwd": [_p, _p, _p] + [_i] * 9 + [_p],
     "bf_maxpool_bwd": [_p, _p, _p] + [_i] * 9 + [_p],
+    "bf_maxpool_bwd_relu": [_p, _p, _p, _p] + [_i] * 9 + [_p],
     "bf_avgpool_fwd": [_p, _p] + [_i] * 9 + [_p],
     "bf_avgpool_bwd": [_p, _p] + [_i] * 9 + [_p],
     "bf_lrn_fwd": [_p, _p, _p, _i, _i, _i, _i, _i, _f, _f, _f, _p],
     "bf_lrn_bwd": [_p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _f, _f, _f, _p],
+    "bf_lrn_bwd_relu": [_p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _f, _f, _f, _p],
     "bf_concat_fwd": [_p, _p, _i, _p, _i, _i, _i, _p],
     "bf_concat_bwd": [_p, _p, _p, _i, _i, _i, _i, _p],
     "bf_nccl_unique_id": [_p],

@@ -91,11 +91,19 @@ int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, flo
 int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx, int N, int C, int H, int W,
                        int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
                        int64_t ws_bytes, bf_stream_t s) {
+  return bf_conv2d_bwd_data_relu(w, dy, dx, nullptr, N, C, H, W, K, R, S, P, Q, stride, pad, ws,
+                                 ws_bytes, s);
+}
+
+int bf_conv2d_bwd_data_relu(const float* w, const float* dy, float* dx, const float* relu_x,
+                            int N, int C, int H, int W, int K, int R, int S, int P, int Q,
+                            int stride, int pad, float* ws, int64_t ws_bytes, bf_stream_t s) {
   if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
   ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
   LdDgradDY la{dy, g};
   LdDgradW lb{w, g};
   EpiNCHW epi{dx, nullptr, H * W, C};
+  epi.relu_x = relu_x;
   if (g_gemm_engine == 0 || g_gemm_engine == 3) {
     int rc = tc4_conv_dgrad(g, dy, w, epi, ws, ws_bytes, as_stream(s), "conv2d_backward_data");
     if (rc >= 0) return rc;

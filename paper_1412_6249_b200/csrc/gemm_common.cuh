@@ -147,10 +147,13 @@ struct EpiNCHW {
   // can land directly in a channel slice of a concatenated tensor
   int64_t relu_img = 0;  // 0: same layout as out
   int relu_c0 = 0;
+  // relu_backward folded in (dgrad): out = (relu_x > 0 ? v : 0), relu_x laid out as out
+  const float* relu_x = nullptr;
   __device__ __forceinline__ void operator()(int m, int n, float v) const {
     int img = m / PQ, pq = m - img * PQ;
     if (bias) v = __fadd_rn(v, bias[n]);
     const int64_t o = ((int64_t)img * Cout + n) * PQ + pq;
+    if (relu_x) v = relu_x[o] > 0.f ? v : 0.f;
     out[o] = v;
     if (relu_out) relu_out[relu_index(img, pq) + (int64_t)n * PQ] = relu_value(v);
   }
@@ -166,8 +169,30 @@ struct EpiNCHW {
   __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
     if (bias) v = __fadd_rn(v, __ldg(bias + n));
     float* p = r.p + (int64_t)n * PQ;
+    if (relu_x) v = __ldg(relu_x + (p - out)) > 0.f ? v : 0.f;
     *p = v;
     if (relu_out) p[r.relu_delta] = relu_value(v);
+  }
+  // 16 consecutive columns of one row (the tcgen05 epilogues): the folded
+  // ReLU's x values are all loaded before any store, so the loads overlap
+  __device__ __forceinline__ void store16(const RowPtr& r, int n0, const uint32_t (&v)[16],
+                                          int nlim) const {
+    float m[16];
+    if (relu_x) {
+      const float* mx = relu_x + (r.p - out) + (int64_t)n0 * PQ;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) m[j] = j < nlim ? __ldg(mx + (int64_t)j * PQ) : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j >= nlim) continue;
+      float x = __uint_as_float(v[j]);
+      if (bias) x = __fadd_rn(x, __ldg(bias + n0 + j));
+      if (relu_x) x = m[j] > 0.f ? x : 0.f;
+      float* p = r.p + (int64_t)(n0 + j) * PQ;
+      *p = x;
+      if (relu_out) p[r.relu_delta] = relu_value(x);
+    }
   }
 };
 
@@ -184,6 +209,12 @@ struct EpiT {
   __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
     if (bias) v = __fadd_rn(v, r.bias_row);
     r.p[n * ldo] = v;
+  }
+  __device__ __forceinline__ void store16(const RowPtr& r, int n0, const uint32_t (&v)[16],
+                                          int nlim) const {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nlim) store(r, n0 + j, __uint_as_float(v[j]));
   }
 };
 

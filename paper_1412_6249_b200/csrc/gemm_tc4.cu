@@ -264,9 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 16; ++j)
               if (j < nlim) part.store(rp, n0 + c0 + j, __uint_as_float(v[j]));
           } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nlim) epi.store(rp, n0 + c0 + j, __uint_as_float(v[j]));
+            epi.store16(rp, n0 + c0, v, nlim);
           }
         }
       }

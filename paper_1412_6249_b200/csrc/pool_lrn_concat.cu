@@ -57,9 +57,16 @@ __device__ __forceinline__ void covering(int h, int stride, int pad, int k, int 
   hi = min((h + pad) / stride + 1, P);
 }
 
+// relu_backward folded into the kernel producing its dy (dispatcher fusion):
+// relu_g(x, g) = x > 0 ? g : 0 exactly as elementwise.cu
+__device__ __forceinline__ float relu_fold(const float* __restrict__ rx, int64_t i, float v) {
+  return rx ? (__ldg(rx + i) > 0.f ? v : 0.f) : v;
+}
+
 __global__ void maxpool_bwd_kernel(const float* __restrict__ mask, const float* __restrict__ dy,
                                    float* __restrict__ dx, int64_t total, int H, int W, int P,
-                                   int Q, int k, int stride, int pad) {
+                                   int Q, int k, int stride, int pad,
+                                   const float* __restrict__ relu_x) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     int w = (int)(i % W);
@@ -75,7 +82,7 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ mask, const float* 
     for (int p = p0; p < p1; ++p)
       for (int q = q0; q < q1; ++q)
         if (mp[p * Q + q] == me) acc = __fadd_rn(acc, gp[p * Q + q]);
-    dx[i] = acc;
+    dx[i] = relu_fold(relu_x, i, acc);
   }
 }
 
@@ -152,7 +159,7 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, float* __restrict__ 
 __global__ void lrn_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                const float* __restrict__ scale, const float* __restrict__ dy,
                                float* __restrict__ dx, int64_t total, int C, int HW, int pre,
-                               int post, float coef, float beta) {
+                               int post, float coef, float beta, const float* __restrict__ relu_x) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     int c = (int)((i / HW) % C);
@@ -165,7 +172,7 @@ __global__ void lrn_bwd_kernel(const float* __restrict__ x, const float* __restr
     }
     float a = __fmul_rn(dy[i], powf(scale[i], -beta));
     float b = __fmul_rn(__fmul_rn(coef, x[i]), acc);
-    dx[i] = __fsub_rn(a, b);
+    dx[i] = relu_fold(relu_x, i, __fsub_rn(a, b));
   }
 }
 
@@ -300,7 +307,7 @@ __global__ void maxpool_fwd_plane(const float* __restrict__ x, float* __restrict
 
 __global__ void maxpool_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
                                   float* __restrict__ dx, int H, int W, int P, int Q, int k,
-                                  int stride, int pad) {
+                                  int stride, int pad, const float* __restrict__ relu_x) {
   extern __shared__ float sm[];
   float* ms = sm;
   float* gs = sm + P * Q;
@@ -322,7 +329,7 @@ __global__ void maxpool_bwd_plane(const float* __restrict__ mask, const float* _
     for (int p = p0; p < p1; ++p)
       for (int q = q0; q < q1; ++q)
         if (ms[p * Q + q] == me) acc = __fadd_rn(acc, gs[p * Q + q]);
-    dp[i] = acc;
+    dp[i] = relu_fold(relu_x, pl * (int64_t)H * W + i, acc);
   }
 }
 
@@ -455,7 +462,7 @@ __device__ __forceinline__ void stage_pairs(float2* __restrict__ dst, const floa
 template <int S, int CW>
 __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
                                    float* __restrict__ dx, int planes, int G, int H, int W, int P,
-                                   int Q, int pad) {
+                                   int Q, int pad, const float* __restrict__ relu_x) {
   extern __shared__ float2 pairs_all[];
   const int64_t pl0 = (int64_t)blockIdx.x * G;
   const int g_here = (int)(planes - pl0 < G ? planes - pl0 : G);
@@ -469,7 +476,8 @@ __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* 
   for (int rr = warp * RPW + roff; rr < g_here * H; rr += nw * RPW) {
     const int g = rr / H, h = rr - g * H;
     const float2* pr = pairs_all + g * PQ;
-    float* dp = dx + (pl0 + g) * (int64_t)H * W + h * W;
+    const int64_t row0 = (pl0 + g) * (int64_t)H * W + h * W;
+    float* dp = dx + row0;
     // output rows whose window covers h: p*S - pad <= h <= p*S - pad + 2
     const int hp = h + pad;
     const int p0 = hp < 3 ? 0 : (hp - 3) / S + 1;
@@ -497,7 +505,7 @@ __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* 
           acc = __fadd_rn(acc, (ok && mg.x == me) ? mg.y : 0.f);
         }
       }
-      dp[w] = acc;
+      dp[w] = relu_fold(relu_x, row0 + w, acc);
     }
   }
 }
@@ -511,7 +519,7 @@ __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* 
 template <int CW>
 __global__ void maxpool3s2_bwd_plane(const float* __restrict__ mask, const float* __restrict__ dy,
                                      float* __restrict__ dx, int planes, int G, int H, int W,
-                                     int P, int Q, int pad) {
+                                     int P, int Q, int pad, const float* __restrict__ relu_x) {
   extern __shared__ float2 pairs_all[];
   const int64_t pl0 = (int64_t)blockIdx.x * G;
   const int g_here = (int)(planes - pl0 < G ? planes - pl0 : G);
@@ -525,7 +533,8 @@ __global__ void maxpool3s2_bwd_plane(const float* __restrict__ mask, const float
   for (int rr = warp * RPW + roff; rr < g_here * BI; rr += nw * RPW) {
     const int g = rr / BI, i = rr - g * BI;
     const float2* pr = pairs_all + g * PQ;
-    float* dp = dx + (pl0 + g) * (int64_t)H * W;
+    const int64_t pbase = (pl0 + g) * (int64_t)H * W;
+    float* dp = dx + pbase;
     const int h0 = 2 * i - pad;
     const bool r0 = h0 >= 0, r1 = h0 + 1 < H;  // block rows inside the plane
     const bool pa = i - 1 >= 0 && i - 1 < P, pb = i < P;
@@ -555,13 +564,14 @@ __global__ void maxpool3s2_bwd_plane(const float* __restrict__ mask, const float
       a10 = __fadd_rn(a10, (bb && wBB.x == e10) ? wBB.y : 0.f);
       a11 = __fadd_rn(a11, (bb && wBB.x == e11) ? wBB.y : 0.f);
       const bool c0 = w0 >= 0, c1 = w0 + 1 < W;
+      const int64_t o00 = (int64_t)h0 * W + w0, o10 = o00 + W;
       if (r0) {
-        if (c0) dp[h0 * W + w0] = a00;
-        if (c1) dp[h0 * W + w0 + 1] = a01;
+        if (c0) dp[o00] = relu_fold(relu_x, pbase + o00, a00);
+        if (c1) dp[o00 + 1] = relu_fold(relu_x, pbase + o00 + 1, a01);
       }
       if (r1) {
-        if (c0) dp[(h0 + 1) * W + w0] = a10;
-        if (c1) dp[(h0 + 1) * W + w0 + 1] = a11;
+        if (c0) dp[o10] = relu_fold(relu_x, pbase + o10, a10);
+        if (c1) dp[o10 + 1] = relu_fold(relu_x, pbase + o10 + 1, a11);
       }
     }
   }
@@ -661,7 +671,7 @@ template <int V>
 __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                 const float* __restrict__ scale, const float* __restrict__ dy,
                                 float* __restrict__ dx, int N, int C, int HW, float coef,
-                                float beta, int CH) {
+                                float beta, int CH, const float* __restrict__ relu_x) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int HWV = HW / V;
   if (t >= (int64_t)N * HWV) return;
@@ -720,6 +730,12 @@ __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __rest
       const float a = __fmul_rn(ds[0][v], pw[0][v]);
       const float b = __fmul_rn(__fmul_rn(coef, xs[0][v]), acc);
       out[v] = __fsub_rn(a, b);
+    }
+    if (relu_x) {
+      float rx[V];
+      Vec<V>::ld(relu_x + base + (int64_t)c * HW, rx);
+#pragma unroll
+      for (int v = 0; v < V; ++v) out[v] = rx[v] > 0.f ? out[v] : 0.f;
     }
     Vec<V>::st(dx + base + (int64_t)c * HW, out);
     float xn[V], dn[V], pn[V], rn[V];
@@ -884,6 +900,12 @@ int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, i
 
 int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, int H, int W,
                    int P, int Q, int kernel, int stride, int pad, bf_stream_t s) {
+  return bf_maxpool_bwd_relu(mask, dy, dx, nullptr, N, C, H, W, P, Q, kernel, stride, pad, s);
+}
+
+int bf_maxpool_bwd_relu(const float* mask, const float* dy, float* dx, const float* relu_x, int N,
+                        int C, int H, int W, int P, int Q, int kernel, int stride, int pad,
+                        bf_stream_t s) {
   int64_t total = (int64_t)N * C * H * W;
   if (total <= 0) return 0;
   const int smem = 2 * P * Q * 4;
@@ -912,7 +934,7 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
       const int sm = G * 2 * P * Q * 4;
       const int cw = W <= 8 ? 8 : (W <= 16 ? 16 : 32);
 #define BF_MP3B(SS, CC) \
-  maxpool3_bwd_plane<SS, CC><<<blocks, 256, sm, as_stream(s)>>>(mask, dy, dx, planes, G, H, W, P, Q, pad)
+  maxpool3_bwd_plane<SS, CC><<<blocks, 256, sm, as_stream(s)>>>(mask, dy, dx, planes, G, H, W, P, Q, pad, relu_x)
       if (stride == 1) {
         if (cw == 8) BF_MP3B(1, 8); else if (cw == 16) BF_MP3B(1, 16); else BF_MP3B(1, 32);
       } else {
@@ -920,7 +942,7 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
         const int cw2 = bj <= 8 ? 8 : (bj <= 16 ? 16 : 32);
 #define BF_MP3B2(CC)                                                                            \
   maxpool3s2_bwd_plane<CC><<<blocks, 256, sm, as_stream(s)>>>(mask, dy, dx, planes, G, H, W, P, \
-                                                              Q, pad)
+                                                              Q, pad, relu_x)
         if (cw2 == 8) BF_MP3B2(8); else if (cw2 == 16) BF_MP3B2(16); else BF_MP3B2(32);
 #undef BF_MP3B2
       }
@@ -928,11 +950,11 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
       return check_launch("maxpool_backward");
     }
     maxpool_bwd_plane<<<N * C, 256, smem, as_stream(s)>>>(mask, dy, dx, H, W, P, Q, kernel,
-                                                          stride, pad);
+                                                          stride, pad, relu_x);
     return check_launch("maxpool_backward");
   }
   maxpool_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
-      mask, dy, dx, total, H, W, P, Q, kernel, stride, pad);
+      mask, dy, dx, total, H, W, P, Q, kernel, stride, pad, relu_x);
   return check_launch("maxpool_backward");
 }
 
@@ -984,6 +1006,12 @@ int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int 
 int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* dy, float* dx,
                int N, int C, int H, int W, int size, float alpha, float beta, float k,
                bf_stream_t s) {
+  return bf_lrn_bwd_relu(x, y, scale, dy, dx, nullptr, N, C, H, W, size, alpha, beta, k, s);
+}
+
+int bf_lrn_bwd_relu(const float* x, const float* y, const float* scale, const float* dy,
+                    float* dx, const float* relu_x, int N, int C, int H, int W, int size,
+                    float alpha, float beta, float k, bf_stream_t s) {
   BF_REQUIRE(size >= 1, "lrn_backward: size must be >= 1");
   int64_t total = (int64_t)N * C * H * W;
   if (total <= 0) return 0;
@@ -994,21 +1022,23 @@ int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* 
   if (size == 5) {
     int64_t px = (int64_t)N * H * W;
     if (LRN_VEC == 4 && (H * W) % 4 == 0 &&
-        (((uintptr_t)x | (uintptr_t)y | (uintptr_t)scale | (uintptr_t)dy | (uintptr_t)dx) & 15) ==
-            0)
+        (((uintptr_t)x | (uintptr_t)y | (uintptr_t)scale | (uintptr_t)dy | (uintptr_t)dx |
+          (uintptr_t)relu_x) & 15) == 0)
     {
       const int ch = lrn_chunk(px / 4, C);
       lrn5_bwd_kernel<4><<<dim3((unsigned)((px / 4 + 255) / 256), (C + ch - 1) / ch), 256, 0,
-                           as_stream(s)>>>(x, y, scale, dy, dx, N, C, H * W, coef, beta, ch);
+                           as_stream(s)>>>(x, y, scale, dy, dx, N, C, H * W, coef, beta, ch,
+                                           relu_x);
     } else {
       const int ch = lrn_chunk(px, C);
       lrn5_bwd_kernel<1><<<dim3((unsigned)((px + 255) / 256), (C + ch - 1) / ch), 256, 0,
-                           as_stream(s)>>>(x, y, scale, dy, dx, N, C, H * W, coef, beta, ch);
+                           as_stream(s)>>>(x, y, scale, dy, dx, N, C, H * W, coef, beta, ch,
+                                           relu_x);
     }
     return check_launch("lrn_backward");
   }
   lrn_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
-      x, y, scale, dy, dx, total, C, H * W, pre, post, coef, beta);
+      x, y, scale, dy, dx, total, C, H * W, pre, post, coef, beta, relu_x);
   (void)k;
   return check_launch("lrn_backward");
 }

@@ -420,6 +420,24 @@ class _Plan:
                     c0 += graph.tensors[t].shape[1]
                 self.fused_away.add(oid)
 
+        # relu_backward folded into the operator producing its dy (a data
+        # gradient epilogue, the max-pool or LRN backward kernel) when that dy
+        # has no other consumer: the producer writes relu_backward's dx directly
+        # (bit-identical: the same x > 0 ? g : 0 select), dy is never stored
+        foldable = tuple(k for k in os.environ.get(RELU_FOLD_ENV, RELU_FOLD_DEFAULT).split(",") if k)
+        for oid, op in graph.operators.items():
+            if op.kind != "relu_backward" or oid in self.fusion or len(op.inputs) != 2:
+                continue
+            g = op.inputs[1]
+            p = graph.producer_of(g)
+            if (p is None or graph.operators[p].kind not in foldable or p in self.fusion
+                    or len(graph.consumers_of(g)) != 1 or p in self.fused_away):
+                continue
+            self.fusion[p] = {"relu_x": graph.tensors[op.inputs[0]].name,
+                              "relu_dx": graph.tensors[op.outputs[0]].name}
+            self.fused_away.add(oid)
+            self.elided.add(graph.tensors[g].name)
+
     def _split_branches(self, graph: BiGraph, branches: int) -> None:
         """Event-driven device concurrency inside a lane: the lane's operators
         are spread over up to ``branches`` CUDA streams by greedy chain
@@ -479,6 +497,10 @@ def _branch_streams() -> int:
 
 
 FUSE_ENV = "PURINE_B200_FUSE"  # "0" disables epilogue fusion (A/B and debugging)
+# producer kinds that may absorb the relu_backward after them (all three have the
+# kernel support; measured net gains decide the default)
+RELU_FOLD_ENV = "PURINE_B200_RELU_FOLD"
+RELU_FOLD_DEFAULT = "conv2d_backward_data,lrn_backward"
 
 
 def _fusion_enabled(registry) -> bool:
@@ -490,7 +512,8 @@ def _fusion_enabled(registry) -> bool:
                                                       "conv2d_backward_weight",
                                                       "conv2d_backward_bias", "concat_forward",
                                                       "concat_backward", "relu_backward",
-                                                      "aggregate"))
+                                                      "aggregate", "conv2d_backward_data",
+                                                      "maxpool_backward", "lrn_backward"))
 
 
 _PLAN_CACHE: dict[tuple[int, int, int], tuple[int, _Plan]] = {}

@@ -138,8 +138,23 @@ def _conv_bwd(ctx, op):
     _conv_bwd_parts(ctx, op.attrs, x, w, dy, dx, dw, db)
 
 
+def _relu_fold(ctx, op):
+    """(relu_x, output) when the following relu_backward is folded into this
+    operator (dispatcher _Plan): write relu_backward's dx instead of our dy."""
+    fused = getattr(ctx, "fused", None)
+    if not (fused and "relu_x" in fused):
+        return None, None
+    rx = ctx.store.get(fused["relu_x"])
+    return rx, ctx.store.ensure(fused["relu_dx"], rx.shape)
+
+
 def _conv_bwd_data(ctx, op):
     x, w, dy = _ins(ctx, op)
+    rx, rdx = _relu_fold(ctx, op)
+    if rx is not None:
+        _L()("bf_conv2d_bwd_data_relu", w.ptr, dy.ptr, rdx.ptr, rx.ptr, *_geom(x, w, op.attrs),
+             *_ws(ctx), ctx.stream)
+        return
     (dx,) = _outs(ctx, op)
     _conv_bwd_parts(ctx, op.attrs, x, w, dy, dx, None, None)
 
@@ -315,9 +330,14 @@ def _maxpool_fwd(ctx, op):
 
 def _maxpool_bwd(ctx, op):
     x, mask, dy = _ins(ctx, op)
-    (dx,) = _outs(ctx, op)
     k, s, p = pool_attrs(op.attrs)
     n, c, h, w = x.shape
+    rx, rdx = _relu_fold(ctx, op)
+    if rx is not None:
+        _L()("bf_maxpool_bwd_relu", mask.ptr, dy.ptr, rdx.ptr, rx.ptr, n, c, h, w, dy.shape[2],
+             dy.shape[3], k, s, p, ctx.stream)
+        return
+    (dx,) = _outs(ctx, op)
     _L()("bf_maxpool_bwd", mask.ptr, dy.ptr, dx.ptr, n, c, h, w, dy.shape[2], dy.shape[3], k, s,
          p, ctx.stream)
 
@@ -348,8 +368,13 @@ def _lrn_fwd(ctx, op):
 
 def _lrn_bwd(ctx, op):
     x, y, scale, dy = _ins(ctx, op)
-    (dx,) = _outs(ctx, op)
     size, alpha, beta, k = lrn_attrs(op.attrs)
+    rx, rdx = _relu_fold(ctx, op)
+    if rx is not None:
+        _L()("bf_lrn_bwd_relu", x.ptr, y.ptr, scale.ptr, dy.ptr, rdx.ptr, rx.ptr, *x.shape, size,
+             alpha, beta, k, ctx.stream)
+        return
+    (dx,) = _outs(ctx, op)
     _L()("bf_lrn_bwd", x.ptr, y.ptr, scale.ptr, dy.ptr, dx.ptr, *x.shape, size, alpha, beta, k,
          ctx.stream)
 
