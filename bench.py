@@ -291,12 +291,18 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(args.steps):
-            store.set(xname, x_pin)
-            store.set(lname, l_pin)
+        # every step: its batch is copied host->device inside the timed region
+        # (prefetched on a side stream while the previous step computes) and
+        # its loss is read back
+        exe.prefetch({xname: x_pin, lname: l_pin})
+        reads = []
+        for s in range(args.steps):
             exe.step()
-            _ = store.array(loss_name)
+            reads.append(store.read_async(loss_name))  # this step's loss, device -> host
+            if s + 1 < args.steps:
+                exe.prefetch({xname: x_pin, lname: l_pin})
         e1.record()
+        e2e_losses = [float(r.value()[0]) for r in reads]
         e1.synchronize()
         e2e_ms = e0.elapsed_time(e1)
         if dist is not None:
@@ -306,7 +312,11 @@ def run_ours(args):
         e2e = {"value": world * args.batch * args.steps / (e2e_ms / 1e3), "unit": "img/s",
                "h2d_bytes_per_step": int(x_pin.numel() * 4 + l_pin.numel() * 4),
                "d2h_bytes_per_step": 4, "wall_s": time.perf_counter() - t0,
-               "api": "TensorStore.set(pinned) -> CapturedSequence.step() -> TensorStore.array(loss)"}
+               "api": "CapturedSequence.prefetch(pinned batch) -> .step() -> "
+                      "TensorStore.read_async(loss)",
+               "overlap": "batch i+1's host->device copy runs on a side stream during step i; "
+                          "each step's loss is copied to pinned host memory behind it",
+               "losses_finite": bool(np.all(np.isfinite(e2e_losses)))}
 
     # traced replay of the same schedule, serialised on one stream per lane
     # (branch streams off) so each operator's interval is its own kernels'

@@ -53,6 +53,11 @@ class CapturedSequence:
         # per parity, per graph: [(op id, start event, end event)] recorded by the replays
         self.timing: list[list[list]] = [[], []]
         self.launches_per_step = 0
+        self._copy_stream = None  # prefetch(): host->device copies of the next step's inputs
+        self._staging: dict[tuple[int, str], torch.Tensor] = {}
+        self._pending = None
+        self._slot = 0
+        self._consumed: list = [None, None]
 
     def _ctx(self, g, it=0):
         return RunContext(store=self.store, graph=g, iteration=it)
@@ -123,9 +128,55 @@ class CapturedSequence:
                 out.append((gi, g.operators[oid], s, s + int(round(a.elapsed_time(b) * 1e6))))
         return out
 
+    def prefetch(self, inputs: dict) -> None:
+        """Start copying the NEXT step's source tensors (name -> pinned host
+        torch tensor, e.g. the data batch and labels) on a side stream into
+        device staging buffers; the following `step()` waits for the copy and
+        moves the staged data into the bound tensors with one device-to-device
+        copy each.  Issued right after `step()`, the host->device transfer of
+        batch i+1 overlaps the compute of batch i (the reference's feeder
+        writes the store synchronously before each iteration, builders.py:
+        284-365)."""
+        dev = self.store.device
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=dev)
+        cs = self._copy_stream
+        # two staging sets: this copy may only overwrite the set whose previous
+        # contents were already moved into the bound tensors (event recorded
+        # right after those device-to-device copies, not after the whole step)
+        slot = self._slot
+        self._slot ^= 1
+        if self._consumed[slot] is not None:
+            cs.wait_event(self._consumed[slot])
+        else:
+            cs.wait_stream(torch.cuda.current_stream(dev))
+        staged = {}
+        with torch.cuda.stream(cs):
+            for name, src in inputs.items():
+                key = (slot, name)
+                buf = self._staging.get(key)
+                if buf is None or buf.shape != src.shape:
+                    buf = torch.empty(src.shape, dtype=torch.float32, device=dev)
+                    self._staging[key] = buf
+                buf.copy_(src, non_blocking=True)
+                staged[name] = buf
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        self._pending = (staged, ev, slot)
+
     def step(self, after_graph=None, iteration: int = 0) -> None:
         if not self.ready:
             raise DispatchError("CapturedSequence.step() before prepare()")
+        if self._pending is not None:  # inputs staged by prefetch()
+            staged, ev, slot = self._pending
+            self._pending = None
+            cur = torch.cuda.current_stream(self.store.device)
+            cur.wait_event(ev)
+            for name, buf in staged.items():
+                self.store.get(name).data.copy_(buf.reshape(self.store.get(name).data.shape))
+            done = torch.cuda.Event()
+            done.record(cur)
+            self._consumed[slot] = done
         for gi, cg in enumerate(self.graphs[self.parity]):
             if cg is None:
                 self._run_eager(gi, iteration)

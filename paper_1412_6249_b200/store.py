@@ -74,6 +74,17 @@ def _as_f32_tensor(array, device) -> torch.Tensor:
     return torch.from_numpy(arr).to(device)
 
 
+class PendingRead:
+    """Result of `TensorStore.read_async`."""
+
+    def __init__(self, host, event, shape) -> None:
+        self._host, self._event, self._shape = host, event, shape
+
+    def value(self) -> np.ndarray:
+        self._event.synchronize()
+        return self._host.numpy().reshape(self._shape)
+
+
 class TensorStore:
     """Named device buffers shared by every graph of a run."""
 
@@ -127,6 +138,17 @@ class TensorStore:
     def array(self, name: str) -> np.ndarray:
         """Host snapshot (synchronises with the work that produced it)."""
         return self.get(name).data.detach().cpu().numpy().reshape(self.get(name).shape)
+
+    def read_async(self, name: str) -> "PendingRead":
+        """Device->host copy of ``name`` enqueued on the current stream into
+        pinned memory; `.value()` waits for it.  Lets a training loop read
+        every step's loss without stalling the host between steps."""
+        t = self.get(name)
+        host = torch.empty(t.data.shape, dtype=torch.float32, pin_memory=True)
+        host.copy_(t.data, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return PendingRead(host, ev, t.shape)
 
     def has(self, name: str) -> bool:
         return name in self._tensors

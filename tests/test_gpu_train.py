@@ -264,3 +264,39 @@ def test_dag_net_iteration_matches_oracle(factory, monkeypatch):
     assert_close(store.array("loss"), ref["loss"], rtol=RTOL, atol=ATOL, what="loss")
     n = _teacher_forced_check(seq, store)
     assert n >= len(seq.graphs[0].operators) - 5
+
+
+def test_prefetched_inputs_match_synchronous_feed():
+    """CapturedSequence.prefetch (host->device copy of the next batch on a side
+    stream, consumed by the next step) trains bit-identically to writing the
+    batch into the store before each step."""
+    import torch
+
+    from paper_1412_6249_b200.exchange import build_rank_sequence
+    from paper_1412_6249_b200.executor import CapturedSequence
+
+    net = cifar_convnet(batch=4, lr=0.01)
+    feed = SyntheticFeed.for_net(net, 11, spread=0.0)
+    results = []
+    for mode in ("sync", "prefetch"):
+        st = TensorStore("cuda:0")
+        seq, _ = build_rank_sequence(net, 1, 0, st, bucket_bytes=32 << 10)
+        init_params(net, st, 11, seq.layout)
+        xname, lname = seq.layout.data_names[0], seq.layout.label_names[0]
+        batches = [feed.batch_for(it, 0) for it in range(4)]
+        st.set(xname, batches[0][0])
+        st.set(lname, batches[0][1])
+        exe = CapturedSequence(seq, st)
+        exe.prepare()
+        pinned = [(torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory())
+                  for x, y in batches]
+        for it in range(1, 4):
+            if mode == "sync":
+                st.set(xname, pinned[it][0])
+                st.set(lname, pinned[it][1])
+            else:
+                exe.prefetch({xname: pinned[it][0], lname: pinned[it][1]})
+            exe.step()
+        results.append({p: st.array(f"{p}_p0") for p, _ in net.param_shapes()})
+    for p in results[0]:
+        assert np.array_equal(results[0][p], results[1][p]), p
