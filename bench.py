@@ -369,6 +369,25 @@ def run_ours(args):
                          "intervals of a traced replay" + ("" if world > 1 else
                                                            "; world 1: the exchange is the "
                                                            "local fused mean+SGD, no NCCL"))}
+    # the virtual-time simulator calibrated with this run's
+    # per-operator device times predicts the 1..8-GPU scaling of this config
+    predicted = None
+    if rank == 0 and world == 1:
+        from paper_1412_6249_b200.costsim import predict_scaling
+
+        op_s = {name: t / 1e3 for name, (kind, t, _f, _b) in rows.items()}
+        try:
+            first = predict_scaling(net, [1], op_s)[0]
+            scale = (ms / args.steps / 1e3) / first.iteration_s
+            pts = predict_scaling(net, [1, 2, 4, 8], op_s, compute_scale=scale)
+            predicted = {"basis": "costsim.predict_scaling: measured op times (scaled to the "
+                                  "measured step), NVLink bucket-exchange model x1.5 overlap "
+                                  "slowdown; a prediction, not a measurement",
+                         "points": [{"n_gpus": p.world, "img_s": round(p.images_per_s, 1),
+                                     "efficiency": round(p.efficiency, 4),
+                                     "exposed_comm": round(p.exposed_comm, 4)} for p in pts]}
+        except Exception as exc:  # noqa: BLE001 - the prediction is optional
+            predicted = {"error": str(exc)}
     if args.op_table and rank == 0:
         with open(args.op_table, "w") as f:
             f.write("op\tkind\tms\tgflop\tmbytes\n")
@@ -416,6 +435,7 @@ def run_ours(args):
                    "image": 224, "parallelism": f"dp{world}",
                    "l2": "inputs (77 MB/batch) and activations (~3.4 GB) exceed the 126 MB L2"},
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "exposed_comm": exposed,
+        "predicted_scaling": predicted,
         "clocks": clocks.summary(),
         "gpu_launches": int(exe.launches_per_step) * args.steps,
         "launches_per_step": int(exe.launches_per_step),
