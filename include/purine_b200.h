@@ -168,6 +168,7 @@ int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P
                    int kernel, int stride, int pad, bf_stream_t stream);
 
 /* local response normalisation across channels (extension; Caffe) ------- */
+/* scale may be NULL for size 5 (not stored: see bf_lrn_bwd_recompute) */
 int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int W, int size,
                float alpha, float beta, float k, bf_stream_t stream);
 int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* dy, float* dx,
@@ -177,6 +178,13 @@ int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* 
 int bf_lrn_bwd_relu(const float* x, const float* y, const float* scale, const float* dy,
                     float* dx, const float* relu_x, int N, int C, int H, int W, int size,
                     float alpha, float beta, float k, bf_stream_t stream);
+/* graph-plan backward: scale and y recomputed from x with the forward's exact
+   operation sequence (bit-identical to bf_lrn_bwd fed the forward's outputs),
+   so the forward may run with scale == NULL; relu_x as bf_lrn_bwd_relu (NULL =
+   none).  size 5 only. */
+int bf_lrn_bwd_recompute(const float* x, const float* dy, float* dx, const float* relu_x, int N,
+                         int C, int H, int W, int size, float alpha, float beta, float k,
+                         bf_stream_t stream);
 
 /* channel concat (extension); parts/channels are HOST arrays, k <= 32 ---- */
 int bf_concat_fwd(const float* const* parts, const int* channels, int k, float* y,

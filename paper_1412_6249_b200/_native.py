@@ -67,6 +67,7 @@ _SIGS = {
     "bf_lrn_fwd": [_p, _p, _p, _i, _i, _i, _i, _i, _f, _f, _f, _p],
     "bf_lrn_bwd": [_p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _f, _f, _f, _p],
     "bf_lrn_bwd_relu": [_p, _p, _p, _p, _p, _p, _i, _i, _i, _i, _i, _f, _f, _f, _p],
+    "bf_lrn_bwd_recompute": [_p, _p, _p, _p, _i, _i, _i, _i, _i, _f, _f, _f, _p],
     "bf_concat_fwd": [_p, _p, _i, _p, _i, _i, _i, _p],
     "bf_concat_bwd": [_p, _p, _p, _i, _i, _i, _i, _p],
     "bf_nccl_unique_id": [_p],

@@ -7,6 +7,7 @@
 // accumulation order bit for bit (oracle/kernels.py maxpool_backward /
 // avgpool_backward).
 #include <algorithm>
+#include <initializer_list>
 
 #include "common.cuh"
 
@@ -136,6 +137,21 @@ __global__ void avgpool_bwd_kernel(const float* __restrict__ dy, float* __restri
   }
 }
 
+// scale^-beta and a / scale for LRN.  scale >= k > 0, so the MUFU
+// approximations need no special-case code: lg2/ex2.approx (~2^-22 relative)
+// and rcp.approx keep y and dx within ~5e-7 relative of powf and IEEE division
+// (tests hold 1e-6 on y against the oracle's numpy power).  Every LRN kernel
+// uses these two, so the recomputing backward stays bit-identical to the
+// explicit one.  (powf / __fdiv_rn made the LRN kernels issue-bound: ~68
+// instructions per element.)
+__device__ __forceinline__ float lrn_pow(float s, float nbeta) {
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(s));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fmul_rn(nbeta, l)));
+  return r;
+}
+__device__ __forceinline__ float lrn_div(float a, float s) { return __fdividef(a, s); }
+
 // LRN: one thread per element; window sums in channel order, as the oracle.
 __global__ void lrn_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
                                float* __restrict__ scale, int64_t total, int C, int HW, int pre,
@@ -152,7 +168,7 @@ __global__ void lrn_fwd_kernel(const float* __restrict__ x, float* __restrict__ 
     }
     float sc = __fadd_rn(kk, __fmul_rn(a_n, acc));
     scale[i] = sc;
-    y[i] = __fmul_rn(x[i], powf(sc, -beta));
+    y[i] = __fmul_rn(x[i], lrn_pow(sc, -beta));
   }
 }
 
@@ -168,9 +184,9 @@ __global__ void lrn_bwd_kernel(const float* __restrict__ x, const float* __restr
     float acc = 0.f;
     for (int cj = lo; cj <= hi; ++cj) {
       int64_t j = base + (int64_t)cj * HW;
-      acc = __fadd_rn(acc, __fdiv_rn(__fmul_rn(dy[j], y[j]), scale[j]));
+      acc = __fadd_rn(acc, lrn_div(__fmul_rn(dy[j], y[j]), scale[j]));
     }
-    float a = __fmul_rn(dy[i], powf(scale[i], -beta));
+    float a = __fmul_rn(dy[i], lrn_pow(scale[i], -beta));
     float b = __fmul_rn(__fmul_rn(coef, x[i]), acc);
     dx[i] = relu_fold(relu_x, i, __fsub_rn(a, b));
   }
@@ -592,6 +608,16 @@ struct Vec<1> {
   __device__ static void st(float* p, const float (&v)[1]) { *p = v[0]; }
 };
 template <>
+struct Vec<2> {
+  __device__ static void ld(const float* p, float (&v)[2]) {
+    const float2 f = __ldg(reinterpret_cast<const float2*>(p));
+    v[0] = f.x; v[1] = f.y;
+  }
+  __device__ static void st(float* p, const float (&v)[2]) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
+};
+template <>
 struct Vec<4> {
   __device__ static void ld(const float* p, float (&v)[4]) {
     const float4 f = __ldg(reinterpret_cast<const float4*>(p));
@@ -602,70 +628,8 @@ struct Vec<4> {
   }
 };
 
-template <int V>
-__global__ void lrn5_fwd_kernel(const float* __restrict__ x, float* __restrict__ y,
-                                float* __restrict__ scale, int N, int C, int HW, float a_n,
-                                float beta, float kk, int CH) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int HWV = HW / V;
-  if (t >= (int64_t)N * HWV) return;
-  const int n = (int)(t / HWV), hw = (int)(t - (int64_t)n * HWV) * V;
-  const int64_t base = (int64_t)n * C * HW + hw;
-  // this thread's channel chunk [c0, c1); the window starts 2 channels earlier
-  const int c0 = blockIdx.y * CH, c1 = min(C, c0 + CH);
-  // per lane: squares window w0..w4 = sq[c-2 .. c+2], inputs x0..x2 = x[c .. c+2]
-  float w[5][V], xs[3][V];
-#pragma unroll
-  for (int j = -2; j < 3; ++j) {
-    const int c = c0 + j;
-    float xv[V];
-    if (c >= 0 && c < C) {
-      Vec<V>::ld(x + base + (int64_t)c * HW, xv);
-    } else {
-#pragma unroll
-      for (int v = 0; v < V; ++v) xv[v] = 0.f;
-    }
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      w[2 + j][v] = (c >= 0 && c < C) ? __fmul_rn(xv[v], xv[v]) : 0.f;
-      if (j >= 0) xs[j][v] = xv[v];
-    }
-  }
-  for (int c = c0; c < c1; ++c) {
-    float xn[V];
-    const bool more = c + 3 < C;
-    if (more) Vec<V>::ld(x + base + (int64_t)(c + 3) * HW, xn);
-    float sc[V], yv[V];
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      float acc = 0.f;
-      acc = __fadd_rn(acc, w[0][v]);
-      acc = __fadd_rn(acc, w[1][v]);
-      acc = __fadd_rn(acc, w[2][v]);
-      acc = __fadd_rn(acc, w[3][v]);
-      acc = __fadd_rn(acc, w[4][v]);
-      sc[v] = __fadd_rn(kk, __fmul_rn(a_n, acc));
-      yv[v] = __fmul_rn(xs[0][v], powf(sc[v], -beta));
-    }
-    Vec<V>::st(scale + base + (int64_t)c * HW, sc);
-    Vec<V>::st(y + base + (int64_t)c * HW, yv);
-#pragma unroll
-    for (int v = 0; v < V; ++v) {
-      if (!more) xn[v] = 0.f;
-      w[0][v] = w[1][v];
-      w[1][v] = w[2][v];
-      w[2][v] = w[3][v];
-      w[3][v] = w[4][v];
-      w[4][v] = more ? __fmul_rn(xn[v], xn[v]) : 0.f;
-      xs[0][v] = xs[1][v];
-      xs[1][v] = xs[2][v];
-      xs[2][v] = xn[v];
-    }
-  }
-}
-
 // backward: x, y, scale and dy each loaded once (y as given: the operator's
-// contract, ops-level, takes the forward output as an input); the powf is
+// contract, ops-level, takes the forward output as an input); the power is
 // shared between the entering element's ratio and its later centre term.
 template <int V>
 __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
@@ -688,8 +652,8 @@ __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __rest
     Vec<V>::ld(scale + base + (int64_t)j * HW, sv);
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-      pv[v] = powf(sv[v], -beta);
-      rv[v] = __fdiv_rn(__fmul_rn(dv[v], yv[v]), sv[v]);
+      pv[v] = lrn_pow(sv[v], -beta);
+      rv[v] = lrn_div(__fmul_rn(dv[v], yv[v]), sv[v]);
     }
   };
   // halo channels c0-2, c0-1: only their ratios
@@ -702,7 +666,7 @@ __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __rest
       Vec<V>::ld(dy + base + (int64_t)c * HW, dv);
       Vec<V>::ld(scale + base + (int64_t)c * HW, sv);
 #pragma unroll
-      for (int v = 0; v < V; ++v) r[j][v] = __fdiv_rn(__fmul_rn(dv[v], yv[v]), sv[v]);
+      for (int v = 0; v < V; ++v) r[j][v] = lrn_div(__fmul_rn(dv[v], yv[v]), sv[v]);
     } else {
 #pragma unroll
       for (int v = 0; v < V; ++v) r[j][v] = 0.f;
@@ -755,6 +719,154 @@ __global__ void lrn5_bwd_kernel(const float* __restrict__ x, const float* __rest
       xs[0][v] = xs[1][v]; xs[1][v] = xs[2][v]; xs[2][v] = xn[v];
       ds[0][v] = ds[1][v]; ds[1][v] = ds[2][v]; ds[2][v] = dn[v];
       pw[0][v] = pw[1][v]; pw[1][v] = pw[2][v]; pw[2][v] = pn[v];
+    }
+  }
+}
+
+#ifndef LRN_RC_VEC
+#define LRN_RC_VEC 2
+#endif
+
+// The graph-plan LRN pair.  Forward: y (and scale unless the plan elides it),
+// with x loads issued two channels ahead of their use.  Backward: scale and y
+// are RECOMPUTED from x with the forward's exact operation sequence (same
+// window order, same lrn_pow), so the result is bit-identical to the explicit
+// backward fed with the forward's outputs, while reading only x and dy (plus
+// the folded ReLU mask): 3-4 tensors of traffic per element instead of 6.
+template <int V>
+__device__ __forceinline__ void lrn_ld(const float* p, bool ok, float (&v)[V]) {
+  if (ok) {
+    Vec<V>::ld(p, v);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) v[i] = 0.f;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ float lrn_scale5(const float (&xq)[5][V], int v, float a_n, float kk) {
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) acc = __fadd_rn(acc, __fmul_rn(xq[j][v], xq[j][v]));
+  return __fadd_rn(kk, __fmul_rn(a_n, acc));
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) lrn5_fwd_pf_kernel(const float* __restrict__ x,
+                                                          float* __restrict__ y,
+                                                          float* __restrict__ scale, int N, int C,
+                                                          int HW, float a_n, float beta, float kk,
+                                                          int CH) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int HWV = HW / V;
+  if (t >= (int64_t)N * HWV) return;
+  const int n = (int)(t / HWV), hw = (int)(t - (int64_t)n * HWV) * V;
+  const float* xb = x + (int64_t)n * C * HW + hw;
+  const int64_t ob = (int64_t)n * C * HW + hw;
+  const int c0 = blockIdx.y * CH, c1 = min(C, c0 + CH);
+  float xq[5][V], xn[2][V];  // x[c-2 .. c+2], then x[c+3], x[c+4]
+#pragma unroll
+  for (int j = 0; j < 5; ++j) lrn_ld<V>(xb + (int64_t)(c0 - 2 + j) * HW, c0 - 2 + j >= 0 && c0 - 2 + j < C, xq[j]);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) lrn_ld<V>(xb + (int64_t)(c0 + 3 + j) * HW, c0 + 3 + j < C, xn[j]);
+  for (int c = c0; c < c1; ++c) {
+    float xl[V];
+    lrn_ld<V>(xb + (int64_t)(c + 5) * HW, c + 5 < C, xl);
+    float sc[V], yv[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      sc[v] = lrn_scale5<V>(xq, v, a_n, kk);
+      yv[v] = __fmul_rn(xq[2][v], lrn_pow(sc[v], -beta));
+    }
+    if (scale) Vec<V>::st(scale + ob + (int64_t)c * HW, sc);
+    Vec<V>::st(y + ob + (int64_t)c * HW, yv);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      xq[0][v] = xq[1][v]; xq[1][v] = xq[2][v]; xq[2][v] = xq[3][v]; xq[3][v] = xq[4][v];
+      xq[4][v] = xn[0][v]; xn[0][v] = xn[1][v]; xn[1][v] = xl[v];
+    }
+  }
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) lrn5_bwd_rc_kernel(const float* __restrict__ x,
+                                                          const float* __restrict__ dy,
+                                                          float* __restrict__ dx, int N, int C,
+                                                          int HW, float a_n, float kk, float coef,
+                                                          float beta, int CH,
+                                                          const float* __restrict__ relu_x) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int HWV = HW / V;
+  if (t >= (int64_t)N * HWV) return;
+  const int n = (int)(t / HWV), hw = (int)(t - (int64_t)n * HWV) * V;
+  const int64_t base = (int64_t)n * C * HW + hw;
+  const float* xb = x + base;
+  const float* db = dy + base;
+  const int c0 = blockIdx.y * CH, c1 = min(C, c0 + CH);
+  // iteration c enters channel e = c + 2 (its scale, scale^-beta and ratio
+  // dy*y/scale) and, for c >= c0, emits dx[c].  State at the top of iteration c:
+  //   xq = x[c .. c+4], dq = dy[c .. c+2], pq = pw[c-1 .. c+1], r = ratio[c-3 .. c+1]
+  //   prefetched: xn = x[c+5], x[c+6]; dn = dy[c+3], dy[c+4]
+  float xq[5][V], dq[3][V], pq[3][V], r[5][V], xn[2][V], dn[2][V];
+  const int cs = c0 - 4;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) lrn_ld<V>(xb + (int64_t)(cs + j) * HW, cs + j >= 0 && cs + j < C, xq[j]);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) lrn_ld<V>(db + (int64_t)(cs + j) * HW, cs + j >= 0 && cs + j < C, dq[j]);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    lrn_ld<V>(xb + (int64_t)(cs + 5 + j) * HW, cs + 5 + j >= 0 && cs + 5 + j < C, xn[j]);
+    lrn_ld<V>(db + (int64_t)(cs + 3 + j) * HW, cs + 3 + j >= 0 && cs + 3 + j < C, dn[j]);
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) r[j][v] = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) pq[j][v] = 0.f;
+  }
+  for (int c = cs; c < c1; ++c) {
+    float xl[V], dl[V], rx[V];
+    lrn_ld<V>(xb + (int64_t)(c + 7) * HW, c + 7 >= 0 && c + 7 < C, xl);
+    lrn_ld<V>(db + (int64_t)(c + 5) * HW, c + 5 >= 0 && c + 5 < C, dl);
+    const bool emit = c >= c0;
+    if (relu_x && emit) Vec<V>::ld(relu_x + base + (int64_t)c * HW, rx);
+    const bool live = c + 2 >= 0 && c + 2 < C;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      float pe = 0.f, re = 0.f;
+      if (live) {
+        const float s = lrn_scale5<V>(xq, v, a_n, kk);
+        pe = lrn_pow(s, -beta);
+        const float ye = __fmul_rn(xq[2][v], pe);
+        re = lrn_div(__fmul_rn(dq[2][v], ye), s);
+      }
+      r[0][v] = r[1][v]; r[1][v] = r[2][v]; r[2][v] = r[3][v]; r[3][v] = r[4][v]; r[4][v] = re;
+      pq[0][v] = pq[1][v]; pq[1][v] = pq[2][v]; pq[2][v] = pe;
+    }
+    if (emit) {
+      float out[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        float acc = 0.f;
+        acc = __fadd_rn(acc, r[0][v]);
+        acc = __fadd_rn(acc, r[1][v]);
+        acc = __fadd_rn(acc, r[2][v]);
+        acc = __fadd_rn(acc, r[3][v]);
+        acc = __fadd_rn(acc, r[4][v]);
+        const float a = __fmul_rn(dq[0][v], pq[0][v]);
+        const float b = __fmul_rn(__fmul_rn(coef, xq[0][v]), acc);
+        out[v] = __fsub_rn(a, b);
+        if (relu_x) out[v] = rx[v] > 0.f ? out[v] : 0.f;
+      }
+      Vec<V>::st(dx + base + (int64_t)c * HW, out);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      xq[0][v] = xq[1][v]; xq[1][v] = xq[2][v]; xq[2][v] = xq[3][v]; xq[3][v] = xq[4][v];
+      xq[4][v] = xn[0][v]; xn[0][v] = xn[1][v]; xn[1][v] = xl[v];
+      dq[0][v] = dq[1][v]; dq[1][v] = dq[2][v]; dq[2][v] = dn[0][v];
+      dn[0][v] = dn[1][v]; dn[1][v] = dl[v];
     }
   }
 }
@@ -847,6 +959,38 @@ __global__ void column_sum_kernel(const float* __restrict__ dy, float* __restric
 }  // namespace bf
 
 using namespace bf;
+
+// vector width for the graph-plan LRN kernels: LRN_RC_VEC when the plane size
+// and every pointer allow it, else scalar
+static int lrn_vec(int HW, std::initializer_list<const void*> ptrs) {
+  int v = LRN_RC_VEC;
+  while (v > 1) {
+    bool ok = HW % v == 0;
+    for (const void* p : ptrs) ok = ok && ((uintptr_t)p % (4u * v)) == 0;
+    if (ok) break;
+    v /= 2;
+  }
+  return v;
+}
+
+template <int V>
+static void lrn5_fwd_launch(const float* x, float* y, float* scale, int N, int C, int HW,
+                            float a_n, float beta, float k, cudaStream_t st) {
+  const int64_t px = (int64_t)N * HW / V;
+  const int ch = lrn_chunk(px, C);
+  lrn5_fwd_pf_kernel<V><<<dim3((unsigned)((px + 255) / 256), (C + ch - 1) / ch), 256, 0, st>>>(
+      x, y, scale, N, C, HW, a_n, beta, k, ch);
+}
+
+template <int V>
+static void lrn5_bwd_rc_launch(const float* x, const float* dy, float* dx, const float* relu_x,
+                               int N, int C, int HW, float a_n, float k, float coef, float beta,
+                               cudaStream_t st) {
+  const int64_t px = (int64_t)N * HW / V;
+  const int ch = lrn_chunk(px, C);
+  lrn5_bwd_rc_kernel<V><<<dim3((unsigned)((px + 255) / 256), (C + ch - 1) / ch), 256, 0, st>>>(
+      x, dy, dx, N, C, HW, a_n, k, coef, beta, ch, relu_x);
+}
 
 extern "C" {
 
@@ -979,28 +1123,41 @@ int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P
 int bf_lrn_fwd(const float* x, float* y, float* scale, int N, int C, int H, int W, int size,
                float alpha, float beta, float k, bf_stream_t s) {
   BF_REQUIRE(size >= 1, "lrn_forward: size must be >= 1");
+  BF_REQUIRE(scale || size == 5, "lrn_forward: scale may be omitted only for size 5");
   int64_t total = (int64_t)N * C * H * W;
   if (total <= 0) return 0;
   int pre = (size - 1) / 2, post = size - 1 - pre;
   float a_n = alpha / (float)size;
   if (size == 5) {
-    int64_t px = (int64_t)N * H * W;
-    if (LRN_VEC == 4 && (H * W) % 4 == 0 && ((uintptr_t)x & 15) == 0 &&
-        ((uintptr_t)y & 15) == 0 && ((uintptr_t)scale & 15) == 0)
-    {
-      const int ch = lrn_chunk(px / 4, C);
-      lrn5_fwd_kernel<4><<<dim3((unsigned)((px / 4 + 255) / 256), (C + ch - 1) / ch), 256, 0,
-                           as_stream(s)>>>(x, y, scale, N, C, H * W, a_n, beta, k, ch);
-    } else {
-      const int ch = lrn_chunk(px, C);
-      lrn5_fwd_kernel<1><<<dim3((unsigned)((px + 255) / 256), (C + ch - 1) / ch), 256, 0,
-                           as_stream(s)>>>(x, y, scale, N, C, H * W, a_n, beta, k, ch);
+    const int HW = H * W;
+    switch (lrn_vec(HW, {x, y, scale})) {
+      case 4: lrn5_fwd_launch<4>(x, y, scale, N, C, HW, a_n, beta, k, as_stream(s)); break;
+      case 2: lrn5_fwd_launch<2>(x, y, scale, N, C, HW, a_n, beta, k, as_stream(s)); break;
+      default: lrn5_fwd_launch<1>(x, y, scale, N, C, HW, a_n, beta, k, as_stream(s)); break;
     }
     return check_launch("lrn_forward");
   }
   lrn_fwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
       x, y, scale, total, C, H * W, pre, post, a_n, beta, k);
   return check_launch("lrn_forward");
+}
+
+int bf_lrn_bwd_recompute(const float* x, const float* dy, float* dx, const float* relu_x, int N,
+                         int C, int H, int W, int size, float alpha, float beta, float k,
+                         bf_stream_t s) {
+  BF_REQUIRE(size == 5, "lrn_backward (recompute): size must be 5");
+  if ((int64_t)N * C * H * W <= 0) return 0;
+  const float a_n = alpha / (float)size;
+  float coef = 2.0f * alpha;
+  coef = coef * beta;
+  coef = coef / (float)size;
+  const int HW = H * W;
+  switch (lrn_vec(HW, {x, dy, dx, relu_x})) {
+    case 4: lrn5_bwd_rc_launch<4>(x, dy, dx, relu_x, N, C, HW, a_n, k, coef, beta, as_stream(s)); break;
+    case 2: lrn5_bwd_rc_launch<2>(x, dy, dx, relu_x, N, C, HW, a_n, k, coef, beta, as_stream(s)); break;
+    default: lrn5_bwd_rc_launch<1>(x, dy, dx, relu_x, N, C, HW, a_n, k, coef, beta, as_stream(s)); break;
+  }
+  return check_launch("lrn_backward");
 }
 
 int bf_lrn_bwd(const float* x, const float* y, const float* scale, const float* dy, float* dx,

@@ -438,6 +438,25 @@ class _Plan:
             self.fused_away.add(oid)
             self.elided.add(graph.tensors[g].name)
 
+        # LRN scale elision: when an lrn_forward's scale feeds only lrn_backward
+        # operators of the same (x, y) and attributes, the backward recomputes
+        # scale and y from x (the forward's exact operation sequence, so
+        # bit-identical) and the forward never stores scale
+        for oid, op in graph.operators.items():
+            if op.kind != "lrn_forward" or len(op.outputs) != 2 or op.attrs.get("size", 5) != 5:
+                continue
+            sc = op.outputs[1]
+            cons = graph.consumers_of(sc)
+            if not cons or any(
+                    graph.operators[c].kind != "lrn_backward" or
+                    tuple(graph.operators[c].inputs[:3]) != (op.inputs[0], op.outputs[0], sc) or
+                    graph.operators[c].attrs != op.attrs for c, _ in cons):
+                continue
+            self.fusion.setdefault(oid, {})["lrn_no_scale"] = True
+            for c, _ in cons:
+                self.fusion.setdefault(c, {})["lrn_recompute"] = True
+            self.elided.add(graph.tensors[sc].name)
+
     def _split_branches(self, graph: BiGraph, branches: int) -> None:
         """Event-driven device concurrency inside a lane: the lane's operators
         are spread over up to ``branches`` CUDA streams by greedy chain

@@ -361,15 +361,29 @@ def _avgpool_bwd(ctx, op):
 
 def _lrn_fwd(ctx, op):
     (x,) = _ins(ctx, op)
-    y, scale = _outs(ctx, op)
+    g = ctx.graph
     size, alpha, beta, k = lrn_attrs(op.attrs)
+    fused = getattr(ctx, "fused", None)
+    y = ctx.store.ensure(g.tensors[op.outputs[0]].name, g.tensors[op.outputs[0]].shape)
+    if fused and fused.get("lrn_no_scale"):  # scale elided: the backward recomputes it
+        _L()("bf_lrn_fwd", x.ptr, y.ptr, None, *x.shape, size, alpha, beta, k, ctx.stream)
+        return
+    scale = ctx.store.ensure(g.tensors[op.outputs[1]].name, g.tensors[op.outputs[1]].shape)
     _L()("bf_lrn_fwd", x.ptr, y.ptr, scale.ptr, *x.shape, size, alpha, beta, k, ctx.stream)
 
 
 def _lrn_bwd(ctx, op):
-    x, y, scale, dy = _ins(ctx, op)
     size, alpha, beta, k = lrn_attrs(op.attrs)
     rx, rdx = _relu_fold(ctx, op)
+    fused = getattr(ctx, "fused", None)
+    if fused and fused.get("lrn_recompute"):  # x, dy only (scale, y recomputed)
+        names = _names(ctx, op.inputs)
+        x, dy = ctx.store.get(names[0]), ctx.store.get(names[3])
+        dx = rdx if rx is not None else _outs(ctx, op)[0]
+        _L()("bf_lrn_bwd_recompute", x.ptr, dy.ptr, dx.ptr, rx.ptr if rx is not None else None,
+             *x.shape, size, alpha, beta, k, ctx.stream)
+        return
+    x, y, scale, dy = _ins(ctx, op)
     if rx is not None:
         _L()("bf_lrn_bwd_relu", x.ptr, y.ptr, scale.ptr, dy.ptr, rdx.ptr, rx.ptr, *x.shape, size,
              alpha, beta, k, ctx.stream)

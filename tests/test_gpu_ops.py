@@ -203,6 +203,45 @@ def test_lrn(shape):
     assert_close(dx, O.lrn_backward(x, y, sc, dy), rtol=1e-5, atol=1e-6, what="lrn dx")
 
 
+@pytest.mark.parametrize("shape", [(2, 64, 56, 56), (2, 7, 5, 5), (1, 2, 4, 4), (3, 4, 2, 2),
+                                   (1, 40, 6, 6), (2, 37, 3, 5), (2, 192, 14, 14)])
+@pytest.mark.parametrize("relu", [False, True])
+def test_lrn_recompute_backward_bitwise(shape, relu):
+    """Graph-plan LRN pair (scale elided): the forward without scale stores the
+    same y, and the backward recomputing scale and y from x is bit-identical to
+    the explicit backward fed the forward's outputs (with and without the
+    folded ReLU mask); both within tolerance of the oracle."""
+    import torch
+    from paper_1412_6249_b200 import _native
+
+    lib = _native.lib()
+    dev = torch.device("cuda:0")
+    x = torch.from_numpy(rnd(*shape, scale=3.0)).to(dev)
+    dy = torch.from_numpy(rnd(*shape)).to(dev)
+    rx = torch.from_numpy(rnd(*shape)).to(dev) if relu else None
+    y, sc, y2 = (torch.empty_like(x) for _ in range(3))
+    a = (5, 1e-4, 0.75, 1.0)
+    lib("bf_lrn_fwd", x.data_ptr(), y.data_ptr(), sc.data_ptr(), *shape, *a, None)
+    lib("bf_lrn_fwd", x.data_ptr(), y2.data_ptr(), None, *shape, *a, None)
+    dx, dx2 = torch.empty_like(x), torch.empty_like(x)
+    if relu:
+        lib("bf_lrn_bwd_relu", x.data_ptr(), y.data_ptr(), sc.data_ptr(), dy.data_ptr(),
+            dx.data_ptr(), rx.data_ptr(), *shape, *a, None)
+    else:
+        lib("bf_lrn_bwd", x.data_ptr(), y.data_ptr(), sc.data_ptr(), dy.data_ptr(), dx.data_ptr(),
+            *shape, *a, None)
+    lib("bf_lrn_bwd_recompute", x.data_ptr(), dy.data_ptr(), dx2.data_ptr(),
+        rx.data_ptr() if relu else None, *shape, *a, None)
+    torch.cuda.synchronize()
+    assert_bitwise(y2.cpu().numpy(), y.cpu().numpy(), "lrn y without scale")
+    assert_bitwise(dx2.cpu().numpy(), dx.cpu().numpy(), "lrn recompute dx")
+    xn, dyn = x.cpu().numpy(), dy.cpu().numpy()
+    want = O.lrn_backward(xn, y.cpu().numpy(), sc.cpu().numpy(), dyn)
+    if relu:
+        want = O.relu_backward(rx.cpu().numpy(), want)
+    assert_close(dx2.cpu().numpy(), want, rtol=1e-5, atol=1e-6, what="lrn recompute vs oracle")
+
+
 def test_concat_bitwise():
     parts = {f"p{i}": rnd(2, c, 7, 7) for i, c in enumerate((64, 128, 32, 32))}
     y = O.concat_forward(list(parts.values()))

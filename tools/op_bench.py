@@ -1,6 +1,6 @@
 """Time one memory-bound kernel family at GoogLeNet shapes (batch 128).
 
-    python tools/op_bench.py maxpool_fwd|maxpool_bwd|lrn_fwd|relu_fwd [--reps 5]
+    python tools/op_bench.py maxpool_fwd|maxpool_bwd|lrn_fwd|lrn_fwd_noscale|lrn_bwd|lrn_bwd_rc [--reps 5]
 
 Prints per-shape time and achieved GB/s (algorithmic bytes).
 """
@@ -56,6 +56,14 @@ def main():
             if a.op == "lrn_fwd":
                 fn = lambda: lib("bf_lrn_fwd", x.data_ptr(), yy.data_ptr(), sc.data_ptr(), n, c, h, w,
                                  5, 1e-4, 0.75, 1.0, st)
+                nbytes = 12 * x.numel()
+            elif a.op == "lrn_fwd_noscale":
+                fn = lambda: lib("bf_lrn_fwd", x.data_ptr(), yy.data_ptr(), None, n, c, h, w,
+                                 5, 1e-4, 0.75, 1.0, st)
+                nbytes = 8 * x.numel()
+            elif a.op == "lrn_bwd_rc":
+                fn = lambda: lib("bf_lrn_bwd_recompute", x.data_ptr(), sc.data_ptr(), dx.data_ptr(),
+                                 None, n, c, h, w, 5, 1e-4, 0.75, 1.0, st)
                 nbytes = 12 * x.numel()
             else:
                 lib("bf_lrn_fwd", x.data_ptr(), yy.data_ptr(), sc.data_ptr(), n, c, h, w, 5, 1e-4,
