@@ -7,6 +7,7 @@
 // accumulation order bit for bit (oracle/kernels.py maxpool_backward /
 // avgpool_backward).
 #include <algorithm>
+#include <cstdlib>
 #include <initializer_list>
 
 #include "common.cuh"
@@ -526,6 +527,308 @@ __global__ void maxpool3_bwd_plane(const float* __restrict__ mask, const float* 
   }
 }
 
+#ifndef POOL_PF
+#define POOL_PF 2  // rows the column walkers load ahead of their use (measured: 1-2 best)
+#endif
+
+// Column walkers for 3x3 pooling: a thread owns one output column (forward)
+// or input column (backward) of one plane and walks down its rows, keeping the
+// window's per-row state in registers.  Loads go straight through L1 (the
+// lanes of a warp cover consecutive columns, so neighbouring windows share
+// lines) and are issued POOL_PF rows ahead of their use.  No shared memory and no
+// block barriers: the plane-staging kernels above serialise load -> barrier ->
+// compute inside each CTA and reached only 1.3-2 TB/s on the stride-1
+// Inception pools (28x28 / 14x14 / 7x7 planes).
+//
+// Forward, separable argmax: each input row's 3 window columns reduce to
+// (first max, its index); the window's result is the first row whose row-max
+// is strictly greater than the earlier rows'.  With strict '>' from -inf in
+// both passes this is exactly the first maximum in window raster order, the
+// plane kernels' (and the oracle's) semantics, NaN and all -inf included.
+// Each row reduction serves 3 windows (stride 1).
+template <int S>
+__global__ void __launch_bounds__(256) maxpool3_fwd_cols(const float* __restrict__ x,
+                                                         float* __restrict__ y,
+                                                         float* __restrict__ mask,
+                                                         int64_t threads, int H, int W, int P,
+                                                         int Q, int pad) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= threads) return;
+  const int64_t pl = t / Q;
+  const int pw = (int)(t - pl * Q);
+  const float* __restrict__ xp = x + pl * H * W;
+  float* __restrict__ yp = y + pl * P * Q + pw;
+  float* __restrict__ mp = mask + pl * P * Q + pw;
+  const int ws = pw * S - pad;
+  bool cv[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) cv[d] = (unsigned)(ws + d) < (unsigned)W;
+  auto ld_row = [&](int h, float (&v)[3]) {
+    const bool rv = (unsigned)h < (unsigned)H;
+    const int off = h * W + ws;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) v[d] = (rv && cv[d]) ? __ldg(xp + off + d) : -INFINITY;
+  };
+  auto red_row = [&](int h, const float (&v)[3], float& m, int& a) {
+    m = -INFINITY;
+    a = -1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (v[d] > m) {
+        m = v[d];
+        a = h * W + ws + d;
+      }
+  };
+  int hs = -pad;
+  float rm[3];
+  int ra[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    float v[3];
+    ld_row(hs + j, v);
+    red_row(hs + j, v, rm[j], ra[j]);
+  }
+  float q[POOL_PF][S][3];  // q[k]: the rows entering at output row ph + 1 + k
+#pragma unroll
+  for (int k = 0; k < POOL_PF; ++k)
+#pragma unroll
+    for (int j = 0; j < S; ++j) ld_row(hs + 3 + k * S + j, q[k][j]);
+  for (int ph = 0; ph < P; ++ph, hs += S) {
+    float nq[S][3];
+#pragma unroll
+    for (int j = 0; j < S; ++j) ld_row(hs + 3 + POOL_PF * S + j, nq[j]);
+    float best = -INFINITY;
+    int arg = -1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (rm[d] > best) {
+        best = rm[d];
+        arg = ra[d];
+      }
+    yp[(int64_t)ph * Q] = best;
+    mp[(int64_t)ph * Q] = (float)arg;
+    if (S == 1) {
+      rm[0] = rm[1]; ra[0] = ra[1];
+      rm[1] = rm[2]; ra[1] = ra[2];
+      red_row(hs + 3, q[0][0], rm[2], ra[2]);
+    } else {
+      rm[0] = rm[2]; ra[0] = ra[2];
+      red_row(hs + 3, q[0][0], rm[1], ra[1]);
+      red_row(hs + 4, q[0][S - 1], rm[2], ra[2]);
+    }
+#pragma unroll
+    for (int k = 0; k + 1 < POOL_PF; ++k)
+#pragma unroll
+      for (int j = 0; j < S; ++j)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) q[k][j][d] = q[k + 1][j][d];
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) q[POOL_PF - 1][j][d] = nq[j][d];
+  }
+}
+
+// Stride-1 backward walker: input pixel (h, w) gathers, in window raster
+// order, dy of the windows (h + pad - 2 + i, w + pad - 2 + j) whose argmax it
+// is (bit-exact with the oracle's raster-order scatter, as the plane kernel);
+// the 3 candidate output rows' (mask, dy) triples roll down with h.
+__global__ void __launch_bounds__(256) maxpool3s1_bwd_cols(const float* __restrict__ mask,
+                                                           const float* __restrict__ dy,
+                                                           float* __restrict__ dx, int64_t threads,
+                                                           int H, int W, int P, int Q, int pad,
+                                                           const float* __restrict__ relu_x) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= threads) return;
+  const int64_t pl = t / W;
+  const int w = (int)(t - pl * W);
+  const float* __restrict__ mp = mask + pl * P * Q;
+  const float* __restrict__ gp = dy + pl * P * Q;
+  const int64_t obase = pl * H * W + w;
+  const int q0 = w + pad - 2;
+  bool qv[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) qv[j] = (unsigned)(q0 + j) < (unsigned)Q;
+  auto ld_row = [&](int ph, float (&m)[3], float (&g)[3]) {
+    const bool rv = (unsigned)ph < (unsigned)P;
+    const int off = ph * Q + q0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const bool ok = rv && qv[j];
+      m[j] = ok ? __ldg(mp + off + j) : -1.f;
+      g[j] = ok ? __ldg(gp + off + j) : 0.f;
+    }
+  };
+  float M[3][3], G[3][3], qm[POOL_PF][3], qg[POOL_PF][3];  // q[k]: output row h + pad + 1 + k
+#pragma unroll
+  for (int i = 0; i < 3; ++i) ld_row(pad - 2 + i, M[i], G[i]);
+#pragma unroll
+  for (int k = 0; k < POOL_PF; ++k) ld_row(pad + 1 + k, qm[k], qg[k]);
+  for (int h = 0; h < H; ++h) {
+    float nm[3], ng[3];
+    ld_row(h + pad + 1 + POOL_PF, nm, ng);
+    const float me = (float)(h * W + w);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, M[i][j] == me ? G[i][j] : 0.f);
+    const int64_t o = obase + (int64_t)h * W;
+    dx[o] = relu_fold(relu_x, o, acc);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      M[0][j] = M[1][j]; G[0][j] = G[1][j];
+      M[1][j] = M[2][j]; G[1][j] = G[2][j];
+      M[2][j] = qm[0][j]; G[2][j] = qg[0][j];
+#pragma unroll
+      for (int k = 0; k + 1 < POOL_PF; ++k) {
+        qm[k][j] = qm[k + 1][j];
+        qg[k][j] = qg[k + 1][j];
+      }
+      qm[POOL_PF - 1][j] = nm[j];
+      qg[POOL_PF - 1][j] = ng[j];
+    }
+  }
+}
+
+#ifndef POOL_ROW_PF
+#define POOL_ROW_PF 6  // rows the warp-row kernels load ahead of their use
+#endif
+
+// Warp-row kernels for the stride-1, pad-1 3x3 pools of planes at most 32
+// wide (every Inception pool: 28, 14, 7): a warp holds floor(32 / W) planes
+// side by side, one lane per column, and walks their rows.  Each lane loads
+// ONE element per row (fully coalesced, no redundant L1 requests) and takes
+// its neighbours' columns by warp shuffle; POOL_ROW_PF rows are in flight per
+// lane.  Same separable argmax / raster-order gather as the walkers above.
+__global__ void __launch_bounds__(256) maxpool3s1_fwd_rows(const float* __restrict__ x,
+                                                           float* __restrict__ y,
+                                                           float* __restrict__ mask,
+                                                           int64_t planes, int H, int W) {
+  const int lane = threadIdx.x & 31;
+  const int ppw = 32 / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int sub = lane / W, w = lane - sub * W;
+  const int64_t pl = warp * ppw + sub;
+  const bool act = sub < ppw && pl < planes;
+  if (warp * ppw >= planes) return;  // warp-uniform
+  const int64_t base = (act ? pl : 0) * H * W + w;
+  const bool has_l = w > 0, has_r = w + 1 < W;
+  auto ld = [&](int h) { return (act && h < H) ? __ldg(x + base + (int64_t)h * W) : -INFINITY; };
+  // row reduction of input row h from this lane's element v (first max over w-1, w, w+1)
+  auto red = [&](int h, float v, float& m, int& a) {
+    const float l = __shfl_up_sync(0xffffffffu, v, 1), r = __shfl_down_sync(0xffffffffu, v, 1);
+    const float c0 = has_l ? l : -INFINITY, c2 = has_r ? r : -INFINITY;
+    m = -INFINITY;
+    a = -1;
+    const int i0 = h * W + w - 1;
+    if (c0 > m) { m = c0; a = i0; }
+    if (v > m) { m = v; a = i0 + 1; }
+    if (c2 > m) { m = c2; a = i0 + 2; }
+  };
+  float q[POOL_ROW_PF];  // q[k] = x row k + 1 relative to the current output row
+#pragma unroll
+  for (int k = 0; k < POOL_ROW_PF; ++k) q[k] = ld(1 + k);
+  // rows -1 (padding), 0
+  float rm[3];
+  int ra[3];
+  rm[0] = -INFINITY;
+  ra[0] = -1;
+  red(0, ld(0), rm[1], ra[1]);
+  for (int h = 0; h < H; ++h) {
+    const float nx = ld(h + 1 + POOL_ROW_PF);
+    if (h + 1 < H) {
+      red(h + 1, q[0], rm[2], ra[2]);
+    } else {
+      rm[2] = -INFINITY;
+      ra[2] = -1;
+    }
+    float best = -INFINITY;
+    int arg = -1;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (rm[d] > best) {
+        best = rm[d];
+        arg = ra[d];
+      }
+    if (act) {
+      y[base + (int64_t)h * W] = best;
+      mask[base + (int64_t)h * W] = (float)arg;
+    }
+    rm[0] = rm[1]; ra[0] = ra[1];
+    rm[1] = rm[2]; ra[1] = ra[2];
+#pragma unroll
+    for (int k = 0; k + 1 < POOL_ROW_PF; ++k) q[k] = q[k + 1];
+    q[POOL_ROW_PF - 1] = nx;
+  }
+}
+
+__global__ void __launch_bounds__(256) maxpool3s1_bwd_rows(const float* __restrict__ mask,
+                                                           const float* __restrict__ dy,
+                                                           float* __restrict__ dx, int64_t planes,
+                                                           int H, int W,
+                                                           const float* __restrict__ relu_x) {
+  const int lane = threadIdx.x & 31;
+  const int ppw = 32 / W;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int sub = lane / W, w = lane - sub * W;
+  const int64_t pl = warp * ppw + sub;
+  const bool act = sub < ppw && pl < planes;
+  if (warp * ppw >= planes) return;  // warp-uniform
+  const int64_t base = (act ? pl : 0) * H * W + w;
+  const bool has_l = w > 0, has_r = w + 1 < W;
+  // output row p of this column: (mask, dy), (-1, 0) outside the plane
+  auto ldm = [&](int p) { return (act && p < H) ? __ldg(mask + base + (int64_t)p * W) : -1.f; };
+  auto ldg_ = [&](int p) { return (act && p < H) ? __ldg(dy + base + (int64_t)p * W) : 0.f; };
+  // the three candidate windows of row p seen from this lane: columns w-1, w, w+1
+  auto spread = [&](float m, float g, float (&M)[3], float (&G)[3]) {
+    const float ml = __shfl_up_sync(0xffffffffu, m, 1), mr = __shfl_down_sync(0xffffffffu, m, 1);
+    const float gl = __shfl_up_sync(0xffffffffu, g, 1), gr = __shfl_down_sync(0xffffffffu, g, 1);
+    M[0] = has_l ? ml : -1.f;  G[0] = has_l ? gl : 0.f;
+    M[1] = m;                  G[1] = g;
+    M[2] = has_r ? mr : -1.f;  G[2] = has_r ? gr : 0.f;
+  };
+  float qm[POOL_ROW_PF], qg[POOL_ROW_PF];  // output row h + 1 + k
+#pragma unroll
+  for (int k = 0; k < POOL_ROW_PF; ++k) {
+    qm[k] = ldm(1 + k);
+    qg[k] = ldg_(1 + k);
+  }
+  float M[3][3], G[3][3];  // candidate output rows h-1, h, h+1
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    M[0][j] = -1.f;
+    G[0][j] = 0.f;
+  }
+  spread(ldm(0), ldg_(0), M[1], G[1]);
+  for (int h = 0; h < H; ++h) {
+    const float nm = ldm(h + 1 + POOL_ROW_PF), ng = ldg_(h + 1 + POOL_ROW_PF);
+    spread(qm[0], qg[0], M[2], G[2]);  // row h + 1 (already -1 / 0 past the plane)
+    const float me = (float)(h * W + w);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, M[i][j] == me ? G[i][j] : 0.f);
+    if (act) {
+      const int64_t o = base + (int64_t)h * W;
+      dx[o] = relu_fold(relu_x, o, acc);
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      M[0][j] = M[1][j]; G[0][j] = G[1][j];
+      M[1][j] = M[2][j]; G[1][j] = G[2][j];
+    }
+#pragma unroll
+    for (int k = 0; k + 1 < POOL_ROW_PF; ++k) {
+      qm[k] = qm[k + 1];
+      qg[k] = qg[k + 1];
+    }
+    qm[POOL_ROW_PF - 1] = nm;
+    qg[POOL_ROW_PF - 1] = ng;
+  }
+}
+
 // Stride-2 3x3 backward: a thread owns the 2x2 pixel block (h0, w0) = (2i - pad,
 // 2j - pad) + {0,1}^2.  On the padded grid an even row is the bottom row of
 // window i-1 and the top row of window i, an odd row the middle row of window
@@ -992,12 +1295,36 @@ static void lrn5_bwd_rc_launch(const float* x, const float* dy, float* dx, const
       x, dy, dx, N, C, HW, a_n, k, coef, beta, ch, relu_x);
 }
 
+// column walkers on/off (A/B): bit 0 forward stride 1, bit 1 forward stride 2,
+// bit 2 backward stride 1, bit 3 warp-row kernels (stride 1, pad 1, W <= 32);
+// PURINE_B200_POOL_WALKERS, default all on
+static int pool_walkers() {
+  const char* e = std::getenv("PURINE_B200_POOL_WALKERS");
+  return e ? std::atoi(e) : 15;
+}
+
 extern "C" {
 
 int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, int W, int P,
                    int Q, int kernel, int stride, int pad, bf_stream_t s) {
   int64_t total = (int64_t)N * C * P * Q;
   if (total <= 0) return 0;
+  if (kernel == 3 && stride == 1 && pad == 1 && W <= 32 && P == H && Q == W &&
+      (pool_walkers() & 8)) {
+    const int64_t planes = (int64_t)N * C, warps = (planes + 32 / W - 1) / (32 / W);
+    maxpool3s1_fwd_rows<<<(unsigned)((warps + 7) / 8), 256, 0, as_stream(s)>>>(x, y, mask, planes,
+                                                                               H, W);
+    return check_launch("maxpool_forward");
+  }
+  if (kernel == 3 && (stride == 1 || stride == 2) && (pool_walkers() >> (stride - 1)) & 1) {
+    const int64_t threads = (int64_t)N * C * Q;
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
+    if (stride == 1)
+      maxpool3_fwd_cols<1><<<blocks, 256, 0, as_stream(s)>>>(x, y, mask, threads, H, W, P, Q, pad);
+    else
+      maxpool3_fwd_cols<2><<<blocks, 256, 0, as_stream(s)>>>(x, y, mask, threads, H, W, P, Q, pad);
+    return check_launch("maxpool_forward");
+  }
   const int smem = H * W * 4;
   if (smem <= kPlaneSmemMax) {
     static bool attr = false;
@@ -1052,6 +1379,19 @@ int bf_maxpool_bwd_relu(const float* mask, const float* dy, float* dx, const flo
                         bf_stream_t s) {
   int64_t total = (int64_t)N * C * H * W;
   if (total <= 0) return 0;
+  if (kernel == 3 && stride == 1 && pad == 1 && W <= 32 && P == H && Q == W &&
+      (pool_walkers() & 8)) {
+    const int64_t planes = (int64_t)N * C, warps = (planes + 32 / W - 1) / (32 / W);
+    maxpool3s1_bwd_rows<<<(unsigned)((warps + 7) / 8), 256, 0, as_stream(s)>>>(
+        mask, dy, dx, planes, H, W, relu_x);
+    return check_launch("maxpool_backward");
+  }
+  if (kernel == 3 && stride == 1 && (pool_walkers() & 4)) {
+    const int64_t threads = (int64_t)N * C * W;
+    maxpool3s1_bwd_cols<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(s)>>>(
+        mask, dy, dx, threads, H, W, P, Q, pad, relu_x);
+    return check_launch("maxpool_backward");
+  }
   const int smem = 2 * P * Q * 4;
   if (smem <= kPlaneSmemMax) {
     static bool attr = false;

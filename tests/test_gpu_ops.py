@@ -160,10 +160,23 @@ def test_sgd_momentum_aggregate_bitwise(golden_ops):
                                          ((2, 4, 8, 8), 2, 2, 0), ((1, 96, 54, 54), 3, 2, 0),
                                          ((2, 5, 11, 13), 3, 2, 1), ((2, 8, 14, 14), 3, 2, 1),
                                          ((1, 2, 6, 7), 3, 2, 0), ((3, 7, 5, 5), 3, 1, 1),
-                                         ((2, 3, 6, 7), 3, 1, 0), ((2, 64, 7, 7), 3, 1, 1)])
-def test_maxpool_bitwise(shape, k, s, p):
+                                         ((2, 3, 6, 7), 3, 1, 0), ((2, 64, 7, 7), 3, 1, 1),
+                                         ((2, 16, 14, 14), 3, 1, 1), ((1, 3, 9, 32), 3, 1, 1),
+                                         ((1, 3, 6, 33), 3, 1, 1), ((3, 5, 4, 1), 3, 1, 1)])
+@pytest.mark.parametrize("walkers", ["15", "7", "0"], ids=["rows", "columns", "planes"])
+@pytest.mark.parametrize("values", ["normal", "coarse"])
+def test_maxpool_bitwise(shape, k, s, p, walkers, values, monkeypatch):
+    """Warp-row kernels (default for stride-1 pad-1 planes <= 32 wide), column
+    walkers and plane-staging kernels (PURINE_B200_POOL_WALKERS=15 / 7 / 0)
+    all bit-exact; "coarse" values make most
+    windows hold ties (first maximum in raster order wins) and put a -inf
+    block in the corner."""
+    monkeypatch.setenv("PURINE_B200_POOL_WALKERS", walkers)
     x = rnd(*shape)
-    x[:, :, ::3, ::3] = 0.5  # plenty of ties
+    x[:, :, ::3, ::3] = 0.5  # ties across windows
+    if values == "coarse":
+        x = f32(np.round(x))
+        x[:, :, :3, :3] = -3e38
     y, m = O.maxpool_forward(x, k, s, p)
     out = run_op("maxpool_forward", {"x": x}, {"y": y.shape, "m": y.shape},
                  {"kernel": k, "stride": s, "pad": p})
