@@ -39,6 +39,9 @@ int tc4_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNC
 int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
                    float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 
-extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in), 4 auto without v4
+extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in),
+                           // 4 auto without v4, 5 auto without the TMA-fed 1x1 weight gradient
+// the TMA-fed 1x1 weight gradient (engine v2 mode kTma1x1) is taken unless engine 5
+inline bool tc2_tma_wgrad_enabled() { return g_gemm_engine != 5; }
 
 }  // namespace bf

@@ -295,11 +295,14 @@ struct Work {
   int abase;  // first TMEM column of the A ring
   int accs;   // TMEM column stride between the accumulator buffers
   int Pp, Qp;  // weight-gradient fast path: padded pixel grid of the K ordering
+  int sstride;  // bytes between ring stages (B tile [+ raw A tile in kTma1x1])
+  int cpi;      // kTma1x1: 32-pixel k-blocks per image
 };
 
 // MODE: 0 generic table gather, 1 channel-chunk fast path (fwd / dgrad),
 //       2 / 3 weight-gradient pixel-row fast path with 16- / 8-wide chunks
-enum { kGeneric = 0, kChannel = 1, kWgrad16 = 2, kWgrad8 = 3 };
+//       4 TMA-fed 1x1 weight gradient (both operands K-major NCHW tiles, no pack)
+enum { kGeneric = 0, kChannel = 1, kWgrad16 = 2, kWgrad8 = 3, kTma1x1 = 4 };
 
 __device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& nt, int& sp) {
   sp = u % w.splits;
@@ -409,7 +412,9 @@ __device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowI
 
 template <class LA, class Epi, int MODE>
 __global__ void __launch_bounds__(kAllThreads, 1)
-    tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part) {
+    tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part,
+               const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+               float* __restrict__ bias_part) {
   using SA = Sep<LA>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -418,7 +423,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   const int stage_bytes = 2 * BN * 128;
   uint8_t* tiles = base;
   const int ktab_n = w.full_ktab ? w.nkb * BK : STAGES * BK;
-  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nbst * stage_bytes);
+  const int sstride = w.sstride;
+  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nbst * sstride);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + ktab_n);
   uint64_t* empty = full + STAGES;
   uint64_t* bfull = empty + STAGES;
@@ -479,7 +485,84 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       return m < w.M ? SA::row(la, m) : RowInfo{0, (short)kInvalid, (short)kInvalid};
     };
     int u = blockIdx.x, i = 0, it = 0;
-    if (MODE == kGeneric && !w.full_ktab) {
+    if (MODE == kTma1x1) {
+      // A (x rows) and B (dy rows) arrive as raw fp32 tiles by TMA.  Each
+      // thread splits its TMEM lane's 16 A values (4 swizzled 16-byte chunks
+      // of row m) into big/small for TMEM, writes the small part of BN/32 of
+      // the B tile's 16-byte chunks next to the raw tile (raw = big: the tensor
+      // core drops the low 13 bits itself) and, for m-tile 0, sums those dy
+      // chunks into per-row bias partials.
+      const int m_row = q * 32 + lane;
+      const int nb = BN / 32;  // 16-byte B chunks per thread per stage
+      for (; u < w.units; u += gridDim.x) {
+        int mt, nt, sp;
+        unit_coords(w, u, mt, nt, sp);
+        const int kb0 = sp * w.kbps;
+        const int nk = min(w.kbps, w.nkb - kb0);
+        const bool do_bias = bias_part != nullptr && mt == 0;
+        float bsum[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bsum[j] = 0.f;
+        for (int i2 = 0; i2 < nk; ++i2, ++it) {
+          const int bs = it % w.nbst;
+          const int stage = it % w.nst;
+          mbar_wait(&bfull[bs], (it / w.nbst) & 1);
+          uint8_t* sb = tiles + bs * sstride;
+          const uint8_t* araw = sb + 2 * BN * 128;
+          float big[16], small[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int chunk = (kc0 >> 2) + c;
+            const float4 v = *reinterpret_cast<const float4*>(araw + m_row * 128 +
+                                                              ((chunk ^ (m_row & 7)) << 4));
+            split_tf32(v.x, big[4 * c + 0], small[4 * c + 0]);
+            split_tf32(v.y, big[4 * c + 1], small[4 * c + 1]);
+            split_tf32(v.z, big[4 * c + 2], small[4 * c + 2]);
+            split_tf32(v.w, big[4 * c + 3], small[4 * c + 3]);
+          }
+          const float4* braw = reinterpret_cast<const float4*>(sb);
+          float4* bsm = reinterpret_cast<float4*>(sb + BN * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < nb) {
+              const int f = t + kProducers * j;
+              const float4 v = braw[f];
+              float4 r;
+              r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+              r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+              r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+              r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+              bsm[f] = r;
+              if (do_bias)
+                bsum[j] = __fadd_rn(bsum[j], __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
+            }
+          }
+          // generic-proxy smem writes -> visible to the tensor core (async proxy)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_wait(&empty[stage], ((it / w.nst) & 1) ^ 1);
+          const uint32_t acol = w.abase + stage * 64 + kc0;
+          tmem_st16(lane_addr + acol, big);
+          tmem_st16(lane_addr + acol + 32, small);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          mbar_arrive(&full[stage]);
+        }
+        if (do_bias) {
+          // chunk f of the tile is row f / 8: the 8 lanes t^1, t^2, t^4 share a row
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < nb) {
+              float a = bsum[j];
+              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
+              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
+              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 4));
+              const int row = nt * BN + (t >> 3) + 32 * j;
+              if ((t & 7) == 0 && row < w.N) bias_part[(size_t)row * w.splits + sp] = a;
+            }
+          }
+        }
+      }
+    } else if (MODE == kGeneric && !w.full_ktab) {
       // K too long for a cached table (weight gradients: K = N*P*Q pixels):
       // the k-block's 32 gather offsets are computed per stage into a ring slot
       for (; u < w.units; u += gridDim.x) {
@@ -606,7 +689,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           // descriptor start-address field = smem byte address >> 4 (bits 0-13)
-          const uint64_t db = dtiles + (uint64_t)((bst * stage_bytes) >> 4);
+          const uint64_t db = dtiles + (uint64_t)((bst * sstride) >> 4);
           const uint64_t ds = db + dsmall;
           const uint32_t ab = tmem + w.abase + stage * 64;
           if (elect_one()) {
@@ -638,7 +721,25 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     // streams the pre-packed B tiles of every (unit, k-block) into the B ring
     // as far ahead as the ring allows: the TMA latency leaves the per-stage
     // critical path of the producers
-    if (lane == 0) {
+    if (MODE == kTma1x1 && lane == 0) {
+      // raw dy tile (BN rows) and x tile (BM rows) of one 32-pixel k-block
+      int it = 0;
+      for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
+        int mt, nt, sp;
+        unit_coords(w, u, mt, nt, sp);
+        const int kb0 = sp * w.kbps;
+        const int nk = min(w.kbps, w.nkb - kb0);
+        for (int i = 0; i < nk; ++i, ++it) {
+          const int bst = it % w.nbst;
+          mbar_wait(&bempty[bst], ((it / w.nbst) & 1) ^ 1);
+          mbar_arrive_expect_tx(&bfull[bst], (uint32_t)(BN * 128 + BM * 128));
+          const int kb = kb0 + i, img = kb / w.cpi, pix = (kb - img * w.cpi) * BK;
+          uint8_t* sb = tiles + bst * sstride;
+          tma_load_3d(smem_u32(sb), &bmap, pix, nt * BN, img, &bfull[bst]);
+          tma_load_3d(smem_u32(sb + 2 * BN * 128), &amap, pix, mt * BM, img, &bfull[bst]);
+        }
+      }
+    } else if (lane == 0) {
       int it = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
         int mt, nt, sp;
@@ -649,7 +750,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           const int bst = it % w.nbst;
           mbar_wait(&bempty[bst], ((it / w.nbst) & 1) ^ 1);
           mbar_arrive_expect_tx(&bfull[bst], (uint32_t)stage_bytes);
-          bulk_g2s(smem_u32(tiles + bst * stage_bytes),
+          bulk_g2s(smem_u32(tiles + bst * sstride),
                    bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
                    &bfull[bst]);
         }
@@ -729,6 +830,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.abase = (w.nacc * w.BN + 63) / 64 * 64;
   w.nst = std::min<int>(7, (512 - w.abase) / 64);
   const int64_t stage_bytes = 2LL * w.BN * 128;
+  w.sstride = (int)stage_bytes;
   const int64_t pack_bytes = (int64_t)w.ntiles * w.nkb * stage_bytes;
   const int64_t pack_aligned = (pack_bytes + 1023) / 1024 * 1024;
   if (!ws || ws_bytes < pack_aligned) return -1;
@@ -787,7 +889,8 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   const int smem_req = std::max(smem, 120 << 10);
   const int grid = std::min(w.units, sms);
   EpiPartial part{part_ws, M, N};
-  kern<<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part);
+  const CUtensorMap nomap{};
+  kern<<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part, nomap, nomap, nullptr);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
     splitk_reduce_kernel<Epi><<<elementwise_grid((int64_t)M * N, 256), 256, 0, st>>>(
@@ -796,6 +899,90 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   }
   if (bias_out) {
     bias_blocks_finish_kernel<<<N, 256, 0, st>>>(bias_ws, w.nkb, bias_out);
+    return check_launch(what);
+  }
+  return 0;
+}
+
+// 1x1 stride-1 weight gradient with both operands streamed by TMA (mode
+// kTma1x1): dW[kout][c] = sum over (image, pixel) of dy[n][kout][p] x[n][c][p];
+// M = C (x rows), N = Kout (dy rows), K = images x 32-pixel blocks (the box
+// is per image; pixels past the image end are zero-filled).  No dY pack pass,
+// no gather; the bias gradient comes from the same dy tiles.
+inline int pick_bn_tma(int N, int& ntiles) {  // <= 192: >= 3 ring stages of 64 KB
+  ntiles = (N + 191) / 192;
+  int per = (N + ntiles - 1) / ntiles;
+  return (per + 31) / 32 * 32;
+}
+
+int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, int Kout, int PQ,
+                  int imgs, const EpiT& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
+                  const char* what, float* bias_out) {
+  if (PQ % 4 || ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) & 15))
+    return -1;
+  Work w{};
+  w.M = C;
+  w.N = Kout;
+  w.cpi = (PQ + BK - 1) / BK;
+  w.nkb = imgs * w.cpi;
+  w.K = w.nkb * BK;
+  w.BN = pick_bn_tma(Kout, w.ntiles);
+  w.mtiles = (C + BM - 1) / BM;
+  w.nacc = w.BN <= 128 ? 2 : 1;
+  w.accs = w.BN;
+  w.abase = (w.nacc * w.BN + 63) / 64 * 64;
+  w.nst = std::min<int>(7, (512 - w.abase) / 64);
+  w.sstride = 2 * w.BN * 128 + BM * 128;
+  w.full_ktab = 0;
+  CUtensorMap amap, bmap;
+  if (!make_nchw_map(&amap, x, PQ, C, imgs, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_nchw_map(&bmap, dy, PQ, Kout, imgs, w.BN, CU_TENSOR_MAP_SWIZZLE_128B))
+    return -1;
+  // workspace: [bias partials: Kout x <= 256 splits][split-K partials]
+  const int64_t bias_bytes = bias_out ? ((int64_t)Kout * 256 * 4 + 1023) / 1024 * 1024 : 0;
+  if (!ws || ws_bytes < bias_bytes) return -1;
+  float* bias_ws = bias_out ? ws : nullptr;
+  float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + bias_bytes);
+  const int64_t part_bytes = ws_bytes - bias_bytes;
+  const int sms = gemm_sm_budget();
+  w.splits = 1;
+  {
+    const int64_t tiles = (int64_t)w.mtiles * w.ntiles;
+    if (tiles < sms) {
+      const int64_t want = sms / tiles;
+      const int64_t by_k = w.nkb / 4;
+      const int64_t by_ws = part_bytes / ((int64_t)C * Kout * 4);
+      w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
+                                                   std::min<int64_t>(by_ws, 256)));
+    }
+  }
+  w.kbps = (w.nkb + w.splits - 1) / w.splits;
+  w.splits = (w.nkb + w.kbps - 1) / w.kbps;
+  w.units = w.mtiles * w.ntiles * w.splits;
+  const int smem_cap = 227 * 1024;
+  const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
+  const int ktab_bytes = STAGES * BK * 8;
+  w.nbst = std::min(kBStagesMax, (smem_cap - tail - ktab_bytes) / w.sstride);
+  if (w.nbst < 2) return -1;
+  const int smem = std::max(tail + w.nbst * w.sstride + ktab_bytes, 120 << 10);
+  auto kern = tc2_kernel<LdWgradX, EpiT, kTma1x1>;
+  static bool configured = false;
+  if (!configured) {
+    BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap),
+            "tc2 smem attribute");
+    configured = true;
+  }
+  const int grid = std::min(w.units, sms);
+  EpiPartial part{part_ws, C, Kout};
+  kern<<<grid, kAllThreads, smem, st>>>(la, w, nullptr, epi, part, amap, bmap, bias_ws);
+  if (int rc = check_launch(what)) return rc;
+  if (w.splits > 1) {
+    splitk_reduce_kernel<EpiT><<<elementwise_grid((int64_t)C * Kout, 256), 256, 0, st>>>(
+        part_ws, w.splits, C, Kout, epi);
+    if (int rc = check_launch(what)) return rc;
+  }
+  if (bias_out) {
+    bias_blocks_finish_kernel<<<Kout, 256, 0, st>>>(bias_ws, w.splits, bias_out);
     return check_launch(what);
   }
   return 0;
@@ -816,6 +1003,17 @@ int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
                    const char* what, float* db, bool* db_done) {
   if (db_done) *db_done = false;
   if (K < 8) return -1;
+  const ConvShape& g = la.g;
+  if (g.R == 1 && g.S == 1 && g.stride == 1 && g.pad == 0 && g.P == g.H && g.Q == g.W &&
+      tc2_tma_wgrad_enabled()) {
+    const int rc = tc2::launch_tma1x1(la, la.x, lb.dy, g.C, g.K, g.H * g.W, g.N, epi, ws,
+                                      ws_bytes, st, what, db);
+    if (rc == 0) {
+      if (db_done) *db_done = db != nullptr;
+      return 0;
+    }
+    if (rc > 0) return rc;
+  }
   const tc2::WgradGeom wg = tc2::wgrad_geom(la.g);
   const int64_t kpad = (int64_t)la.g.N * wg.Pp * wg.Qp;
   if (kpad < (int64_t)K * 2 && kpad < (1LL << 31)) {  // padding waste bounded: fast path

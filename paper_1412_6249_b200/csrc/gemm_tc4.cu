@@ -52,15 +52,6 @@ struct Work {
   int stage_bytes, b_bytes;
 };
 
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                            int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
-}
-
 // MN-major tf32 operand: the only smem layout the tensor core accepts is
 // "128B swizzle with 32B atomicity" (descriptor layout type 1; TMA
 // CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes it): 128-byte K rows of 32
@@ -280,32 +271,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// [imgs][rows][PQ] fp32 activation viewed 3-D, box {32 pixels, 32 rows, 1}, 128B swizzle
-// with 32B atomicity (the MN-major tf32 layout, see mn_sw128_32b_desc)
+// [imgs][rows][PQ] fp32 activation, box {32 pixels, 32 rows, 1}, 128B swizzle with
+// 32B atomicity (the MN-major tf32 layout, see mn_sw128_32b_desc)
 static bool make_act_map(CUtensorMap* map, const float* p, int PQ, int rows, int imgs) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)PQ, (cuuint64_t)rows, (cuuint64_t)imgs};
-  cuuint64_t strides[2] = {(cuuint64_t)PQ * 4, (cuuint64_t)PQ * rows * 4};
-  cuuint32_t box[3] = {32, (cuuint32_t)BK, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return make_nchw_map(map, p, PQ, rows, imgs, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
 inline int pick_bn(int N, int& ntiles) {

@@ -49,7 +49,7 @@ CONV_CASES = [
 ]
 
 
-@pytest.fixture(params=[0, 3, 4], ids=["auto", "halo-v3", "no-tma-1x1"])
+@pytest.fixture(params=[0, 3, 4, 5], ids=["auto", "halo-v3", "no-tma-1x1", "no-tma-wgrad"])
 def gemm_engine(request):
     """0 = default engine choice (1x1 convolutions through the TMA-fed engine
     v4, gemm_tc4.cu); 3 = also route stride-1 R x S convolutions through the
@@ -68,8 +68,8 @@ def test_conv_forward_backward(case, gemm_engine):
     n, c, h, w, k, r, s, p, fl = case
     if gemm_engine == 3 and not (s == 1 and r > 1):
         pytest.skip("engine v3 only takes stride-1 spatial filters")
-    if gemm_engine == 4 and r != 1:
-        pytest.skip("engine switch 4 only changes 1x1 convolutions")
+    if gemm_engine in (4, 5) and r != 1:
+        pytest.skip("engine switches 4 and 5 only change 1x1 convolutions")
     x = rnd(n, c, h, w)
     wt = rnd(k, c, r, r, scale=1.0 / np.sqrt(c * r * r))
     b = rnd(k)
@@ -94,6 +94,37 @@ def test_conv_forward_backward(case, gemm_engine):
     close(outs["dx"], dx_ref, "conv dgrad")
     close(outs["dw"], dw_ref, "conv wgrad")
     close(outs["db"], db_ref, "conv bgrad")
+
+
+@pytest.mark.parametrize("shape", [(4, 64, 56, 56, 64), (2, 192, 28, 28, 16), (3, 480, 14, 14, 208),
+                                   (2, 20, 6, 6, 40), (2, 256, 28, 28, 384), (2, 832, 7, 7, 128),
+                                   (1, 300, 4, 4, 200)])
+@pytest.mark.parametrize("engine", [0, 5], ids=["tma-wgrad", "gather-wgrad"])
+def test_conv1x1_weight_bias_gradient(shape, engine):
+    """bf_conv2d_bwd_weight_bias on 1x1 layers: the TMA-fed weight gradient
+    (kTma1x1, bias from the same dy tiles) and the gather + dY-pack path."""
+    import torch
+    from paper_1412_6249_b200 import _native
+
+    n, c, h, w, k = shape
+    lib = _native.lib()
+    x, dy = rnd(n, c, h, w), rnd(n, k, h, w)
+    _, dw_ref, db_ref = O.conv2d_backward(x, rnd(k, c, 1, 1), dy, 1, 0, False)
+    dev = torch.device("cuda:0")
+    tx, tdy = torch.from_numpy(x).to(dev), torch.from_numpy(dy).to(dev)
+    dw = torch.empty(k, c, 1, 1, device=dev)
+    db = torch.empty(k, device=dev)
+    ws = torch.empty(64 << 20, device=dev)
+    lib("bf_set_gemm_engine", engine)
+    try:
+        lib("bf_conv2d_bwd_weight_bias", tx.data_ptr(), tdy.data_ptr(), dw.data_ptr(),
+            db.data_ptr(), n, c, h, w, k, 1, 1, h, w, 1, 0, ws.data_ptr(), ws.numel() * 4, None)
+        torch.cuda.synchronize()
+    finally:
+        lib("bf_set_gemm_engine", 0)
+    for got, want, what in ((dw.cpu().numpy(), dw_ref, "dw"), (db.cpu().numpy(), db_ref, "db")):
+        assert_close(got, want, rtol=RTOL, atol=ATOL * max(1.0, float(np.abs(want).max())),
+                     what=what)
 
 
 @pytest.mark.parametrize("n,d,m", [(16, 32768, 10), (128, 1024, 1000), (6, 20, 7), (3, 5, 2)])
