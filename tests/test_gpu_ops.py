@@ -46,6 +46,8 @@ CONV_CASES = [
     (3, 480, 14, 14, 208, 1, 1, 0, False),        # 1x1, two pixel tiles per image
     (2, 20, 6, 6, 40, 1, 1, 0, False),            # 1x1, partial channel block, tiny image
     (2, 256, 28, 28, 384, 1, 1, 0, False),        # 1x1, two output-channel tiles
+    (2, 5, 19, 17, 24, 7, 1, 3, False),           # 7x7 stride 1 on 5 channels
+    (1, 2, 16, 16, 40, 8, 3, 2, False),           # 8x8 stride 3
 ]
 
 
