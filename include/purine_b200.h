@@ -51,8 +51,9 @@ long long bf_launch_count(void);
 /* select the GEMM engine: 0 = auto (tcgen05 v2 > v1 where supported), 1 = SIMT fp32,
    2 = tcgen05 v1 only, 3 = auto with the halo-staged engine v3 for stride-1 R x S convs
    (opt-in: measured slower than v2 on GoogLeNet shapes), 4 = auto without the
-   TMA-fed 1x1 engine v4, 5 = auto without the TMA-fed 1x1 weight gradient
-   (A/B comparisons) */
+   TMA-fed 1x1 engine v4, 5 = auto without the TMA-fed 1x1 weight gradient,
+   6 = auto with engine v2's gathers prefetched one k-block ahead in registers
+   instead of staged several k-blocks ahead by cp.async (A/B comparisons) */
 int bf_set_gemm_engine(int engine);
 
 /* bind this library's CUDA runtime to `device` for the calling thread */

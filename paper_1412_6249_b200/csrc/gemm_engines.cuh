@@ -40,8 +40,11 @@ int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const Ep
                    float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 
 extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in),
-                           // 4 auto without v4, 5 auto without the TMA-fed 1x1 weight gradient
+                           // 4 auto without v4, 5 auto without the TMA-fed 1x1 weight gradient,
+                           // 6 auto with register-prefetched (not cp.async-staged) gathers
 // the TMA-fed 1x1 weight gradient (engine v2 mode kTma1x1) is taken unless engine 5
 inline bool tc2_tma_wgrad_enabled() { return g_gemm_engine != 5; }
+// engine v2's gathers staged AD k-blocks ahead through cp.async unless engine 6
+inline bool tc2_async_gather_enabled() { return g_gemm_engine != 6; }
 
 }  // namespace bf

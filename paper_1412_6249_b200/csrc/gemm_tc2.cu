@@ -320,11 +320,30 @@ __device__ __forceinline__ float ldg_pred(const float* p, int ok) {
   return v;
 }
 
-template <class SA, bool kTable, class LA>
+// Where a gathered element goes: RegSink loads it into a register now;
+// AsyncSink issues a 4-byte cp.async (zero-filled when out of bounds) into the
+// thread's own column of a shared-memory staging slot, read back by the same
+// thread AD k-blocks later (loads in flight without holding registers).
+struct RegSink {
+  float (&v)[16];
+  __device__ __forceinline__ void operator()(int j, const float* p, int ok) const {
+    v[j] = ldg_pred(p, ok);
+  }
+};
+struct AsyncSink {
+  uint32_t dst;  // smem address of element 0; element j at dst + j * kProducers * 4
+  __device__ __forceinline__ void operator()(int j, const float* p, int ok) const {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + j * kProducers * 4),
+                 "l"(p), "r"(ok ? 4 : 0)
+                 : "memory");
+  }
+};
+
+template <class SA, bool kTable, class LA, class Sink>
 __device__ __forceinline__ void gather16_impl(const LA& la, const Work& w, const RowInfo* ktab,
                                               const RowInfo& ri, int kbase, int kc0,
                                               const float* __restrict__ pa, unsigned hb,
-                                              unsigned wb, float (&v)[16]) {
+                                              unsigned wb, const Sink& out) {
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int k = kbase + kc0 + j;
@@ -334,28 +353,28 @@ __device__ __forceinline__ void gather16_impl(const LA& la, const Work& w, const
     else
       ki = k < w.K ? SA::kin(la, k) : RowInfo{0, (short)kInvalid, (short)kInvalid};
     const int ok = (unsigned)(ri.h + ki.h) < hb && (unsigned)(ri.w + ki.w) < wb;
-    v[j] = ldg_pred(pa + (ok ? ri.off + ki.off : 0), ok);
+    out(j, pa + (ok ? ri.off + ki.off : 0), ok);
   }
 }
 
 // fast path: the chunk is 16 consecutive channels at one filter tap
-template <class LA>
+template <class LA, class Sink>
 __device__ __forceinline__ void gather16_fast(const LA& la, const RowInfo* ktab,
                                               const RowInfo& ri, int kbase, int kc0,
                                               const float* __restrict__ pa, unsigned hb,
-                                              unsigned wb, float (&v)[16]) {
+                                              unsigned wb, const Sink& out) {
   const ChunkInfo ci = reinterpret_cast<const ChunkInfo*>(ktab)[(kbase + kc0) >> 4];
   const int ok = (unsigned)(ri.h + ci.dh) < hb && (unsigned)(ri.w + ci.dw) < wb;
   const float* p = pa + (ok ? ri.off + ci.off : 0);
   const int stride = Fast<LA>::stride(la);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = ldg_pred(p + j * stride, ok);
+  for (int j = 0; j < 16; ++j) out(j, p + j * stride, ok);
 }
 
-template <int CCW, class LA>
+template <int CCW, class LA, class Sink>
 __device__ __forceinline__ void gather16_wgrad(const LA& la, const Work& w, const RowInfo& ri,
                                                int kk, const float* __restrict__ pa,
-                                               float (&v)[16]) {
+                                               const Sink& out) {
   const ConvShape& g = la.g;
   const int per = w.Pp * w.Qp;
   const int n = kk / per, rem = kk - n * per;
@@ -371,7 +390,7 @@ __device__ __forceinline__ void gather16_wgrad(const LA& la, const Work& w, cons
     const int ih = ihb + jr * st, iw = iwb + jc * st;
     const int ok = live && (p0 + jr < g.P) && (q0 + jc < g.Q) && (unsigned)ih < (unsigned)g.H &&
                    (unsigned)iw < (unsigned)g.W;
-    v[j] = ldg_pred(pa + (ok ? off0 + (int64_t)jr * st * g.W + jc * st : 0), ok);
+    out(j, pa + (ok ? off0 + (int64_t)jr * st * g.W + jc * st : 0), ok);
   }
 }
 
@@ -393,24 +412,34 @@ __device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
 
 // the table/no-table choice is hoisted out of the unrolled loop so the
 // division-heavy fallback is never if-converted into the common path
+template <class SA, int MODE, class LA, class Sink>
+__device__ __forceinline__ void gather16_to(const LA& la, const Work& w, const RowInfo* ktab,
+                                            const RowInfo& ri, int kbase, int kc0,
+                                            const float* __restrict__ pa, unsigned hb,
+                                            unsigned wb, const Sink& out) {
+  if (MODE == kWgrad16)
+    gather16_wgrad<16>(la, w, ri, kbase + kc0, pa, out);
+  else if (MODE == kWgrad8)
+    gather16_wgrad<8>(la, w, ri, kbase + kc0, pa, out);
+  else if (MODE == kChannel)
+    gather16_fast(la, ktab, ri, kbase, kc0, pa, hb, wb, out);
+  else if (w.full_ktab)
+    gather16_impl<SA, true>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, out);
+  else
+    gather16_impl<SA, false>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, out);
+}
 template <class SA, int MODE, class LA>
 __device__ __forceinline__ void gather16(const LA& la, const Work& w, const RowInfo* ktab,
                                          const RowInfo& ri, int kbase, int kc0,
                                          const float* __restrict__ pa, unsigned hb, unsigned wb,
                                          float (&v)[16]) {
-  if (MODE == kWgrad16)
-    gather16_wgrad<16>(la, w, ri, kbase + kc0, pa, v);
-  else if (MODE == kWgrad8)
-    gather16_wgrad<8>(la, w, ri, kbase + kc0, pa, v);
-  else if (MODE == kChannel)
-    gather16_fast(la, ktab, ri, kbase, kc0, pa, hb, wb, v);
-  else if (w.full_ktab)
-    gather16_impl<SA, true>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
-  else
-    gather16_impl<SA, false>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, v);
+  gather16_to<SA, MODE>(la, w, ktab, ri, kbase, kc0, pa, hb, wb, RegSink{v});
 }
 
-template <class LA, class Epi, int MODE>
+// AD > 0: the producers' gathers run AD k-blocks ahead through cp.async into a
+// shared-memory staging ring (AD x 16 KB) instead of one k-block ahead in
+// registers (which is all the 17-warp register budget allows)
+template <class LA, class Epi, int MODE, int AD = 0>
 __global__ void __launch_bounds__(kAllThreads, 1)
     tc2_kernel(LA la, Work w, const uint8_t* __restrict__ bpack, Epi epi, EpiPartial part,
                const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
@@ -424,7 +453,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   uint8_t* tiles = base;
   const int ktab_n = w.full_ktab ? w.nkb * BK : STAGES * BK;
   const int sstride = w.sstride;
-  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nbst * sstride);
+  float* staging = reinterpret_cast<float*>(base + w.nbst * sstride);  // AD x [16][kProducers]
+  RowInfo* ktab = reinterpret_cast<RowInfo*>(base + w.nbst * sstride + AD * 16 * kProducers * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + ktab_n);
   uint64_t* empty = full + STAGES;
   uint64_t* bfull = empty + STAGES;
@@ -582,7 +612,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           }
           named_sync(1, kProducers);
           float v[16];
-          gather16_impl<SA, true>(la, w, slot - kbase, ri, kbase, kc0, pa, hb, wb, v);
+          gather16_impl<SA, true>(la, w, slot - kbase, ri, kbase, kc0, pa, hb, wb, RegSink{v});
           float big[16], small[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -597,6 +627,78 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           mbar_arrive(&full[stage]);
         }
       }
+    } else if (AD > 0 && u < w.units) {
+      // issue cursor (iu, ii) runs AD k-blocks ahead of the consume cursor (u, i)
+      int iu = u, ii = 0, ikb0, ink;
+      RowInfo iri = row_of(iu);
+      {
+        int mt2, nt2, sp2;
+        unit_coords(w, iu, mt2, nt2, sp2);
+        ikb0 = sp2 * w.kbps;
+        ink = min(w.kbps, w.nkb - ikb0);
+      }
+      const uint32_t stg = smem_u32(staging) + t * 4;
+      auto issue = [&](int slot) {
+        if (iu < w.units) {
+          gather16_to<SA, MODE>(la, w, ktab, iri, (ikb0 + ii) * BK, kc0, pa, hb, wb,
+                                AsyncSink{stg + (uint32_t)(slot * 16 * kProducers * 4)});
+          if (++ii >= ink) {
+            iu += gridDim.x;
+            ii = 0;
+            if (iu < w.units) {
+              int mt2, nt2, sp2;
+              unit_coords(w, iu, mt2, nt2, sp2);
+              iri = row_of(iu);
+              ikb0 = sp2 * w.kbps;
+              ink = min(w.kbps, w.nkb - ikb0);
+            }
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+#pragma unroll
+      for (int d = 0; d < (AD > 0 ? AD : 1); ++d) issue(d);
+      int pstage = 0, slot = 0;
+      uint32_t pphase = 0;
+      int nk;
+      {
+        int mt2, nt2, sp2;
+        unit_coords(w, u, mt2, nt2, sp2);
+        nk = min(w.kbps, w.nkb - sp2 * w.kbps);
+      }
+      while (true) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(AD > 0 ? AD - 1 : 0) : "memory");
+        float big[16], small[16];
+        {
+          const float* sv = staging + slot * 16 * kProducers + t;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) split_tf32(sv[j * kProducers], big[j], small[j]);
+        }
+        issue(slot);  // refill the slot just read (its values are in registers)
+        if (++slot == AD) slot = 0;
+        const int stage = pstage;
+        const uint32_t phase = pphase;
+        if (++pstage == w.nst) {
+          pstage = 0;
+          pphase ^= 1;
+        }
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t acol = w.abase + stage * 64 + kc0;
+        tmem_st16(lane_addr + acol, big);
+        tmem_st16(lane_addr + acol + 32, small);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&full[stage]);
+        if (++i >= nk) {
+          u += gridDim.x;
+          i = 0;
+          if (u >= w.units) break;
+          int mt2, nt2, sp2;
+          unit_coords(w, u, mt2, nt2, sp2);
+          nk = min(w.kbps, w.nkb - sp2 * w.kbps);
+        }
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
     } else if (u < w.units) {
       int pstage = 0;
       uint32_t pphase = 0;
@@ -872,18 +974,42 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
   w.full_ktab = (mode == kChannel || (mode == kGeneric && K <= kKtabMax)) ? 1 : 0;
   const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;  // as the kernel carves it
-  w.nbst = (int)std::min<int64_t>(kBStagesMax, (smem_cap - tail - ktab_bytes) / stage_bytes);
+  // async-staged gather depth: 4 k-blocks (64 KB of staging) when that still
+  // leaves >= 3 B stages, else 2, else the register path.  Weight gradients
+  // over pixel rows >= 16 wide only: measured (tools/conv_bench.py, GoogLeNet)
+  // 5-11% faster there (conv1 0.83 -> 0.75 ms), but 4-14% slower on 7x7 maps
+  // and up to 1.9x slower for the table-driven forward / data gradients, whose
+  // per-element 4-byte cp.async costs more issue than the predicated loads
+  int ad = 0;
+  if (tc2_async_gather_enabled() && mode == kWgrad16) {
+    for (int cand : {4, 2}) {
+      const int64_t left = smem_cap - tail - ktab_bytes - (int64_t)cand * 16 * kProducers * 4;
+      if (left / stage_bytes >= 3) {
+        ad = cand;
+        break;
+      }
+    }
+  }
+  const int stg_bytes = ad * 16 * kProducers * 4;
+  w.nbst = (int)std::min<int64_t>(kBStagesMax,
+                                  (smem_cap - tail - ktab_bytes - stg_bytes) / stage_bytes);
   if (w.nbst < 2) return -1;
-  const int smem = tail + (int)(w.nbst * stage_bytes) + ktab_bytes;
-  auto kern = mode == kChannel ? tc2_kernel<LA, Epi, kChannel>
-             : mode == kWgrad16 ? tc2_kernel<LA, Epi, kWgrad16>
-             : mode == kWgrad8  ? tc2_kernel<LA, Epi, kWgrad8>
-                                : tc2_kernel<LA, Epi, kGeneric>;
-  static bool configured[4] = {false, false, false, false};
-  if (!configured[mode]) {
+  const int smem = tail + (int)(w.nbst * stage_bytes) + stg_bytes + ktab_bytes;
+  using KernT = decltype(&tc2_kernel<LA, Epi, kGeneric>);
+  KernT kern;
+  switch (mode * 3 + ad / 2) {
+    case kChannel * 3: kern = tc2_kernel<LA, Epi, kChannel>; break;
+    case kWgrad16 * 3 + 0: kern = tc2_kernel<LA, Epi, kWgrad16>; break;
+    case kWgrad16 * 3 + 1: kern = tc2_kernel<LA, Epi, kWgrad16, 2>; break;
+    case kWgrad16 * 3 + 2: kern = tc2_kernel<LA, Epi, kWgrad16, 4>; break;
+    case kWgrad8 * 3: kern = tc2_kernel<LA, Epi, kWgrad8>; break;
+    default: kern = tc2_kernel<LA, Epi, kGeneric>; break;
+  }
+  static bool configured[16] = {};
+  if (!configured[mode * 3 + ad / 2]) {
     BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap),
             "tc2 smem attribute");
-    configured[mode] = true;
+    configured[mode * 3 + ad / 2] = true;
   }
   // >= 120 KB of shared memory keeps one CTA (one 512-column TMEM allocation) per SM
   const int smem_req = std::max(smem, 120 << 10);

@@ -51,12 +51,15 @@ CONV_CASES = [
 ]
 
 
-@pytest.fixture(params=[0, 3, 4, 5], ids=["auto", "halo-v3", "no-tma-1x1", "no-tma-wgrad"])
+@pytest.fixture(params=[0, 3, 4, 5, 6],
+                ids=["auto", "halo-v3", "no-tma-1x1", "no-tma-wgrad", "reg-prefetch"])
 def gemm_engine(request):
     """0 = default engine choice (1x1 convolutions through the TMA-fed engine
     v4, gemm_tc4.cu); 3 = also route stride-1 R x S convolutions through the
     opt-in halo-staged engine v3 (gemm_tc3.cu); 4 = 1x1 convolutions through
-    the gathering engine v2 instead of v4."""
+    the gathering engine v2 instead of v4; 5 = 1x1 weight gradients gathered
+    instead of TMA-fed; 6 = engine v2 gathers prefetched in registers instead
+    of cp.async-staged."""
     from paper_1412_6249_b200 import _native
 
     lib = _native.lib()
