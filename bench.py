@@ -77,6 +77,25 @@ def _tf32_peak(peaks):
     return bf / 2.0 / 3.0, "measured bf16 sustained (MEASURED_PEAKS.json) / 2 (tf32 rate) / 3 passes"
 
 
+def _step_traffic(net):
+    """DRAM bytes per step of the contraction family and of the HBM-bound kernels,
+    from the newest committed ncu capture of one captured step
+    (profiles/*_step_traffic_*.json, tools/summarize_ncu.py traffic): ncu
+    replays each kernel cold-cache, so this bounds the real (L2-warm) traffic
+    from above."""
+    if net != "googlenet":
+        return None
+    files = sorted((ROOT / "profiles").glob("*_step_traffic_*.json"))
+    if not files:
+        return None
+    try:
+        rec = json.loads(files[-1].read_text())
+        rec["file"] = "profiles/" + files[-1].name
+        return rec
+    except Exception:
+        return None
+
+
 class _Clocks:
     """nvidia-smi sampling during the timed region."""
 
@@ -395,9 +414,15 @@ def run_ours(args):
                 f.write(f"{name}\t{kind}\t{t:.4f}\t{fl / 1e9:.3f}\t{by / 1e6:.2f}\n")
     peaks = _peaks()
     tpeak, basis = _tf32_peak(peaks)
+    traffic = _step_traffic(args.net)
     achieved = contraction_flops / (contraction_ms / 1e3) / 1e12 if contraction_ms else 0.0
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
-                "frac": achieved / tpeak if tpeak else None, "traffic": None,
+                "frac": achieved / tpeak if tpeak else None,
+                "traffic": (traffic or {}).get("contraction", {}).get("dram_bytes"),
+                "traffic_basis": (f"dram__bytes_read.sum + dram__bytes_write.sum of the "
+                                  f"contraction family's launches in one step, bytes per step "
+                                  f"({traffic['file']}, ncu, cold-cache per launch)")
+                                 if traffic else None,
                 "kernel": "conv/fc implicit-GEMM family (fwd+dgrad+wgrad), per step",
                 "peak_basis": basis,
                 "share_of_step": contraction_ms / (ms / args.steps),
@@ -405,7 +430,9 @@ def run_ours(args):
                 "algorithmic_tflop_per_step": contraction_flops / 1e12,
                 "hbm_kernels": {"achieved_gbs": hbm_bytes / (hbm_ms / 1e3) / 1e9 if hbm_ms else None,
                                 "peak_gbs": peaks.get("hbm_gbs", 6533.8),
-                                "ms_per_step": hbm_ms},
+                                "ms_per_step": hbm_ms,
+                                "algorithmic_bytes_per_step": hbm_bytes,
+                                "traffic": (traffic or {}).get("hbm_kernels", {}).get("dram_bytes")},
                 # whole iteration = (FLOP / tensor peak + bytes / HBM peak) / T_step
                 "iteration": {"ideal_ms": 1e3 * (contraction_flops / (tpeak * 1e12) +
                                                  hbm_bytes / (peaks.get("hbm_gbs", 6533.8) * 1e9)),

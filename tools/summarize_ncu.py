@@ -7,6 +7,10 @@
 ``--metrics gpu__time_duration.sum`` CSV (cold-cache, serialised: compare
 shares, not absolutes).  `full`: the headline metrics of a ``--set full``
 capture (duration, DRAM bytes, pipe utilisation, occupancy, stall mix).
+`traffic`: per-family time and DRAM bytes from a ``--metrics
+gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum`` CSV of one
+step (tools/step_profile.py), plus a JSON summary (argv[3]) that bench.py
+reports as ``roofline.traffic``.
 """
 
 import csv
@@ -101,5 +105,59 @@ def full(path):
         print(f"| traffic (read+write) | {rd + wr:.4g} {u.get('dram__bytes_read.sum', '')} |\n")
 
 
+_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1, "usecond": 1e3,
+          "us": 1e3, "msecond": 1e6, "ms": 1e6, "nsecond": 1}
+# kernels of the conv / fc contraction family (the tensor-bound roofline's
+# "kernel"): the implicit GEMMs plus their pack / split-K / bias side kernels
+_CONTRACTION = re.compile(r"^(?:\w+::)*(tc\d?_kernel|tc\d?<|tc_gemm|pack_|splitk_|bias_\w*finish|"
+                         r"simt_gemm|gemm_)")
+
+
+def traffic(path, out_json=None):
+    import json
+
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    per = defaultdict(dict)  # launch id -> metric -> value
+    names = {}
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            v = float(d["Metric Value"].replace(",", "")) * _SCALE.get(d["Metric Unit"], 1)
+            per[d["ID"]][d["Metric Name"]] = v
+            names[d["ID"]] = d["Kernel Name"]
+    agg = defaultdict(lambda: [0, 0.0, 0.0])
+    for lid, m in per.items():
+        f = family(names[lid])
+        a = agg[f]
+        a[0] += 1
+        a[1] += m.get("gpu__time_duration.sum", 0.0)
+        a[2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+    tot_t = sum(a[1] for a in agg.values())
+    print(f"launches: {len(per)}, serialised device time {tot_t / 1e6:.3f} ms, DRAM "
+          f"{sum(a[2] for a in agg.values()) / 1e9:.3f} GB\n")
+    print("| kernel family | launches | ms | share | DRAM MB | GB/s |")
+    print("|---|---:|---:|---:|---:|---:|")
+    for f, (c, ns, by) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"| `{f}` | {c} | {ns / 1e6:.3f} | {ns / tot_t:.1%} | {by / 1e6:.1f} | "
+              f"{by / ns if ns else 0:.0f} |")
+    con = [a for f, a in agg.items() if _CONTRACTION.match(f)]
+    oth = [a for f, a in agg.items() if not _CONTRACTION.match(f)]
+    summary = {"source": path, "launches": len(per), "serialised_ms": tot_t / 1e6,
+               "contraction": {"launches": sum(a[0] for a in con),
+                               "ms": sum(a[1] for a in con) / 1e6,
+                               "dram_bytes": sum(a[2] for a in con)},
+               "hbm_kernels": {"launches": sum(a[0] for a in oth),
+                               "ms": sum(a[1] for a in oth) / 1e6,
+                               "dram_bytes": sum(a[2] for a in oth)}}
+    print("\n```json\n" + json.dumps(summary, indent=1) + "\n```")
+    if out_json:
+        with open(out_json, "w") as fh:
+            json.dump(summary, fh, indent=1)
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
