@@ -536,4 +536,7 @@ KERNELS = {
     "lrn_backward": lambda i, a: [lrn_backward(*i, *_lrn_a(a))],
     "concat_forward": lambda i, a: [concat_forward(i)],
     "concat_backward": lambda i, a: concat_backward(i[0], [int(c) for c in a["channels"]]),
+    # pipeline stage entry: passes input 0 through once the token (input 1)
+    # exists; the token only orders (ops.py:745-747, 803-804)
+    "gate": lambda i, a: [np.array(i[0], dtype=np.float32, copy=True)],
 }
