@@ -279,8 +279,8 @@ __global__ void pack_dy_kernel(LdWgradDYPad lb, int N, int K, int BN, int nkb,
 #ifndef TC2_TRUNC_SPLIT
 #define TC2_TRUNC_SPLIT 1
 #endif
-#ifndef TC2_PREFETCH
-#define TC2_PREFETCH 1
+#ifndef TC2_MAX_NST
+#define TC2_MAX_NST 7
 #endif
 constexpr int kEpiWarps = TC2_EPI_WARPS;
 constexpr int kMmaWarp = kProducerWarps;
@@ -699,43 +699,51 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         }
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
-    } else if (u < w.units) {
+    } else if (MODE == kChannel && u < w.units) {
+      // channel-chunk gathers (fwd / dgrad): two k-blocks of register
+      // prefetch, three buffers used round-robin (the body is instantiated
+      // three times with rotated roles: no moves).  Measured: conv2/3x3 data
+      // gradient 0.64 -> 0.59 ms; the table-driven generic gather (conv1's
+      // forward) is slower with the extra registers, so it keeps one k-block
       int pstage = 0;
       uint32_t pphase = 0;
+      int left = 0;  // k-blocks this CTA publishes
+      for (int uu = u; uu < w.units; uu += gridDim.x) {
+        int mt2, nt2, sp2;
+        unit_coords(w, uu, mt2, nt2, sp2);
+        left += min(w.kbps, w.nkb - sp2 * w.kbps);
+      }
       RowInfo ri = row_of(u);
-      int mt, nt, sp;
-      unit_coords(w, u, mt, nt, sp);
-      int kb0 = sp * w.kbps;
-      int nk = min(w.kbps, w.nkb - kb0);
-      float v[16];
-      gather16<SA, MODE>(la, w, ktab, ri, kb0 * BK, kc0, pa, hb, wb, v);
-      while (true) {
-        // next (unit, k-block) and its prefetch
-        int u2 = u, i2 = i + 1;
-        if (i2 >= nk) {
-          u2 = u + gridDim.x;
-          i2 = 0;
+      int kb0, nk;
+      {
+        int mt2, nt2, sp2;
+        unit_coords(w, u, mt2, nt2, sp2);
+        kb0 = sp2 * w.kbps;
+        nk = min(w.kbps, w.nkb - kb0);
+      }
+      auto issue = [&](float (&dst)[16]) {  // gather the issue cursor's k-block, advance it
+        if (u >= w.units) return;
+        gather16<SA, MODE>(la, w, ktab, ri, (kb0 + i) * BK, kc0, pa, hb, wb, dst);
+        if (++i >= nk) {
+          u += gridDim.x;
+          i = 0;
+          if (u < w.units) {
+            int mt2, nt2, sp2;
+            unit_coords(w, u, mt2, nt2, sp2);
+            ri = row_of(u);
+            kb0 = sp2 * w.kbps;
+            nk = min(w.kbps, w.nkb - kb0);
+          }
         }
-        const bool more = u2 < w.units;
-        RowInfo ri2 = ri;
-        int kb02 = kb0, nk2 = nk, nt2 = nt;
-        float v2[16];
-        if (more && u2 != u) {
-          int mt2, sp2;
-          unit_coords(w, u2, mt2, nt2, sp2);
-          ri2 = row_of(u2);
-          kb02 = sp2 * w.kbps;
-          nk2 = min(w.kbps, w.nkb - kb02);
-        }
-#if TC2_PREFETCH
-        if (more) gather16<SA, MODE>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
-#endif
-        // current k-block: split, publish to TMEM + kick off the B tile
+      };
+      float va[16], vb[16], vc[16];
+      issue(va);
+      issue(vb);
+      auto step = [&](float (&cur)[16], float (&pre)[16]) -> bool {
+        issue(pre);
         float big[16], small[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          split_tf32(v[j], big[j], small[j]);
-        }
+        for (int j = 0; j < 16; ++j) split_tf32(cur[j], big[j], small[j]);
         const int stage = pstage;
         const uint32_t phase = pphase;
         if (++pstage == w.nst) {
@@ -749,19 +757,63 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&full[stage]);
-        ++it;
-        if (!more) break;
-#if !TC2_PREFETCH
-        gather16<SA, MODE>(la, w, ktab, ri2, (kb02 + i2) * BK, kc0, pa, hb, wb, v2);
-#endif
-        u = u2;
-        i = i2;
-        ri = ri2;
-        kb0 = kb02;
-        nk = nk2;
-        nt = nt2;
+        return --left > 0;
+      };
+      while (step(va, vc) && step(vb, va) && step(vc, vb)) {
+      }
+    } else if (u < w.units) {
+      // one k-block of register prefetch in two fixed buffers used ping-pong
+      // (the loop body is instantiated twice with the roles swapped): a
+      // rotation copy v = v2 would stall on the prefetch loads at the end of
+      // every k-block (ncu: 9.5% of the conv2 data gradient's samples on that
+      // move), i.e. no overlap across the publish step
+      int pstage = 0;
+      uint32_t pphase = 0;
+      RowInfo ri = row_of(u);
+      int kb0, nk;
+      {
+        int mt2, nt2, sp2;
+        unit_coords(w, u, mt2, nt2, sp2);
+        kb0 = sp2 * w.kbps;
+        nk = min(w.kbps, w.nkb - kb0);
+      }
+      float va[16], vb[16];
+      gather16<SA, MODE>(la, w, ktab, ri, kb0 * BK, kc0, pa, hb, wb, va);
+      // publishes `cur` (the current k-block), prefetching the next into `nxt`;
+      // false once the last k-block is published
+      auto step = [&](float (&cur)[16], float (&nxt)[16]) -> bool {
+        if (++i >= nk) {
+          u += gridDim.x;
+          i = 0;
+          if (u < w.units) {
+            int mt2, nt2, sp2;
+            unit_coords(w, u, mt2, nt2, sp2);
+            ri = row_of(u);
+            kb0 = sp2 * w.kbps;
+            nk = min(w.kbps, w.nkb - kb0);
+          }
+        }
+        const bool more = u < w.units;
+        if (more) gather16<SA, MODE>(la, w, ktab, ri, (kb0 + i) * BK, kc0, pa, hb, wb, nxt);
+        float big[16], small[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = v2[j];
+        for (int j = 0; j < 16; ++j) split_tf32(cur[j], big[j], small[j]);
+        const int stage = pstage;
+        const uint32_t phase = pphase;
+        if (++pstage == w.nst) {
+          pstage = 0;
+          pphase ^= 1;
+        }
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t acol = w.abase + stage * 64 + kc0;
+        tmem_st16(lane_addr + acol, big);
+        tmem_st16(lane_addr + acol + 32, small);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&full[stage]);
+        return more;
+      };
+      while (step(va, vb) && step(vb, va)) {
       }
     }
   } else if (warp == kMmaWarp) {
@@ -927,10 +979,15 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.BN = pick_bn(N, w.ntiles);
   w.nkb = (K + BK - 1) / BK;
   w.mtiles = (M + BM - 1) / BM;
-  w.nacc = w.BN <= 128 ? 2 : 1;
+#ifndef TC2_NACC1_MIN_KB
+#define TC2_NACC1_MIN_KB 1000000000
+#endif
+  // one accumulator (a deeper TMEM A ring) for long k loops, where the ring
+  // depth bounds throughput and the epilogue is a small part of a tile
+  w.nacc = (w.BN <= 128 && w.nkb < TC2_NACC1_MIN_KB) ? 2 : 1;
   w.accs = w.BN;  // multiple of 32
   w.abase = (w.nacc * w.BN + 63) / 64 * 64;
-  w.nst = std::min<int>(7, (512 - w.abase) / 64);
+  w.nst = std::min<int>(TC2_MAX_NST, (512 - w.abase) / 64);
   const int64_t stage_bytes = 2LL * w.BN * 128;
   w.sstride = (int)stage_bytes;
   const int64_t pack_bytes = (int64_t)w.ntiles * w.nkb * stage_bytes;
