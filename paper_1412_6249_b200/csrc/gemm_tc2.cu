@@ -344,6 +344,28 @@ __device__ __forceinline__ void gather16_impl(const LA& la, const Work& w, const
                                               const RowInfo& ri, int kbase, int kc0,
                                               const float* __restrict__ pa, unsigned hb,
                                               unsigned wb, const Sink& out) {
+  if constexpr (kTable) {
+    // the 16 table entries (the same for the whole warp: broadcast) come in as
+    // 8 x 16-byte shared loads; both bounds tests are evaluated branch-free
+    // (a short-circuit && made ptxas predicate the second entry load and
+    // reload the bounds from constant memory per element)
+    const uint32_t kt = smem_u32(ktab + kbase + kc0);
+#pragma unroll
+    for (int j2 = 0; j2 < 16; j2 += 2) {
+      int off0, hw0, off1, hw1;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(off0), "=r"(hw0), "=r"(off1), "=r"(hw1)
+                   : "r"(kt + j2 * 8));
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int off = h2 ? off1 : off0, hw = h2 ? hw1 : hw0;
+        const int kh = (int)(short)(hw & 0xffff), kw = hw >> 16;
+        const int ok = ((unsigned)(ri.h + kh) < hb) & ((unsigned)(ri.w + kw) < wb);
+        out(j2 + h2, pa + (ok ? ri.off + off : 0), ok);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int k = kbase + kc0 + j;
