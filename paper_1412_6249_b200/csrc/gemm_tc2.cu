@@ -1037,7 +1037,11 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.splits = 1;
   {
     int64_t tiles = (int64_t)w.mtiles * w.ntiles;
-    if (tiles < sms) {
+#ifndef TC2_NOSPLIT_MIN_TILES  // forward / data gradients with >= 16 tiles are not split:
+#define TC2_NOSPLIT_MIN_TILES 16  // inside a step the concurrent Inception branches fill the
+#endif                            // SMs, and the partials + reduce launch cost more (+1.2%)
+    const bool wgrad_pack = std::is_same_v<LBP, LdWgradDYPad>;
+    if (tiles < sms && (wgrad_pack || tiles < TC2_NOSPLIT_MIN_TILES)) {
       int64_t want = sms / tiles;  // one wave: units <= SMs (ceil would leave a 2-unit tail)
       int64_t by_k = w.nkb / 4;
       int64_t by_ws = part_bytes / ((int64_t)M * N * 4);

@@ -319,7 +319,10 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
   const int sms = gemm_sm_budget();
   w.splits = 1;
   const int64_t tiles = (int64_t)imgs * w.tiles_img * w.ntiles;
-  if (tiles < sms) {
+#ifndef TC4_NOSPLIT_MIN_TILES
+#define TC4_NOSPLIT_MIN_TILES 1000000
+#endif
+  if (tiles < sms && tiles < TC4_NOSPLIT_MIN_TILES) {
     const int64_t want = sms / tiles;
     const int64_t by_k = w.nkb / 2;
     const int64_t by_ws = part_bytes / ((int64_t)M * Nout * 4);
