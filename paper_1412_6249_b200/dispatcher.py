@@ -20,7 +20,7 @@ lane-level overlap (compute lanes vs. copy lanes) on the GPU.
 
 Inside a compute lane, independent operators (Inception branches; weight vs.
 data gradients) are further spread over up to ``PURINE_B200_BRANCH_STREAMS``
-(default 4) streams by greedy chain decomposition, with event waits on every
+(default 8) streams by greedy chain decomposition, with event waits on every
 cross-stream input: an operator starts when its inputs' events fire.  Lanes
 that carry collectives keep one stream, created at high priority so the block
 scheduler starts exchange CTAs ahead of queued compute CTAs.
@@ -505,7 +505,7 @@ BRANCH_ENV = "PURINE_B200_BRANCH_STREAMS"  # device streams per compute lane (1 
 
 
 def _branch_streams() -> int:
-    raw = os.environ.get(BRANCH_ENV, "4")
+    raw = os.environ.get(BRANCH_ENV, "8")
     try:
         k = int(raw)
     except ValueError:
