@@ -1133,7 +1133,10 @@ __global__ void __launch_bounds__(256) lrn5_bwd_rc_kernel(const float* __restric
     lrn_ld<V>(xb + (int64_t)(c + 7) * HW, c + 7 >= 0 && c + 7 < C, xl);
     lrn_ld<V>(db + (int64_t)(c + 5) * HW, c + 5 >= 0 && c + 5 < C, dl);
     const bool emit = c >= c0;
-    if (relu_x && emit) Vec<V>::ld(relu_x + base + (int64_t)c * HW, rx);
+    // relu_x == x: the folded ReLU's mask is x's own sign (x is that ReLU's
+    // output: relu(a) > 0 <=> a > 0), already in registers as xq[0]
+    const bool own = relu_x == x;
+    if (relu_x && !own && emit) Vec<V>::ld(relu_x + base + (int64_t)c * HW, rx);
     const bool live = c + 2 >= 0 && c + 2 < C;
 #pragma unroll
     for (int v = 0; v < V; ++v) {
@@ -1160,7 +1163,7 @@ __global__ void __launch_bounds__(256) lrn5_bwd_rc_kernel(const float* __restric
         const float a = __fmul_rn(dq[0][v], pq[0][v]);
         const float b = __fmul_rn(__fmul_rn(coef, xq[0][v]), acc);
         out[v] = __fsub_rn(a, b);
-        if (relu_x) out[v] = rx[v] > 0.f ? out[v] : 0.f;
+        if (relu_x) out[v] = (own ? xq[0][v] : rx[v]) > 0.f ? out[v] : 0.f;
       }
       Vec<V>::st(dx + base + (int64_t)c * HW, out);
     }

@@ -433,8 +433,17 @@ class _Plan:
             if (p is None or graph.operators[p].kind not in foldable or p in self.fusion
                     or len(graph.consumers_of(g)) != 1 or p in self.fused_away):
                 continue
-            self.fusion[p] = {"relu_x": graph.tensors[op.inputs[0]].name,
-                              "relu_dx": graph.tensors[op.outputs[0]].name}
+            rx = graph.tensors[op.inputs[0]].name
+            pk = graph.operators[p]
+            if pk.kind == "lrn_backward":
+                # the LRN's own input is the ReLU's output: its sign is the
+                # same mask (relu(a) > 0 <=> a > 0) and the kernel already
+                # reads it -- the pre-activation is not read again
+                for c, _ in graph.consumers_of(op.inputs[0]):
+                    cop = graph.operators[c]
+                    if cop.kind == "relu_forward" and cop.outputs[0] == pk.inputs[0]:
+                        rx = graph.tensors[pk.inputs[0]].name
+            self.fusion[p] = {"relu_x": rx, "relu_dx": graph.tensors[op.outputs[0]].name}
             self.fused_away.add(oid)
             self.elided.add(graph.tensors[g].name)
 
