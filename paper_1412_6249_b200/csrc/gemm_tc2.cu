@@ -564,6 +564,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       // chunks into per-row bias partials.
       const int m_row = q * 32 + lane;
       const int nb = BN / 32;  // 16-byte B chunks per thread per stage
+      int bs = 0, stage = 0;
+      uint32_t bph = 0, ph = 0;
       for (; u < w.units; u += gridDim.x) {
         int mt, nt, sp;
         unit_coords(w, u, mt, nt, sp);
@@ -573,10 +575,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         float bsum[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) bsum[j] = 0.f;
-        for (int i2 = 0; i2 < nk; ++i2, ++it) {
-          const int bs = it % w.nbst;
-          const int stage = it % w.nst;
-          mbar_wait(&bfull[bs], (it / w.nbst) & 1);
+        for (int i2 = 0; i2 < nk; ++i2) {
+          mbar_wait(&bfull[bs], bph);
           uint8_t* sb = tiles + bs * sstride;
           const uint8_t* araw = sb + 2 * BN * 128;
           float big[16], small[16];
@@ -609,13 +609,21 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           }
           // generic-proxy smem writes -> visible to the tensor core (async proxy)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_wait(&empty[stage], ((it / w.nst) & 1) ^ 1);
+          mbar_wait(&empty[stage], ph ^ 1);
           const uint32_t acol = w.abase + stage * 64 + kc0;
           tmem_st16(lane_addr + acol, big);
           tmem_st16(lane_addr + acol + 32, small);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
           mbar_arrive(&full[stage]);
+          if (++bs == w.nbst) {
+            bs = 0;
+            bph ^= 1;
+          }
+          if (++stage == w.nst) {
+            stage = 0;
+            ph ^= 1;
+          }
         }
         if (do_bias) {
           // chunk f of the tile is row f / 8: the 8 lanes t^1, t^2, t^4 share a row
@@ -635,6 +643,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     } else if (MODE == kGeneric && !w.full_ktab) {
       // K too long for a cached table (weight gradients: K = N*P*Q pixels):
       // the k-block's 32 gather offsets are computed per stage into a ring slot
+      int gstage = 0;
+      uint32_t gphase = 0;
       for (; u < w.units; u += gridDim.x) {
         int mt, nt, sp;
         unit_coords(w, u, mt, nt, sp);
@@ -642,8 +652,12 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         const int kb0 = sp * w.kbps;
         const int nk = min(w.kbps, w.nkb - kb0);
         for (int i2 = 0; i2 < nk; ++i2, ++it) {
-          const int stage = it % w.nst;
-          const uint32_t phase = (it / w.nst) & 1;
+          const int stage = gstage;
+          const uint32_t phase = gphase;
+          if (++gstage == w.nst) {
+            gstage = 0;
+            gphase ^= 1;
+          }
           const int kbase = (kb0 + i2) * BK;
           RowInfo* slot = ktab + stage * BK;
           if (t < BK) {
@@ -866,7 +880,10 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       const uint32_t idesc = tf32_idesc(BN);
       const uint64_t dtiles = sw128_desc(smem_u32(tiles));  // B stage 0, big image, k-step 0
       const uint64_t dsmall = (uint64_t)((BN * 128) >> 4);   // big -> small image
-      int it = 0, local = 0;
+      // ring positions advance incrementally: a runtime modulo / divide per
+      // k-block cost the single issuing warp ~80 instructions
+      int stage = 0, bst = 0, local = 0;
+      uint32_t phase = 0, bphase = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
         int mt, nt, sp;
         unit_coords(w, u, mt, nt, sp);
@@ -876,10 +893,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         mbar_wait(&acc_empty[b], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t dacc = tmem + (uint32_t)(b * w.accs);
-        for (int i = 0; i < nk; ++i, ++it) {
-          const int stage = it % w.nst, bst = it % w.nbst;
-          const uint32_t phase = (it / w.nst) & 1;
-          mbar_wait(&bfull[bst], (it / w.nbst) & 1);
+        for (int i = 0; i < nk; ++i) {
+          mbar_wait(&bfull[bst], bphase);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           // descriptor start-address field = smem byte address >> 4 (bits 0-13)
@@ -905,6 +920,14 @@ __global__ void __launch_bounds__(kAllThreads, 1)
             tc_commit(&bempty[bst]);
           }
           __syncwarp();
+          if (++stage == w.nst) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++bst == w.nbst) {
+            bst = 0;
+            bphase ^= 1;
+          }
         }
         if (elect_one()) tc_commit(&acc_full[b]);
         __syncwarp();
@@ -917,36 +940,44 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     // critical path of the producers
     if (MODE == kTma1x1 && lane == 0) {
       // raw dy tile (BN rows) and x tile (BM rows) of one 32-pixel k-block
-      int it = 0;
+      int bst = 0;
+      uint32_t bphase = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
         int mt, nt, sp;
         unit_coords(w, u, mt, nt, sp);
         const int kb0 = sp * w.kbps;
         const int nk = min(w.kbps, w.nkb - kb0);
-        for (int i = 0; i < nk; ++i, ++it) {
-          const int bst = it % w.nbst;
-          mbar_wait(&bempty[bst], ((it / w.nbst) & 1) ^ 1);
+        for (int i = 0; i < nk; ++i) {
+          mbar_wait(&bempty[bst], bphase ^ 1);
           mbar_arrive_expect_tx(&bfull[bst], (uint32_t)(BN * 128 + BM * 128));
           const int kb = kb0 + i, img = kb / w.cpi, pix = (kb - img * w.cpi) * BK;
           uint8_t* sb = tiles + bst * sstride;
           tma_load_3d(smem_u32(sb), &bmap, pix, nt * BN, img, &bfull[bst]);
           tma_load_3d(smem_u32(sb + 2 * BN * 128), &amap, pix, mt * BM, img, &bfull[bst]);
+          if (++bst == w.nbst) {
+            bst = 0;
+            bphase ^= 1;
+          }
         }
       }
     } else if (lane == 0) {
-      int it = 0;
+      int bst = 0;
+      uint32_t bphase = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
         int mt, nt, sp;
         unit_coords(w, u, mt, nt, sp);
         const int kb0 = sp * w.kbps;
         const int nk = min(w.kbps, w.nkb - kb0);
-        for (int i = 0; i < nk; ++i, ++it) {
-          const int bst = it % w.nbst;
-          mbar_wait(&bempty[bst], ((it / w.nbst) & 1) ^ 1);
+        for (int i = 0; i < nk; ++i) {
+          mbar_wait(&bempty[bst], bphase ^ 1);
           mbar_arrive_expect_tx(&bfull[bst], (uint32_t)stage_bytes);
           bulk_g2s(smem_u32(tiles + bst * sstride),
                    bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
                    &bfull[bst]);
+          if (++bst == w.nbst) {
+            bst = 0;
+            bphase ^= 1;
+          }
         }
       }
     }

@@ -129,14 +129,20 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (warp == kTmaWarp) {
     // ======================= TMA issue =======================
     if (lane == 0) {
-      int it = 0;
+      int rs = 0;
+      uint32_t rph = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
         int img, pt, nt, sp;
         unit_coords(w, u, img, pt, nt, sp);
         const int kb0 = sp * w.kbps, nk = min(w.kbps, w.nkb - kb0);
-        for (int i = 0; i < nk; ++i, ++it) {
-          const int s = it % w.nst;
-          mbar_wait(&empty[s], ((it / w.nst) & 1) ^ 1);
+        for (int i = 0; i < nk; ++i) {
+          const int s = rs;
+          const uint32_t sph = rph;
+          if (++rs == w.nst) {
+            rs = 0;
+            rph ^= 1;
+          }
+          mbar_wait(&empty[s], sph ^ 1);
           mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(kABytes + w.b_bytes));
           uint8_t* st = base + s * w.stage_bytes;
           const int kc = (kb0 + i) * BK;
@@ -153,14 +159,20 @@ __global__ void __launch_bounds__(kThreads, 2)
   } else if (warp >= kSplitWarp0 && warp < kSplitWarp0 + kSplitWarps) {
     // ======================= split: small = x - trunc(x) =======================
     const int t = threadIdx.x - kSplitWarp0 * 32;
-    int it = 0;
+    int rs = 0;
+    uint32_t rph = 0;
     for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
       int img, pt, nt, sp;
       unit_coords(w, u, img, pt, nt, sp);
       const int nk = min(w.kbps, w.nkb - sp * w.kbps);
-      for (int i = 0; i < nk; ++i, ++it) {
-        const int s = it % w.nst;
-        mbar_wait(&raw_full[s], (it / w.nst) & 1);
+      for (int i = 0; i < nk; ++i) {
+        const int s = rs;
+        const uint32_t sph = rph;
+        if (++rs == w.nst) {
+          rs = 0;
+          rph ^= 1;
+        }
+        mbar_wait(&raw_full[s], sph);
         const float4* src = reinterpret_cast<const float4*>(base + s * w.stage_bytes);
         float4* dst = reinterpret_cast<float4*>(base + s * w.stage_bytes + kABytes);
 #pragma unroll
@@ -184,7 +196,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     {
       // A MN-major (bit 15), B K-major; M = 128, N = BN
       const uint32_t idesc = tf32_idesc(BN) | (1u << 15);
-      int it = 0, local = 0;
+      int rs = 0, local = 0;
+      uint32_t rph = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
         int img, pt, nt, sp;
         unit_coords(w, u, img, pt, nt, sp);
@@ -194,9 +207,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_wait(&acc_empty[b], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t dacc = tmem + (uint32_t)(b * BN);
-        for (int i = 0; i < nk; ++i, ++it) {
-          const int s = it % w.nst;
-          mbar_wait(&split_full[s], (it / w.nst) & 1);
+        for (int i = 0; i < nk; ++i) {
+          const int s = rs;
+          const uint32_t sph = rph;
+          if (++rs == w.nst) {
+            rs = 0;
+            rph ^= 1;
+          }
+          mbar_wait(&split_full[s], sph);
           tc_fence_after();
           const uint32_t st = smem_u32(base + s * w.stage_bytes);
           const uint64_t abig = mn_sw128_32b_desc(st), asmall = mn_sw128_32b_desc(st + kABytes);
