@@ -316,11 +316,20 @@ inline void divmagic(uint32_t d, uint64_t& m, int& s) {
 //       4 TMA-fed 1x1 weight gradient (both operands K-major NCHW tiles, no pack)
 enum { kGeneric = 0, kChannel = 1, kWgrad16 = 2, kWgrad8 = 3, kTma1x1 = 4 };
 
+// q = x / d, r = x % d, with the (common, warp-uniform) d == 1 case free
+__device__ __forceinline__ void divmod_u(int x, int d, int& q, int& r) {
+  if (d == 1) {
+    q = x;
+    r = 0;
+  } else {
+    q = x / d;
+    r = x - q * d;
+  }
+}
 __device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& nt, int& sp) {
-  sp = u % w.splits;
-  int r = u / w.splits;
-  nt = r % w.ntiles;
-  mt = r / w.ntiles;
+  int r;
+  divmod_u(u, w.splits, r, sp);
+  divmod_u(r, w.ntiles, mt, nt);
 }
 
 __device__ __forceinline__ float ldg_pred(const float* p, int ok) {

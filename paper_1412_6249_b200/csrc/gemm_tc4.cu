@@ -78,12 +78,21 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint3
 
 __device__ __forceinline__ void unit_coords(const Work& w, int u, int& img, int& pt, int& nt,
                                             int& sp) {
-  sp = u % w.splits;
-  int r = u / w.splits;
-  nt = r % w.ntiles;
-  r /= w.ntiles;
-  pt = r % w.tiles_img;
-  img = r / w.tiles_img;
+  // divisions by 1 (no split-K, one channel tile, one pixel tile) skipped:
+  // warp-uniform branches, ~20 instructions saved per division per unit
+  auto dm = [](int x, int d, int& q, int& r) {
+    if (d == 1) {
+      q = x;
+      r = 0;
+    } else {
+      q = x / d;
+      r = x - q * d;
+    }
+  };
+  int r, r2;
+  dm(u, w.splits, r, sp);
+  dm(r, w.ntiles, r2, nt);
+  dm(r2, w.tiles_img, img, pt);
 }
 
 template <class Epi>
