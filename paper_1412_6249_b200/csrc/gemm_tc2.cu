@@ -279,6 +279,17 @@ __global__ void pack_dy_kernel(LdWgradDYPad lb, int N, int K, int BN, int nkb,
 #ifndef TC2_TRUNC_SPLIT
 #define TC2_TRUNC_SPLIT 1
 #endif
+// one tcgen05.commit per k-block: the A and B rings have the same depth and
+// the B loader recycles a stage on the A ring's release barrier (each commit
+// costs the single issuing thread ~130 cycles, profiles/r01_mma_probe.md)
+#ifndef TC2_ONE_COMMIT
+#define TC2_ONE_COMMIT 1
+#endif
+#if TC2_ONE_COMMIT
+#define TC2_BRELEASE empty
+#else
+#define TC2_BRELEASE bempty
+#endif
 #ifndef TC2_MAX_NST
 #define TC2_MAX_NST 7
 #endif
@@ -926,7 +937,9 @@ __global__ void __launch_bounds__(kAllThreads, 1)
               mma_ts_flag<1>(dacc, ab + ks * 8, db + k2, idesc);
             }
             tc_commit(&empty[stage]);
+#if !TC2_ONE_COMMIT
             tc_commit(&bempty[bst]);
+#endif
           }
           __syncwarp();
           if (++stage == w.nst) {
@@ -957,7 +970,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         const int kb0 = sp * w.kbps;
         const int nk = min(w.kbps, w.nkb - kb0);
         for (int i = 0; i < nk; ++i) {
-          mbar_wait(&bempty[bst], bphase ^ 1);
+          mbar_wait(&TC2_BRELEASE[bst], bphase ^ 1);
           mbar_arrive_expect_tx(&bfull[bst], (uint32_t)(BN * 128 + BM * 128));
           const int kb = kb0 + i, img = kb / w.cpi, pix = (kb - img * w.cpi) * BK;
           uint8_t* sb = tiles + bst * sstride;
@@ -978,7 +991,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         const int kb0 = sp * w.kbps;
         const int nk = min(w.kbps, w.nkb - kb0);
         for (int i = 0; i < nk; ++i) {
-          mbar_wait(&bempty[bst], bphase ^ 1);
+          mbar_wait(&TC2_BRELEASE[bst], bphase ^ 1);
           mbar_arrive_expect_tx(&bfull[bst], (uint32_t)stage_bytes);
           bulk_g2s(smem_u32(tiles + bst * sstride),
                    bpack + ((size_t)nt * w.nkb + kb0 + i) * stage_bytes, (uint32_t)stage_bytes,
@@ -1138,6 +1151,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   const int stg_bytes = ad * 16 * kProducers * 4;
   w.nbst = (int)std::min<int64_t>(kBStagesMax,
                                   (smem_cap - tail - ktab_bytes - stg_bytes) / stage_bytes);
+  if (TC2_ONE_COMMIT) w.nst = w.nbst = std::min(w.nst, w.nbst);
   if (w.nbst < 2) return -1;
   const int smem = tail + (int)(w.nbst * stage_bytes) + stg_bytes + ktab_bytes;
   using KernT = decltype(&tc2_kernel<LA, Epi, kGeneric>);
@@ -1234,6 +1248,7 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
   const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
   const int ktab_bytes = STAGES * BK * 8;
   w.nbst = std::min(kBStagesMax, (smem_cap - tail - ktab_bytes) / w.sstride);
+  if (TC2_ONE_COMMIT) w.nst = w.nbst = std::min(w.nst, w.nbst);
   if (w.nbst < 2) return -1;
   const int smem = std::max(tail + w.nbst * w.sstride + ktab_bytes, 120 << 10);
   auto kern = tc2_kernel<LdWgradX, EpiT, kTma1x1>;
