@@ -220,14 +220,17 @@ __global__ void pack_dy_kernel(LdWgradDYPad lb, int N, int K, int BN, int nkb,
   uint8_t* base = out + ((size_t)tile * nkb + kb) * 2 * BN * 128;
   const int per = lb.Pp * lb.Qp;
   const bool vec = (lb.Q & 3) == 0;
+  // the stride (blockDim, a multiple of 8) keeps each thread on one 4-pixel
+  // column chunk c: its pixel decode is done once, not per row
+  const int c = threadIdx.x & 7;
+  const int k0 = kb * BK + c * 4;
+  const int n = k0 / per, rem = k0 - n * per;
+  const int p = rem / lb.Qp, q = rem - p * lb.Qp;
   for (int i = threadIdx.x; i < BN * 8; i += blockDim.x) {
-    const int r = i >> 3, c = i & 7;
+    const int r = i >> 3;
     const int ko = tile * BN + r;
-    const int k0 = kb * BK + c * 4;
     float v[4] = {0.f, 0.f, 0.f, 0.f};
     if (ko < N && k0 < K) {
-      const int n = k0 / per, rem = k0 - n * per;
-      const int p = rem / lb.Qp, q = rem - p * lb.Qp;
       if (p < lb.P) {
         const float* src = lb.dy + (((int64_t)n * lb.K + ko) * lb.P + p) * lb.Q + q;
         if (vec && q + 3 < lb.Q) {
