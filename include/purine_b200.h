@@ -53,7 +53,9 @@ long long bf_launch_count(void);
    (opt-in: measured slower than v2 on GoogLeNet shapes), 4 = auto without the
    TMA-fed 1x1 engine v4, 5 = auto without the TMA-fed 1x1 weight gradient,
    6 = auto with engine v2's gathers prefetched one k-block ahead in registers
-   instead of staged several k-blocks ahead by cp.async (A/B comparisons) */
+   instead of staged several k-blocks ahead by cp.async, 7 = auto + the raw dY
+   streamed by TMA (no dY pack) for weight gradients over 16-aligned pixel
+   rows such as conv1's (opt-in: measured neutral) (A/B comparisons) */
 int bf_set_gemm_engine(int engine);
 
 /* bind this library's CUDA runtime to `device` for the calling thread */

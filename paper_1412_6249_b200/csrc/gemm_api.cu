@@ -39,10 +39,11 @@ using namespace bf;
 extern "C" {
 
 int bf_set_gemm_engine(int engine) {
-  BF_REQUIRE(engine >= 0 && engine <= 6,
+  BF_REQUIRE(engine >= 0 && engine <= 7,
              "bf_set_gemm_engine: 0 (auto), 1 (simt), 2 (tcgen05 v1 only), 3 (auto + halo engine "
              "v3), 4 (auto without the 1x1 TMA engine v4), 5 (auto without the TMA-fed 1x1 "
-             "weight gradient), 6 (auto with register-prefetched gathers)");
+             "weight gradient), 6 (auto with register-prefetched gathers), 7 (auto + TMA-streamed "
+             "raw dY for conv1-type weight gradients)");
   g_gemm_engine = engine;
   return 0;
 }
@@ -72,7 +73,7 @@ int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, flo
   LdFwdX la{x, g};
   LdRowK lb{w, (int64_t)C * R * S};
   EpiNCHW epi{y, b, P * Q, K, relu_cat, (int64_t)relu_ctot * P * Q, relu_c0};
-  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 3) {
+  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3) {
     int rc = tc4_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
     if (rc >= 0) return rc;
   }
@@ -80,7 +81,7 @@ int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, flo
     int rc = tc3_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
     if (rc >= 0) return rc;
   }
-  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 3 || g_gemm_engine == 4) {
+  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3 || g_gemm_engine == 4) {
     int rc = tc2_conv_fwd(la, lb, N * P * Q, K, C * R * S, epi, ws, ws_bytes, as_stream(s),
                           "conv2d_forward");
     if (rc >= 0) return rc;
@@ -105,7 +106,7 @@ int bf_conv2d_bwd_data_relu(const float* w, const float* dy, float* dx, const fl
   LdDgradW lb{w, g};
   EpiNCHW epi{dx, nullptr, H * W, C};
   epi.relu_x = relu_x;
-  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 3) {
+  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3) {
     int rc = tc4_conv_dgrad(g, dy, w, epi, ws, ws_bytes, as_stream(s), "conv2d_backward_data");
     if (rc >= 0) return rc;
   }
@@ -113,7 +114,7 @@ int bf_conv2d_bwd_data_relu(const float* w, const float* dy, float* dx, const fl
     int rc = tc3_conv_dgrad(g, dy, w, epi, ws, ws_bytes, as_stream(s), "conv2d_backward_data");
     if (rc >= 0) return rc;
   }
-  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 3 || g_gemm_engine == 4) {
+  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3 || g_gemm_engine == 4) {
     int rc = tc2_conv_dgrad(la, lb, N * H * W, C, K * R * S, epi, ws, ws_bytes, as_stream(s),
                             "conv2d_backward_data");
     if (rc >= 0) return rc;
@@ -139,7 +140,7 @@ int bf_conv2d_bwd_weight_bias(const float* x, const float* dy, float* dw, float*
   EpiT epi{dw, nullptr, (int64_t)C * R * S};
   int rc = -1;
   bool db_done = false;
-  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 3 || g_gemm_engine == 4)
+  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3 || g_gemm_engine == 4)
     rc = tc2_conv_wgrad(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
                         "conv2d_backward_weight", db, &db_done);
   if (rc < 0)

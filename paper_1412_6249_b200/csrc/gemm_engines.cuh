@@ -41,10 +41,16 @@ int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const Ep
 
 extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in),
                            // 4 auto without v4, 5 auto without the TMA-fed 1x1 weight gradient,
-                           // 6 auto with register-prefetched (not cp.async-staged) gathers
+                           // 6 auto with register-prefetched (not cp.async-staged) gathers,
+                           // 7 auto + TMA-streamed raw dY for conv1-type weight gradients
 // the TMA-fed 1x1 weight gradient (engine v2 mode kTma1x1) is taken unless engine 5
 inline bool tc2_tma_wgrad_enabled() { return g_gemm_engine != 5; }
 // engine v2's gathers staged AD k-blocks ahead through cp.async unless engine 6
 inline bool tc2_async_gather_enabled() { return g_gemm_engine != 6; }
+// engine 7 (opt-in): weight gradients over 16-aligned pixel rows stream the
+// raw dY by TMA (mode kWgradTma, no dY pack).  Measured neutral in the
+// GoogLeNet step (9700 img/s either way) and 5% slower for conv1 alone: the
+// producers, already issue-bound on the gather, also split the B tile
+inline bool tc2_wgrad_tma_enabled() { return g_gemm_engine == 7; }
 
 }  // namespace bf

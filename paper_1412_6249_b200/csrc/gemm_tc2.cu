@@ -328,7 +328,10 @@ inline void divmagic(uint32_t d, uint64_t& m, int& s) {
 // MODE: 0 generic table gather, 1 channel-chunk fast path (fwd / dgrad),
 //       2 / 3 weight-gradient pixel-row fast path with 16- / 8-wide chunks
 //       4 TMA-fed 1x1 weight gradient (both operands K-major NCHW tiles, no pack)
-enum { kGeneric = 0, kChannel = 1, kWgrad16 = 2, kWgrad8 = 3, kTma1x1 = 4 };
+//       5 weight gradient with the kWgrad16 gather for A and the raw dY tile
+//         streamed by TMA for B (small part split in-kernel, no dY pack):
+//         pixel rows exactly 16-aligned and images a whole number of k-blocks
+enum { kGeneric = 0, kChannel = 1, kWgrad16 = 2, kWgrad8 = 3, kTma1x1 = 4, kWgradTma = 5 };
 
 // q = x / d, r = x % d, with the (common, warp-uniform) d == 1 case free
 __device__ __forceinline__ void divmod_u(int x, int d, int& q, int& r) {
@@ -480,7 +483,7 @@ __device__ __forceinline__ void gather16_to(const LA& la, const Work& w, const R
                                             const RowInfo& ri, int kbase, int kc0,
                                             const float* __restrict__ pa, unsigned hb,
                                             unsigned wb, const Sink& out) {
-  if (MODE == kWgrad16)
+  if (MODE == kWgrad16 || MODE == kWgradTma)
     gather16_wgrad<16>(la, w, ri, kbase + kc0, pa, out);
   else if (MODE == kWgrad8)
     gather16_wgrad<8>(la, w, ri, kbase + kc0, pa, out);
@@ -737,12 +740,32 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       for (int d = 0; d < (AD > 0 ? AD : 1); ++d) issue(d);
       int pstage = 0, slot = 0;
       uint32_t pphase = 0;
-      int nk;
-      {
-        int mt2, nt2, sp2;
-        unit_coords(w, u, mt2, nt2, sp2);
-        nk = min(w.kbps, w.nkb - sp2 * w.kbps);
-      }
+      int nk, cmt, cnt_, csp;
+      unit_coords(w, u, cmt, cnt_, csp);
+      nk = min(w.kbps, w.nkb - csp * w.kbps);
+      // kWgradTma: the B stage holds the raw dY tile (TMA); the producers
+      // write its small part next to it and, for m-tile 0, sum it per row
+      // into the bias partials (as in kTma1x1)
+      const int nb = BN / 32;
+      float bsum[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bsum[j] = 0.f;
+      auto flush_bias = [&]() {
+        if (MODE == kWgradTma && bias_part != nullptr && cmt == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < nb) {
+              float a = bsum[j];
+              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
+              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
+              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 4));
+              const int row = cnt_ * BN + (t >> 3) + 32 * j;
+              if ((t & 7) == 0 && row < w.N) bias_part[(size_t)row * w.splits + csp] = a;
+              bsum[j] = 0.f;
+            }
+          }
+        }
+      };
       while (true) {
         asm volatile("cp.async.wait_group %0;" ::"n"(AD > 0 ? AD - 1 : 0) : "memory");
         float big[16], small[16];
@@ -759,6 +782,29 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           pstage = 0;
           pphase ^= 1;
         }
+        if constexpr (MODE == kWgradTma) {
+          mbar_wait(&bfull[stage], phase);  // the raw dY tile of this k-block landed
+          uint8_t* sb = tiles + stage * sstride;
+          const float4* braw = reinterpret_cast<const float4*>(sb);
+          float4* bsm = reinterpret_cast<float4*>(sb + BN * 128);
+          const bool do_bias = bias_part != nullptr && cmt == 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < nb) {
+              const int f = t + kProducers * j;
+              const float4 v = braw[f];
+              float4 r;
+              r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+              r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+              r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+              r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+              bsm[f] = r;
+              if (do_bias)
+                bsum[j] = __fadd_rn(bsum[j], __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t acol = w.abase + stage * 64 + kc0;
         tmem_st16(lane_addr + acol, big);
@@ -767,12 +813,12 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         tc_fence_before();
         mbar_arrive(&full[stage]);
         if (++i >= nk) {
+          flush_bias();
           u += gridDim.x;
           i = 0;
           if (u >= w.units) break;
-          int mt2, nt2, sp2;
-          unit_coords(w, u, mt2, nt2, sp2);
-          nk = min(w.kbps, w.nkb - sp2 * w.kbps);
+          unit_coords(w, u, cmt, cnt_, csp);
+          nk = min(w.kbps, w.nkb - csp * w.kbps);
         }
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
@@ -963,7 +1009,28 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     // streams the pre-packed B tiles of every (unit, k-block) into the B ring
     // as far ahead as the ring allows: the TMA latency leaves the per-stage
     // critical path of the producers
-    if (MODE == kTma1x1 && lane == 0) {
+    if (MODE == kWgradTma && lane == 0) {
+      // raw dy tile (BN rows x 32 pixels) of each k-block; k-blocks never
+      // straddle images (launch_wgrad_tma checks PQ % 32 == 0)
+      int bst = 0;
+      uint32_t bphase = 0;
+      for (int u = blockIdx.x; u < w.units; u += gridDim.x) {
+        int mt, nt, sp;
+        unit_coords(w, u, mt, nt, sp);
+        const int kb0 = sp * w.kbps;
+        const int nk = min(w.kbps, w.nkb - kb0);
+        for (int i = 0; i < nk; ++i) {
+          mbar_wait(&TC2_BRELEASE[bst], bphase ^ 1);
+          mbar_arrive_expect_tx(&bfull[bst], (uint32_t)(BN * 128));
+          const int kb = kb0 + i, img = kb / w.cpi, pix = (kb - img * w.cpi) * BK;
+          tma_load_3d(smem_u32(tiles + bst * sstride), &bmap, pix, nt * BN, img, &bfull[bst]);
+          if (++bst == w.nbst) {
+            bst = 0;
+            bphase ^= 1;
+          }
+        }
+      }
+    } else if (MODE == kTma1x1 && lane == 0) {
       // raw dy tile (BN rows) and x tile (BM rows) of one 32-pixel k-block
       int bst = 0;
       uint32_t bphase = 0;
@@ -1203,6 +1270,91 @@ inline int pick_bn_tma(int N, int& ntiles) {  // <= 192: >= 3 ring stages of 64 
   return (per + 31) / 32 * 32;
 }
 
+// weight gradient, mode kWgradTma (conv1: 3x224x224 -> 64 x 112x112, 7x7/2):
+// M = C*R*S rows gathered from x (kWgrad16 + cp.async staging), B = the raw
+// dY tile streamed by TMA -- no dY pack pass (which read dY and wrote twice
+// its size) and half the B bytes in the GEMM.  Needs Q % 16 == 0 (the
+// pixel-row K order has no padding) and P*Q % 32 == 0 (k-blocks stay inside
+// one image).
+int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi, float* ws,
+                     int64_t ws_bytes, cudaStream_t st, const char* what, float* bias_out) {
+  const ConvShape& g = la.g;
+  const int PQ = g.P * g.Q, imgs = g.N, Kout = g.K;
+  if (g.Q % 16 || PQ % 32 || (reinterpret_cast<uintptr_t>(dy) & 15)) return -1;
+  Work w{};
+  w.M = M;
+  w.N = Kout;
+  w.cpi = PQ / BK;
+  w.nkb = imgs * w.cpi;
+  w.K = w.nkb * BK;
+  w.Pp = g.P;
+  w.Qp = g.Q;
+  divmagic((uint32_t)(w.Pp * w.Qp), w.per_m, w.per_s);
+  divmagic((uint32_t)w.Qp, w.qp_m, w.qp_s);
+  w.BN = pick_bn_tma(Kout, w.ntiles);
+  w.mtiles = (M + BM - 1) / BM;
+  w.nacc = w.BN <= 128 ? 2 : 1;
+  w.accs = w.BN;
+  w.abase = (w.nacc * w.BN + 63) / 64 * 64;
+  w.nst = std::min<int>(TC2_MAX_NST, (512 - w.abase) / 64);
+  w.sstride = 2 * w.BN * 128;
+  w.full_ktab = 0;
+  CUtensorMap bmap;
+  if (!make_nchw_map(&bmap, dy, PQ, Kout, imgs, w.BN, CU_TENSOR_MAP_SWIZZLE_128B)) return -1;
+  // workspace: [bias partials: Kout x <= 256 splits][split-K partials]
+  const int64_t bias_bytes = bias_out ? ((int64_t)Kout * 256 * 4 + 1023) / 1024 * 1024 : 0;
+  if (!ws || ws_bytes < bias_bytes) return -1;
+  float* bias_ws = bias_out ? ws : nullptr;
+  float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + bias_bytes);
+  const int64_t part_bytes = ws_bytes - bias_bytes;
+  const int sms = gemm_sm_budget();
+  w.splits = 1;
+  {
+    const int64_t tiles = (int64_t)w.mtiles * w.ntiles;
+    if (tiles < sms) {
+      const int64_t want = sms / tiles;
+      const int64_t by_k = w.nkb / 4;
+      const int64_t by_ws = part_bytes / ((int64_t)M * Kout * 4);
+      w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
+                                                   std::min<int64_t>(by_ws, 256)));
+    }
+  }
+  w.kbps = (w.nkb + w.splits - 1) / w.splits;
+  w.splits = (w.nkb + w.kbps - 1) / w.kbps;
+  w.units = w.mtiles * w.ntiles * w.splits;
+  constexpr int AD = 4;
+  const int smem_cap = 227 * 1024;
+  const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
+  const int ktab_bytes = STAGES * BK * 8;
+  const int stg_bytes = AD * 16 * kProducers * 4;
+  w.nbst = std::min(kBStagesMax, (smem_cap - tail - ktab_bytes - stg_bytes) / w.sstride);
+  if (TC2_ONE_COMMIT) w.nst = w.nbst = std::min(w.nst, w.nbst);
+  if (w.nbst < 2) return -1;
+  const int smem = std::max(tail + w.nbst * w.sstride + stg_bytes + ktab_bytes, 120 << 10);
+  auto kern = tc2_kernel<LdWgradX, EpiT, kWgradTma, AD>;
+  static bool configured = false;
+  if (!configured) {
+    BF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_cap),
+            "tc2 smem attribute");
+    configured = true;
+  }
+  const int grid = std::min(w.units, sms);
+  EpiPartial part{part_ws, M, Kout};
+  const CUtensorMap nomap{};
+  kern<<<grid, kAllThreads, smem, st>>>(la, w, nullptr, epi, part, nomap, bmap, bias_ws);
+  if (int rc = check_launch(what)) return rc;
+  if (w.splits > 1) {
+    splitk_reduce_kernel<EpiT><<<elementwise_grid((int64_t)M * Kout, 256), 256, 0, st>>>(
+        part_ws, w.splits, M, Kout, epi);
+    if (int rc = check_launch(what)) return rc;
+  }
+  if (bias_out) {
+    bias_blocks_finish_kernel<<<Kout, 256, 0, st>>>(bias_ws, w.splits, bias_out);
+    return check_launch(what);
+  }
+  return 0;
+}
+
 int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, int Kout, int PQ,
                   int imgs, const EpiT& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
                   const char* what, float* bias_out) {
@@ -1297,6 +1449,14 @@ int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
       tc2_tma_wgrad_enabled()) {
     const int rc = tc2::launch_tma1x1(la, la.x, lb.dy, g.C, g.K, g.H * g.W, g.N, epi, ws,
                                       ws_bytes, st, what, db);
+    if (rc == 0) {
+      if (db_done) *db_done = db != nullptr;
+      return 0;
+    }
+    if (rc > 0) return rc;
+  }
+  if (tc2_wgrad_tma_enabled() && g.Q % 16 == 0 && (g.P * g.Q) % 32 == 0) {
+    const int rc = tc2::launch_wgrad_tma(la, lb.dy, M, epi, ws, ws_bytes, st, what, db);
     if (rc == 0) {
       if (db_done) *db_done = db != nullptr;
       return 0;

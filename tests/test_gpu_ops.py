@@ -48,18 +48,21 @@ CONV_CASES = [
     (2, 256, 28, 28, 384, 1, 1, 0, False),        # 1x1, two output-channel tiles
     (2, 5, 19, 17, 24, 7, 1, 3, False),           # 7x7 stride 1 on 5 channels
     (1, 2, 16, 16, 40, 8, 3, 2, False),           # 8x8 stride 3
+    (2, 8, 32, 32, 256, 3, 1, 1, False),          # TMA-streamed dY wgrad, two dY tiles
 ]
 
 
-@pytest.fixture(params=[0, 3, 4, 5, 6],
-                ids=["auto", "halo-v3", "no-tma-1x1", "no-tma-wgrad", "reg-prefetch"])
+@pytest.fixture(params=[0, 3, 4, 5, 6, 7],
+                ids=["auto", "halo-v3", "no-tma-1x1", "no-tma-wgrad", "reg-prefetch",
+                     "tma-dy-wgrad"])
 def gemm_engine(request):
     """0 = default engine choice (1x1 convolutions through the TMA-fed engine
     v4, gemm_tc4.cu); 3 = also route stride-1 R x S convolutions through the
     opt-in halo-staged engine v3 (gemm_tc3.cu); 4 = 1x1 convolutions through
     the gathering engine v2 instead of v4; 5 = 1x1 weight gradients gathered
     instead of TMA-fed; 6 = engine v2 gathers prefetched in registers instead
-    of cp.async-staged."""
+    of cp.async-staged; 7 = also stream the raw dY by TMA for 16-aligned-row
+    weight gradients (conv1 type, opt-in mode kWgradTma)."""
     from paper_1412_6249_b200 import _native
 
     lib = _native.lib()
