@@ -87,6 +87,11 @@ int bf_sgd_momentum(const float* w, const float* g, const float* v, float* w_new
 /* lowered aggregate(mean)+sgd_update (builders.py:589-603): out = w - f32(lr)*(gsum/f32(k)) */
 int bf_sgd_mean_update(const float* w, const float* gsum, float* out, float lr, int k,
                        int64_t n, bf_stream_t stream);
+/* lowered aggregate(mean)+sgd_momentum on one shard of the exchange (builders.py:
+   581-611 with the momentum extension): v' = mu*v + lr*(gsum/f32(k)); w' = w - v' */
+int bf_sgd_mean_momentum(const float* w, const float* gsum, const float* v, float* w_new,
+                         float* v_new, float lr, float momentum, int k, int64_t n,
+                         bf_stream_t stream);
 /* aggregate, ops.py:440-457: rank-ordered sum of k parts (k <= 32); mean divides by f32(k) */
 int bf_aggregate(const float* const* parts, int k, float* out, int64_t n, int mean,
                  bf_stream_t stream);

@@ -42,6 +42,7 @@ _SIGS = {
     "bf_sgd_update": [_p, _p, _p, _f, _l, _p],
     "bf_sgd_momentum": [_p, _p, _p, _p, _p, _f, _f, _l, _p],
     "bf_sgd_mean_update": [_p, _p, _p, _f, _i, _l, _p],
+    "bf_sgd_mean_momentum": [_p, _p, _p, _p, _p, _f, _f, _i, _l, _p],
     "bf_aggregate": [_p, _i, _p, _l, _i, _p],
     "bf_copy": [_p, _i, _p, _i, _l, _p],
     "bf_check_finite": [_p, _l, _p, _p],

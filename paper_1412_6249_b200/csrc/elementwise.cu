@@ -4,6 +4,7 @@
 // reference exactly (no FMA contraction: every product is rounded before the
 // add), so these kernels are bit-identical to the numpy reference.
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include <atomic>
 
@@ -31,6 +32,14 @@ int gemm_sm_budget() {
   const int sms = sm_count_current();
   const int r = g_sm_reserve.load(std::memory_order_relaxed);
   return sms - r >= 1 ? sms - r : 1;
+}
+
+int max_chain_kb() {
+  static const int v = [] {
+    const char* e = getenv("PURINE_B200_MAX_CHAIN_KB");
+    return e && *e ? atoi(e) : 32;
+  }();
+  return v;
 }
 
 int sm_count_current() {
@@ -136,22 +145,64 @@ __global__ void sgd_scalar(const float* __restrict__ w, const float* __restrict_
     out[i] = sgd1(w[i], g[i], lr);
 }
 
-__global__ void sgd_momentum_kernel(const float* __restrict__ w, const float* __restrict__ g,
-                                    const float* __restrict__ v, float* __restrict__ w_new,
-                                    float* __restrict__ v_new, float lr, float mu, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float vn = __fadd_rn(__fmul_rn(mu, v[i]), __fmul_rn(lr, g[i]));
-    v_new[i] = vn;
-    w_new[i] = __fsub_rn(w[i], vn);
+// SGD family over float4 lanes (the 4-aligned body) plus a scalar tail.
+// One functor per update rule keeps the vector and scalar paths identical.
+// The lowered exchange divides the reduce-scattered gradient SUM by f32(k)
+// (aggregate mean, ops.py:454-455: a true division, not a reciprocal
+// multiply) before the update, so at k = 1 it is bitwise the plain rule.
+struct MeanSgd {
+  float lr, k;
+  __device__ __forceinline__ void operator()(float w, float g, float, float& wn, float&) const {
+    wn = __fsub_rn(w, __fmul_rn(lr, __fdiv_rn(g, k)));
+  }
+};
+// Caffe momentum (oracle sgd_momentum): v' = mu*v + lr*g; w' = w - v'
+struct MeanMomentum {
+  float lr, mu, k;
+  __device__ __forceinline__ void operator()(float w, float g, float v, float& wn,
+                                             float& vn) const {
+    vn = __fadd_rn(__fmul_rn(mu, v), __fmul_rn(lr, __fdiv_rn(g, k)));
+    wn = __fsub_rn(w, vn);
+  }
+};
+
+template <class Rule, bool kVel>
+__global__ void sgd_family_kernel(const float* __restrict__ w, const float* __restrict__ g,
+                                  const float* __restrict__ v, float* __restrict__ w_new,
+                                  float* __restrict__ v_new, int64_t n4, int64_t n, Rule rule) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < n4; i += stride) {
+    const float4 a = reinterpret_cast<const float4*>(w)[i];
+    const float4 b = reinterpret_cast<const float4*>(g)[i];
+    float4 c = make_float4(0.f, 0.f, 0.f, 0.f), wn, vn;
+    if (kVel) c = reinterpret_cast<const float4*>(v)[i];
+    rule(a.x, b.x, c.x, wn.x, vn.x);
+    rule(a.y, b.y, c.y, wn.y, vn.y);
+    rule(a.z, b.z, c.z, wn.z, vn.z);
+    rule(a.w, b.w, c.w, wn.w, vn.w);
+    reinterpret_cast<float4*>(w_new)[i] = wn;
+    if (kVel) reinterpret_cast<float4*>(v_new)[i] = vn;
+  }
+  for (int64_t i = 4 * n4 + t0; i < n; i += stride) {
+    float wn, vn;
+    rule(w[i], g[i], kVel ? v[i] : 0.f, wn, vn);
+    w_new[i] = wn;
+    if (kVel) v_new[i] = vn;
   }
 }
 
-__global__ void sgd_mean_kernel(const float* __restrict__ w, const float* __restrict__ gsum,
-                                float* __restrict__ out, float lr, float k, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = __fsub_rn(w[i], __fmul_rn(lr, __fdiv_rn(gsum[i], k)));
+template <class Rule, bool kVel>
+int launch_sgd_family(const float* w, const float* g, const float* v, float* w_new, float* v_new,
+                      int64_t n, Rule rule, cudaStream_t st, const char* what) {
+  if (n <= 0) return 0;
+  bool vec = aligned16(w) && aligned16(g) && aligned16(w_new);
+  if (kVel) vec = vec && aligned16(v) && aligned16(v_new);
+  const int64_t n4 = vec ? n / 4 : 0;
+  const int64_t items = n4 + (n - 4 * n4);
+  sgd_family_kernel<Rule, kVel><<<elementwise_grid(items, kThreads), kThreads, 0, st>>>(
+      w, g, v, w_new, v_new, n4, n, rule);
+  return check_launch(what);
 }
 
 struct Parts {
@@ -363,19 +414,26 @@ int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t 
 
 int bf_sgd_momentum(const float* w, const float* g, const float* v, float* w_new, float* v_new,
                     float lr, float momentum, int64_t n, bf_stream_t s) {
-  if (n <= 0) return 0;
-  sgd_momentum_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(
-      w, g, v, w_new, v_new, lr, momentum, n);
-  return check_launch("sgd_momentum");
+  return launch_sgd_family<MeanMomentum, true>(w, g, v, w_new, v_new, n,
+                                               MeanMomentum{lr, momentum, 1.f}, as_stream(s),
+                                               "sgd_momentum");
 }
 
 int bf_sgd_mean_update(const float* w, const float* gsum, float* out, float lr, int k,
                        int64_t n, bf_stream_t s) {
-  if (n <= 0) return 0;
   BF_REQUIRE(k >= 1, "sgd_mean_update: k must be >= 1");
-  sgd_mean_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(
-      w, gsum, out, lr, (float)k, n);
-  return check_launch("sgd_mean_update");
+  return launch_sgd_family<MeanSgd, false>(w, gsum, nullptr, out, nullptr, n,
+                                           MeanSgd{lr, (float)k}, as_stream(s),
+                                           "sgd_mean_update");
+}
+
+int bf_sgd_mean_momentum(const float* w, const float* gsum, const float* v, float* w_new,
+                         float* v_new, float lr, float momentum, int k, int64_t n,
+                         bf_stream_t s) {
+  BF_REQUIRE(k >= 1, "sgd_mean_momentum: k must be >= 1");
+  return launch_sgd_family<MeanMomentum, true>(w, gsum, v, w_new, v_new, n,
+                                               MeanMomentum{lr, momentum, (float)k},
+                                               as_stream(s), "sgd_mean_momentum");
 }
 
 int bf_aggregate(const float* const* parts, int k, float* out, int64_t n, int mean,

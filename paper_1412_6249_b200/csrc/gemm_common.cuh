@@ -18,6 +18,8 @@
 // loader's thread mapping (kMContig).
 #pragma once
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace bf {
@@ -245,6 +247,106 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     int n = (int)(i / M), m = (int)(i - (int64_t)n * M);
     epi(m, n, acc);
   }
+}
+
+// many splits (chain-bounded weight gradients): thread (quad, g) sums the
+// float4 of outputs [4*quad, 4*quad + 4) over splits g, g + G, g + 2G, ... in
+// order (4 loads in flight per step), then the g = 0 threads add the G group
+// sums in order -- a fixed summation tree, so the result is deterministic.
+// G (a power of two <= 32) is sized so that even a small output (conv1's
+// 9.4k weights over ~800 splits) keeps every SM streaming.
+template <class Epi>
+__global__ void __launch_bounds__(256) splitk_reduce_vec_kernel(const float* __restrict__ ws,
+                                                                int splits, int M, int N, int G,
+                                                                Epi epi) {
+  __shared__ float4 part[256];
+  const int64_t total = (int64_t)M * N, quads = total / 4;
+  const int Q = 256 / G;
+  const int t = threadIdx.x, quad_l = t % Q, g = t / Q;
+  const float4* w4 = reinterpret_cast<const float4*>(ws);
+  for (int64_t qb = (int64_t)blockIdx.x * Q; qb < quads; qb += (int64_t)gridDim.x * Q) {
+    const int64_t quad = qb + quad_l;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (quad < quads && g < splits) {
+      acc = w4[(int64_t)g * quads + quad];
+      int s = g + G;
+      for (; s + 3 * G < splits; s += 4 * G) {
+        const float4 a = w4[(int64_t)s * quads + quad];
+        const float4 b = w4[(int64_t)(s + G) * quads + quad];
+        const float4 c = w4[(int64_t)(s + 2 * G) * quads + quad];
+        const float4 d = w4[(int64_t)(s + 3 * G) * quads + quad];
+        acc.x = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc.x, a.x), b.x), c.x), d.x);
+        acc.y = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc.y, a.y), b.y), c.y), d.y);
+        acc.z = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc.z, a.z), b.z), c.z), d.z);
+        acc.w = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(acc.w, a.w), b.w), c.w), d.w);
+      }
+      for (; s < splits; s += G) {
+        const float4 a = w4[(int64_t)s * quads + quad];
+        acc.x = __fadd_rn(acc.x, a.x);
+        acc.y = __fadd_rn(acc.y, a.y);
+        acc.z = __fadd_rn(acc.z, a.z);
+        acc.w = __fadd_rn(acc.w, a.w);
+      }
+    }
+    if (G > 1) {
+      part[t] = acc;
+      __syncthreads();
+      if (g == 0)
+        for (int q = 1; q < G && q < splits; ++q) {
+          const float4 a = part[q * Q + quad_l];
+          acc.x = __fadd_rn(acc.x, a.x);
+          acc.y = __fadd_rn(acc.y, a.y);
+          acc.z = __fadd_rn(acc.z, a.z);
+          acc.w = __fadd_rn(acc.w, a.w);
+        }
+      __syncthreads();
+    }
+    if (g == 0 && quad < quads) {
+      const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t i = 4 * quad + j;
+        const int n = (int)(i / M), m = (int)(i - (int64_t)n * M);
+        epi(m, n, v[j]);
+      }
+    }
+  }
+}
+
+// launch the split-K reduction that suits the split count
+template <class Epi>
+inline void splitk_reduce(const float* ws, int splits, int M, int N, const Epi& epi,
+                          cudaStream_t st) {
+  const int64_t total = (int64_t)M * N;
+  if (splits >= 8 && total % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0) {
+    const int64_t quads = total / 4;
+    const int64_t want = (int64_t)sm_count_current() * 2048;
+    int G = 1;
+    while (G < 32 && G < splits && quads * G < want) G *= 2;
+    const int Q = 256 / G;
+    const int64_t blocks = (quads + Q - 1) / Q;
+    const int grid = (int)std::min<int64_t>(blocks, (int64_t)sm_count_current() * 8);
+    splitk_reduce_vec_kernel<Epi><<<grid, 256, 0, st>>>(ws, splits, M, N, G, epi);
+  } else {
+    splitk_reduce_kernel<Epi><<<elementwise_grid(total, 256), 256, 0, st>>>(ws, splits, M, N,
+                                                                            epi);
+  }
+}
+
+// Tensor-core accumulation is not round-to-nearest: tcgen05.mma rounds each
+// instruction's fp32 sum toward zero, so a reduction chain of L k-blocks (12
+// kind::tf32 MMAs each under 3xTF32) shrinks its result by ~2e-7 * L
+// (tools/precision_probe.py; profiles/r02_precision.md).  Weight gradients
+// reduce over K = N*P*Q (401k at GoogLeNet's 56x56 layers, batch 128), so
+// their K loop is split into chains of at most max_chain_kb() k-blocks whose
+// partials are summed in fp32 round-to-nearest by the split-K reduction.
+// PURINE_B200_MAX_CHAIN_KB overrides the default of 32 (1024 elements); 0
+// disables the bound.
+constexpr int kMaxSplits = 4096;
+int max_chain_kb();
+inline int64_t chain_min_splits(int64_t nkb) {
+  const int c = max_chain_kb();
+  return c > 0 ? (nkb + c - 1) / c : 1;
 }
 
 enum GemmOp { kConvFwd = 0, kConvDgrad = 1, kConvWgrad = 2, kFcFwd = 3, kFcDgrad = 4, kFcWgrad = 5 };

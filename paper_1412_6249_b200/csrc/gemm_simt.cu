@@ -88,8 +88,7 @@ int simt_gemm(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, f
   simt_gemm_kernel<LA, LB, Epi><<<grid, NT, 0, st>>>(la, lb, M, N, K, kps, epi, part, splits);
   if (int rc = check_launch(what)) return rc;
   if (splits > 1) {
-    splitk_reduce_kernel<Epi><<<elementwise_grid((int64_t)M * N, 256), 256, 0, st>>>(
-        ws, splits, M, N, epi);
+    splitk_reduce<Epi>(ws, splits, M, N, epi, st);
     return check_launch(what);
   }
   return 0;

@@ -498,8 +498,7 @@ int launch(const LA& la, const LB& lb, int M, int N, int K, const Epi& epi, floa
   kern<<<grid, kThreads, L::kTotal, st>>>(la, lb, M, N, K, kbps, epi, part, splits);
   if (int rc = check_launch(what)) return rc;
   if (splits > 1) {
-    splitk_reduce_kernel<Epi><<<elementwise_grid((int64_t)M * N, 256), 256, 0, st>>>(
-        ws, splits, M, N, epi);
+    splitk_reduce<Epi>(ws, splits, M, N, epi, st);
     return check_launch(what);
   }
   return 0;

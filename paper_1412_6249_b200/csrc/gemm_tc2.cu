@@ -460,16 +460,14 @@ __device__ __forceinline__ void gather16_wgrad(const LA& la, const Work& w, cons
   }
 }
 
-// A operand split for 3xTF32.  The tensor core reads a kind::tf32 operand's
-// fp32 bit pattern and ignores the 13 low mantissa bits, so the truncated
-// value trunc(x) is implicit: big = x as is, small = x - trunc(x) (exact in
-// fp32; its own low bits are dropped by the MMA in turn).  |x - big - small| <=
-// 2^-20 |x| (vs 2^-22 with round-to-nearest splitting, which costs 3 more
-// integer ops per element on the producers' critical path).
+// A operand split for 3xTF32: big = x as is (the MMA reads it as trunc(x)),
+// small = tf32_small(x) (tc_ptx.cuh: x - trunc(x), rounded to nearest by the
+// MMA's own truncation).  TC2_TRUNC_SPLIT=0 selects the explicit
+// round-to-nearest split (2 more integer ops per element).
 __device__ __forceinline__ void split_tf32(float x, float& big, float& small) {
 #if TC2_TRUNC_SPLIT
   big = x;
-  small = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  small = tf32_small(x);
 #else
   big = to_tf32_rna(x);
   small = to_tf32_rna(x - big);
@@ -623,11 +621,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
             if (j < nb) {
               const int f = t + kProducers * j;
               const float4 v = braw[f];
-              float4 r;
-              r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-              r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-              r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-              r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+              const float4 r = tf32_small4(v);
               bsm[f] = r;
               if (do_bias)
                 bsum[j] = __fadd_rn(bsum[j], __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
@@ -793,11 +787,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
             if (j < nb) {
               const int f = t + kProducers * j;
               const float4 v = braw[f];
-              float4 r;
-              r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-              r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-              r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-              r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+              const float4 r = tf32_small4(v);
               bsm[f] = r;
               if (do_bias)
                 bsum[j] = __fadd_rn(bsum[j], __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
@@ -1188,10 +1178,15 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
     const bool wgrad_pack = std::is_same_v<LBP, LdWgradDYPad>;
     if (tiles < sms && (wgrad_pack || tiles < TC2_NOSPLIT_MIN_TILES)) {
       int64_t want = sms / tiles;  // one wave: units <= SMs (ceil would leave a 2-unit tail)
+      if (wgrad_pack) want = std::max(want, chain_min_splits(w.nkb));
       int64_t by_k = w.nkb / 4;
       int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
       w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                   std::min<int64_t>(by_ws, 256)));
+                                                   std::min<int64_t>(by_ws, kMaxSplits)));
+    } else if (wgrad_pack) {  // many tiles: split only as far as the chain bound needs
+      const int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
+      w.splits = (int)std::max<int64_t>(1, std::min(chain_min_splits(w.nkb),
+                                                   std::min<int64_t>(by_ws, kMaxSplits)));
     }
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
@@ -1248,8 +1243,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   kern<<<grid, kAllThreads, smem_req, st>>>(la, w, bpack, epi, part, nomap, nomap, nullptr);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
-    splitk_reduce_kernel<Epi><<<elementwise_grid((int64_t)M * N, 256), 256, 0, st>>>(
-        part_ws, w.splits, M, N, epi);
+    splitk_reduce<Epi>(part_ws, w.splits, M, N, epi, st);
     if (int rc = check_launch(what)) return rc;
   }
   if (bias_out) {
@@ -1301,8 +1295,8 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
   w.full_ktab = 0;
   CUtensorMap bmap;
   if (!make_nchw_map(&bmap, dy, PQ, Kout, imgs, w.BN, CU_TENSOR_MAP_SWIZZLE_128B)) return -1;
-  // workspace: [bias partials: Kout x <= 256 splits][split-K partials]
-  const int64_t bias_bytes = bias_out ? ((int64_t)Kout * 256 * 4 + 1023) / 1024 * 1024 : 0;
+  // workspace: [bias partials: Kout x <= kMaxSplits splits][split-K partials]
+  const int64_t bias_bytes = bias_out ? ((int64_t)Kout * kMaxSplits * 4 + 1023) / 1024 * 1024 : 0;
   if (!ws || ws_bytes < bias_bytes) return -1;
   float* bias_ws = bias_out ? ws : nullptr;
   float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + bias_bytes);
@@ -1311,12 +1305,13 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
   w.splits = 1;
   {
     const int64_t tiles = (int64_t)w.mtiles * w.ntiles;
-    if (tiles < sms) {
-      const int64_t want = sms / tiles;
-      const int64_t by_k = w.nkb / 4;
+    {
+      const int64_t want = std::max<int64_t>(tiles < sms ? sms / tiles : 1,
+                                             chain_min_splits(w.nkb));
+      const int64_t by_k = std::max<int64_t>(1, w.nkb / 4);
       const int64_t by_ws = part_bytes / ((int64_t)M * Kout * 4);
       w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                   std::min<int64_t>(by_ws, 256)));
+                                                   std::min<int64_t>(by_ws, kMaxSplits)));
     }
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
@@ -1344,8 +1339,7 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
   kern<<<grid, kAllThreads, smem, st>>>(la, w, nullptr, epi, part, nomap, bmap, bias_ws);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
-    splitk_reduce_kernel<EpiT><<<elementwise_grid((int64_t)M * Kout, 256), 256, 0, st>>>(
-        part_ws, w.splits, M, Kout, epi);
+    splitk_reduce<EpiT>(part_ws, w.splits, M, Kout, epi, st);
     if (int rc = check_launch(what)) return rc;
   }
   if (bias_out) {
@@ -1378,8 +1372,8 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
   if (!make_nchw_map(&amap, x, PQ, C, imgs, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_nchw_map(&bmap, dy, PQ, Kout, imgs, w.BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return -1;
-  // workspace: [bias partials: Kout x <= 256 splits][split-K partials]
-  const int64_t bias_bytes = bias_out ? ((int64_t)Kout * 256 * 4 + 1023) / 1024 * 1024 : 0;
+  // workspace: [bias partials: Kout x <= kMaxSplits splits][split-K partials]
+  const int64_t bias_bytes = bias_out ? ((int64_t)Kout * kMaxSplits * 4 + 1023) / 1024 * 1024 : 0;
   if (!ws || ws_bytes < bias_bytes) return -1;
   float* bias_ws = bias_out ? ws : nullptr;
   float* part_ws = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ws) + bias_bytes);
@@ -1388,12 +1382,13 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
   w.splits = 1;
   {
     const int64_t tiles = (int64_t)w.mtiles * w.ntiles;
-    if (tiles < sms) {
-      const int64_t want = sms / tiles;
-      const int64_t by_k = w.nkb / 4;
+    {
+      const int64_t want = std::max<int64_t>(tiles < sms ? sms / tiles : 1,
+                                             chain_min_splits(w.nkb));
+      const int64_t by_k = std::max<int64_t>(1, w.nkb / 4);
       const int64_t by_ws = part_bytes / ((int64_t)C * Kout * 4);
       w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                   std::min<int64_t>(by_ws, 256)));
+                                                   std::min<int64_t>(by_ws, kMaxSplits)));
     }
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
@@ -1418,8 +1413,7 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
   kern<<<grid, kAllThreads, smem, st>>>(la, w, nullptr, epi, part, amap, bmap, bias_ws);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
-    splitk_reduce_kernel<EpiT><<<elementwise_grid((int64_t)C * Kout, 256), 256, 0, st>>>(
-        part_ws, w.splits, C, Kout, epi);
+    splitk_reduce<EpiT>(part_ws, w.splits, C, Kout, epi, st);
     if (int rc = check_launch(what)) return rc;
   }
   if (bias_out) {

@@ -381,8 +381,7 @@ int launch(const Halo& h, const LdHaloW& lbp, int Nout, const EpiNCHW& epi, floa
   tc3_kernel<EpiNCHW><<<grid, kAllThreads, smem_req, st>>>(h, w, bpack, epi, part);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
-    splitk_reduce_kernel<EpiNCHW><<<elementwise_grid((int64_t)Mreal * Nout, 256), 256, 0, st>>>(
-        part_ws, w.splits, Mreal, Nout, epi);
+    splitk_reduce<EpiNCHW>(part_ws, w.splits, Mreal, Nout, epi, st);
     return check_launch(what);
   }
   return 0;

@@ -187,11 +187,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
         for (int q = 0; q < kABytes / 16 / (kSplitWarps * 32); ++q) {
           const float4 v = src[q * kSplitWarps * 32 + t];
-          float4 r;
-          r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-          r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-          r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-          r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+          const float4 r = tf32_small4(v);
           dst[q * kSplitWarps * 32 + t] = r;
         }
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
@@ -388,8 +384,7 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
   tc4_kernel<EpiNCHW><<<grid, kThreads, smem, st>>>(amap, w, bpack, epi, part);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
-    splitk_reduce_kernel<EpiNCHW><<<elementwise_grid((int64_t)M * Nout, 256), 256, 0, st>>>(
-        part_ws, w.splits, M, Nout, epi);
+    splitk_reduce<EpiNCHW>(part_ws, w.splits, M, Nout, epi, st);
     return check_launch(what);
   }
   return 0;

@@ -164,6 +164,28 @@ __device__ __forceinline__ uint32_t tf32_idesc(int bn) {
 __device__ __forceinline__ float to_tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// Small part of the implicit 3xTF32 split of a raw fp32 operand.  The tensor
+// core reads a kind::tf32 operand's fp32 bits and ignores the 13 low mantissa
+// bits, so big = x as is stands for trunc(x), and s = x - trunc(x) is exact in
+// fp32.  The MMA then truncates s in turn; that error always has the sign of
+// x (|A| shrinks by up to 2^-20 |x|), a coherent bias that adds up over long
+// reductions and network depth.  TF32_SMALL_RNA (default) adds half a TF32
+// ulp to s's magnitude bits so the MMA's truncation rounds s to nearest
+// instead: unbiased, error <= 2^-21 |x|, one integer add per element.
+#ifndef TF32_SMALL_RNA
+#define TF32_SMALL_RNA 1
+#endif
+__device__ __forceinline__ float tf32_small(float x) {
+  const float s = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+#if TF32_SMALL_RNA
+  return __uint_as_float(__float_as_uint(s) + 0x1000u);
+#else
+  return s;
+#endif
+}
+__device__ __forceinline__ float4 tf32_small4(float4 v) {
+  return make_float4(tf32_small(v.x), tf32_small(v.y), tf32_small(v.z), tf32_small(v.w));
+}
 __device__ __forceinline__ uint32_t sw_off(int r, int c) {
   return (uint32_t)(r * 128 + (((c ^ r) & 7) << 4));
 }

@@ -9,7 +9,9 @@ server subgraph by ``dp_exchange`` operators on the rank's upload lane, one
 per gradient *bucket*:
 
     ncclReduceScatter(sum, in place)  ->  fused mean + SGD on the owned shard
-    (bf_sgd_mean_update: w - lr * (g_sum / f32(world)))  ->  ncclAllGather
+    (bf_sgd_mean_update: w - lr * (g_sum / f32(world)), or with momentum
+    bf_sgd_mean_momentum: v' = mu*v + lr*(g_sum / f32(world)); w - v')
+    ->  ncclAllGather
 
 so each GPU is the parameter server for 1/world of every bucket ("gradient
 reduce and parameter broadcast sharded across the box", NS).  Buckets are
@@ -24,9 +26,22 @@ bucket to a multiple of 16*world), so a bucket is one contiguous range for
 NCCL and one launch for the update.  Swapping ``w`` <-> ``w_new`` views keeps
 the layout, so both CUDA-graph bindings see contiguous buckets.
 
+Momentum (the server's ``sgd_momentum`` + velocity swaps, builders.py
+581-611 with SPEC.md:312's extension): each rank keeps only the velocity of
+the shards it owns, one ``vxch_b{i}`` tensor per bucket (length
+flat_len / world) in a fourth and fifth flat arena, ping-ponged with
+``vxch_b{i}_new`` by the swap graph exactly like the parameters.
+
+Collectives go through ``store._collective`` (`NcclCollective` over an
+NCCL communicator, or `LocalGroup`: several ranks' stores on ONE device with
+the reduce-scatter / all-gather done by this library's own rank-ordered
+aggregate and copy kernels -- the single-GPU stand-in the tests use to run
+world-2 product code).
+
 Numerics: at world=1 the result is bitwise the reference's aggregate(mean)
-+ sgd_update; at world>1 NCCL's summation order differs from rank order, so
-parity is tolerance-based.
++ sgd_update (or sgd_momentum); `LocalGroup` sums in rank order, so it is
+bitwise the reference-shaped server graph at any world; over NCCL the
+summation order is NCCL's, so parity is tolerance-based.
 """
 
 from __future__ import annotations
@@ -41,7 +56,8 @@ from .graph import BiGraph, GraphError, GraphSequence, Location
 from .kinds import KernelError
 
 __all__ = ["Bucket", "ExchangePlan", "plan_buckets", "lower_data_parallel", "materialize",
-           "setup_nccl", "build_rank_sequence"]
+           "setup_nccl", "build_rank_sequence", "NcclCollective", "LocalGroup",
+           "velocity_name"]
 
 ALIGN = 16  # floats (64 B)
 
@@ -132,14 +148,23 @@ def lower_data_parallel(seq: GraphSequence, rank: int, plan: ExchangePlan, net) 
         grad_of[c] = f"d{c}{sfx}"
         if not ng.has_tensor(grad_of[c]):
             raise GraphError(f"lowering: gradient {grad_of[c]!r} not found")
+    mu = float(getattr(net, "momentum", 0.0) or 0.0)
+    vel: list[tuple[str, int]] = []
     for i, b in enumerate(plan.buckets):
         ws = [ng.tensor_id(f"{c}{sfx}") for c in b.params]
         gs = [ng.tensor_id(grad_of[c]) for c in b.params]
         outs = [ng.tensor_id(f"{c}_new{sfx}") for c in b.params]
+        attrs = {"lr": net.lr, "world": plan.world, "rank": rank, "flat_len": b.length,
+                 "offsets": [b.offsets[c] - b.start for c in b.params]}
+        if mu > 0:  # the rank's velocity shard of this bucket: one more input / output
+            shard = b.length // plan.world
+            vname = velocity_name(i, rank)
+            ws.append(ng.add_tensor(vname, (shard,), peer))
+            outs.append(ng.add_tensor(f"{vname[:-len(sfx)]}_new{sfx}", (shard,), peer))
+            attrs["momentum"] = mu
+            vel.append((vname, shard))
         ng.add_operator(f"xch_b{i}{sfx}", "dp_exchange", ws + gs, outs, peer, thread=base + 2 * rank,
-                        attrs={"lr": net.lr, "world": plan.world, "rank": rank,
-                               "flat_len": b.length,
-                               "offsets": [b.offsets[c] - b.start for c in b.params]})
+                        attrs=attrs)
     sw = seq.graphs[1]
     nsw = BiGraph()
     for o in sw.insertion_order:
@@ -152,18 +177,31 @@ def lower_data_parallel(seq: GraphSequence, rank: int, plan: ExchangePlan, net) 
             ids.append(nsw.tensor_id(tv.name) if nsw.has_tensor(tv.name)
                        else nsw.add_tensor(tv.name, tv.shape, tv.location))
         nsw.add_operator(op.name, op.kind, [], ids, op.location, op.thread, dict(op.attrs))
+        swap_thread = op.thread
+    for vname, shard in vel:  # velocity ping-pong, next to the parameter swaps
+        vnew = f"{vname[:-len(sfx)]}_new{sfx}"
+        a = nsw.add_tensor(vname, (shard,), peer)
+        b = nsw.add_tensor(vnew, (shard,), peer)
+        nsw.add_operator(f"swap_{vname}", "swap", [], [a, b], peer, swap_thread)
     canon = tuple(plan.shapes)
     lay = Layout(scheme="data", data_names=(f"x{sfx}",), label_names=(f"labels{sfx}",),
                  loss_names=(f"loss{sfx}",), canonical_params=canon,
                  peer_params=(tuple(f"{c}{sfx}" for c in canon),),
                  copy_threads=layout.copy_threads, classes=layout.classes, batch=layout.batch,
-                 canonical_in_store=False)
+                 velocity_params=tuple(v for v, _ in vel), canonical_in_store=False,
+                 first_rank=rank)
     return GraphSequence([ng, nsw], iterations=seq.iterations, layout=lay)
 
 
-def materialize(store, plan: ExchangePlan, rank: int) -> None:
-    """Allocate the three flat arenas on the store's device and bind the
-    rank's parameter / new-parameter / gradient tensors as views into them."""
+def velocity_name(bucket: int, rank: int) -> str:
+    """The lowered graph's velocity shard of ``bucket`` on ``rank``."""
+    return f"vxch_b{bucket}_p{rank}"
+
+
+def materialize(store, plan: ExchangePlan, rank: int, momentum: bool = False) -> None:
+    """Allocate the flat arenas on the store's device and bind the rank's
+    parameter / new-parameter / gradient tensors (and, with momentum, its
+    velocity shards) as views into them."""
     import torch
 
     sfx = f"_p{rank}"
@@ -175,6 +213,15 @@ def materialize(store, plan: ExchangePlan, rank: int) -> None:
             o = b.offsets[c]
             for arena, name in zip(arenas, (f"{c}{sfx}", f"{c}_new{sfx}", f"d{c}{sfx}")):
                 store.place(name, arena[o:o + n].view(plan.shapes[c]))
+    if momentum:  # this rank's velocity shards, bucket order (1/world of the parameters)
+        vel = [torch.zeros(plan.total // plan.world, dtype=torch.float32, device=store.device)
+               for _ in range(2)]
+        store._arenas += vel
+        for i, b in enumerate(plan.buckets):
+            shard, o = b.length // plan.world, b.start // plan.world
+            vname = velocity_name(i, rank)
+            store.place(vname, vel[0][o:o + shard])
+            store.place(f"{vname[:-len(sfx)]}_new{sfx}", vel[1][o:o + shard])
 
 
 def setup_nccl(store, world: int, rank: int) -> None:
@@ -206,6 +253,7 @@ def setup_nccl(store, world: int, rank: int) -> None:
     store._nccl = comm.value
     store._nccl_rank = rank
     store._nccl_world = world
+    store._collective = NcclCollective(comm.value, world, rank)
 
 
 def build_rank_sequence(net, world: int, rank: int, store, bucket_bytes: int = 4 << 20,
@@ -217,12 +265,125 @@ def build_rank_sequence(net, world: int, rank: int, store, bucket_bytes: int = 4
     full = build_data_parallel(net, plan)
     xplan = plan_buckets(param_names(net), world, bucket_bytes)
     seq = lower_data_parallel(full, rank, xplan, net)
-    materialize(store, xplan, rank)
+    materialize(store, xplan, rank, momentum=bool(seq.layout.velocity_params))
     if nccl is None:
         nccl = world > 1
     if nccl:  # world == 1 with nccl=True exercises the NCCL path on one GPU (tests)
         setup_nccl(store, world, rank)
     return seq, xplan
+
+
+class NcclCollective:
+    """In-place reduce-scatter(sum) / all-gather of one bucket over an NCCL
+    communicator (csrc/nccl_ops.cu), enqueued on the exchange lane's stream."""
+
+    def __init__(self, comm: int, world: int, rank: int) -> None:
+        self.comm, self.world, self.rank = comm, world, rank
+
+    def reduce_scatter(self, base: int, shard: int, stream: int) -> None:
+        from . import _native
+
+        _native.lib()("bf_nccl_reduce_scatter", self.comm, base, base + 4 * shard * self.rank,
+                      shard, stream)
+
+    def all_gather(self, base: int, shard: int, stream: int) -> None:
+        from . import _native
+
+        _native.lib()("bf_nccl_all_gather", self.comm, base + 4 * shard * self.rank, base, shard,
+                      stream)
+
+
+class LocalGroup:
+    """``world`` ranks' stores on ONE CUDA device, each dispatched from its own
+    host thread, exchanging through this library's kernels instead of NCCL.
+
+    Each collective is a rendezvous: every rank records an event on its
+    exchange stream and waits at a barrier; the last rank to arrive makes its
+    stream wait on all the others' events, runs the collective there
+    (reduce-scatter: `bf_aggregate` sum of every rank's shard in RANK order,
+    written in place into the owner's shard -- the reference aggregate's
+    order, ops.py:440-457; all-gather: `bf_copy` of every owned shard to every
+    rank), records a completion event, and every rank's stream waits on it.
+    Host order is the serial dispatch order, identical on every rank, so the
+    rendezvous sequence matches.  Eager dispatch only (a captured CUDA graph
+    cannot wait on another capture's events)."""
+
+    def __init__(self, world: int, timeout_s: float = 120.0) -> None:
+        import threading
+
+        self.world = world
+        self._barrier = threading.Barrier(world, timeout=timeout_s)
+        self._lock = threading.Lock()
+        self._slots: list = [None] * world
+        self._done = None
+
+    def member(self, rank: int) -> "_LocalMember":
+        return _LocalMember(self, rank)
+
+    def _rendezvous(self, rank: int, base: int, shard: int, stream: int, op: str) -> None:
+        import torch
+
+        ext = torch.cuda.ExternalStream(stream)
+        ev = torch.cuda.Event()
+        ev.record(ext)
+        self._slots[rank] = (base, shard, ext, ev, op)
+        import threading
+
+        try:
+            idx = self._barrier.wait()
+            if idx == 0:  # exactly one thread runs the collective
+                try:
+                    self._run()
+                except BaseException:
+                    self._barrier.abort()
+                    raise
+            self._barrier.wait()
+        except threading.BrokenBarrierError:
+            raise KernelError("LocalGroup: a peer rank failed or never reached this "
+                              "collective") from None
+        ext.wait_event(self._done)
+        self._barrier.wait()  # every rank has consumed `_done` before it is reused
+
+    def _run(self) -> None:
+        import torch
+
+        from . import _native
+
+        slots = list(self._slots)
+        bases, shards, ops = [s[0] for s in slots], {s[1] for s in slots}, {s[4] for s in slots}
+        if len(shards) != 1 or len(ops) != 1:
+            raise KernelError(f"LocalGroup: ranks disagree on the collective ({ops}, {shards})")
+        shard, op = shards.pop(), ops.pop()
+        st = slots[0][2]
+        for s in slots[1:]:
+            st.wait_event(s[3])
+        lib = _native.lib()
+        h = st.cuda_stream
+        if op == "reduce_scatter":
+            for r in range(self.world):
+                parts = _native.ptr_array([b + 4 * shard * r for b in bases])
+                lib("bf_aggregate", parts, self.world, bases[r] + 4 * shard * r, shard, 0, h)
+        else:  # all_gather: owner r's shard to every other rank
+            dev = torch.cuda.current_device()
+            for r in range(self.world):
+                for q in range(self.world):
+                    if q != r:
+                        lib("bf_copy", bases[q] + 4 * shard * r, dev, bases[r] + 4 * shard * r,
+                            dev, shard, h)
+        done = torch.cuda.Event()
+        done.record(st)
+        self._done = done
+
+
+class _LocalMember:
+    def __init__(self, group: LocalGroup, rank: int) -> None:
+        self.group, self.rank, self.world = group, rank, group.world
+
+    def reduce_scatter(self, base: int, shard: int, stream: int) -> None:
+        self.group._rendezvous(self.rank, base, shard, stream, "reduce_scatter")
+
+    def all_gather(self, base: int, shard: int, stream: int) -> None:
+        self.group._rendezvous(self.rank, base, shard, stream, "all_gather")
 
 
 def shard_of(flat_len: int, world: int, rank: int) -> tuple[int, int]:

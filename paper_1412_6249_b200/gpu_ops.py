@@ -288,31 +288,44 @@ def _no_transport(ctx, op):
 
 
 def _dp_exchange(ctx, op):
-    """Lowered parameter-server subgraph for one gradient bucket (exchange.py)."""
-    from .exchange import check_bucket
+    """Lowered parameter-server subgraph for one gradient bucket (exchange.py):
+    reduce-scatter(sum) -> fused mean + SGD (or momentum) on the owned shard
+    -> all-gather.  Inputs: the bucket's parameters [, velocity shard], then
+    its gradients; outputs: the new parameters [, new velocity shard]."""
+    from .exchange import check_bucket, shard_of
 
     ins = _ins(ctx, op)
     outs = _outs(ctx, op)
-    n = len(outs)
-    w0, g0, o0 = check_bucket(ins[:n], ins[n:], outs, op.attrs["offsets"])
-    length = int(op.attrs["flat_len"])
-    world = int(op.attrs["world"])
-    lr = float(op.attrs["lr"])
-    lib = _L()
-    comm = getattr(ctx.store, "_nccl", None)
-    if world == 1 and comm is None:  # single GPU: the exchange is the local update
-        lib("bf_sgd_mean_update", w0, g0, o0, lr, 1, length, ctx.stream)
-        return
-    if comm is None:
-        raise KernelError("dp_exchange: no NCCL communicator on this store "
-                          "(exchange.setup_nccl)")
-    from .exchange import shard_of
-
-    shard, first = shard_of(length, world, int(op.attrs["rank"]))
+    a = op.attrs
+    mu = float(a.get("momentum", 0.0) or 0.0)
+    nb = len(a["offsets"])
+    if len(outs) != nb + (mu > 0) or len(ins) != 2 * nb + (mu > 0):
+        raise KernelError(f"dp_exchange: {len(ins)} inputs / {len(outs)} outputs do not match "
+                          f"{nb} parameters (momentum {mu})")
+    w0, g0, o0 = check_bucket(ins[:nb], ins[len(ins) - nb:], outs[:nb], a["offsets"])
+    length, world, lr = int(a["flat_len"]), int(a["world"]), float(a["lr"])
+    shard, first = shard_of(length, world, int(a["rank"]))
+    coll = getattr(ctx.store, "_collective", None)
+    if coll is None and world > 1:
+        raise KernelError("dp_exchange: no collective attached to this store "
+                          "(exchange.setup_nccl or LocalGroup)")
+    if coll is not None and coll.world != world:
+        raise KernelError(f"dp_exchange: collective spans {coll.world} ranks, op expects {world}")
+    if mu > 0:
+        v, vn = ins[nb], outs[nb]
+        if v.numel != shard or vn.numel != shard:
+            raise KernelError(f"dp_exchange: velocity shard holds {v.numel} floats, expected {shard}")
     off = first * 4
-    lib("bf_nccl_reduce_scatter", comm, g0, g0 + off, shard, ctx.stream)
-    lib("bf_sgd_mean_update", w0 + off, g0 + off, o0 + off, lr, world, shard, ctx.stream)
-    lib("bf_nccl_all_gather", comm, o0 + off, o0, shard, ctx.stream)
+    lib = _L()
+    if coll is not None:
+        coll.reduce_scatter(g0, shard, ctx.stream)
+    if mu > 0:
+        lib("bf_sgd_mean_momentum", w0 + off, g0 + off, v.ptr, o0 + off, vn.ptr, lr, mu, world,
+            shard, ctx.stream)
+    else:
+        lib("bf_sgd_mean_update", w0 + off, g0 + off, o0 + off, lr, world, shard, ctx.stream)
+    if coll is not None:
+        coll.all_gather(o0, shard, ctx.stream)
 
 
 # ---------------------------------------------------------------------------

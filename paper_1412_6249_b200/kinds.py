@@ -355,12 +355,17 @@ def _ck_gate(ins, outs, a):
 
 
 def _ck_dp_exchange(ins, outs, a):
-    # lowered parameter-server subgraph (exchange.py): [w..., dw...] -> [w_new...]
-    _req(len(ins) == 2 * len(outs) and len(outs) >= 1, "dp_exchange: needs [w*, dw*] -> [w_new*]")
-    n = len(outs)
+    # lowered parameter-server subgraph (exchange.py):
+    # [w..., (v_shard), dw...] -> [w_new..., (v_shard_new)]; v only with momentum > 0
+    mom = float(a.get("momentum", 0.0) or 0.0) > 0
+    n = len(outs) - mom
+    _req(n >= 1 and len(ins) == 2 * n + mom,
+         "dp_exchange: needs [w*, (v), dw*] -> [w_new*, (v_new)]")
     for i in range(n):
-        _same("dp_exchange", ins[n + i], ins[i], f"grad {i} shape")
+        _same("dp_exchange", ins[n + mom + i], ins[i], f"grad {i} shape")
         _same("dp_exchange", outs[i], ins[i], f"output {i} shape")
+    if mom:
+        _same("dp_exchange", outs[n], ins[n], "velocity shard shape")
     _req("lr" in a and "world" in a, "dp_exchange: needs attrs lr, world")
 
 

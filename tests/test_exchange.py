@@ -131,3 +131,48 @@ def test_exchange_sweep_sizes_and_bandwidth_math():
     alg, bus = mod.bus_bw(1 << 30, 0.5, 8)
     assert abs(alg - 2.147483648) < 1e-9 and abs(bus - alg * 14 / 8) < 1e-9
     assert mod.bus_bw(1000, 1e-6, 1) == (1.0, 1.0)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_lowered_partition_carries_momentum_shards(world):
+    """With momentum the server's sgd_momentum + velocity swaps (builders.py
+    581-611) become one velocity shard per bucket on each rank (length
+    flat_len / world), an extra input/output of dp_exchange, and a swap."""
+    net = cifar_convnet(batch=4, momentum=0.9)
+    full = _full(net, world)
+    assert any(op.kind == "sgd_momentum" for op in full.graphs[0].operators.values())
+    plan = plan_buckets(param_names(net), world, bucket_bytes=64 << 10)
+    for rank in range(world):
+        seq = lower_data_parallel(full, rank, plan, net)
+        g, sw = seq.graphs
+        assert g.validate().ok and sw.validate().ok
+        xch = [op for op in g.operators.values() if op.kind == "dp_exchange"]
+        assert len(xch) == len(plan.buckets)
+        for i, (op, b) in enumerate(zip(xch, plan.buckets)):
+            assert op.attrs["momentum"] == 0.9
+            nb = len(b.params)
+            assert len(op.inputs) == 2 * nb + 1 and len(op.outputs) == nb + 1
+            v = g.tensors[op.inputs[nb]]
+            assert v.name == f"vxch_b{i}_p{rank}" and v.shape == (b.length // world,)
+            assert g.tensors[op.outputs[nb]].name == f"vxch_b{i}_new_p{rank}"
+        assert seq.layout.velocity_params == tuple(f"vxch_b{i}_p{rank}"
+                                                   for i in range(len(plan.buckets)))
+        swapped = {sw.tensors[op.outputs[0]].name for op in sw.operators.values()}
+        assert set(seq.layout.velocity_params) <= swapped
+        assert len(sw.operators) == len(param_names(net)) + len(plan.buckets)
+        assert seq.layout.first_rank == rank
+
+
+def test_dp_exchange_shape_check_rejects_bad_arity():
+    from paper_1412_6249_b200 import BiGraph, GraphError
+    from paper_1412_6249_b200.kinds import KernelError
+
+    loc = Location("local", 0)
+    g = BiGraph()
+    w = g.add_tensor("w", (4,), loc)
+    d = g.add_tensor("dw", (4,), loc)
+    o = g.add_tensor("w_new", (4,), loc)
+    with pytest.raises((GraphError, KernelError)):  # momentum needs the velocity pair
+        g.add_operator("x", "dp_exchange", [w, d], [o], loc, attrs={"lr": 0.1, "world": 1,
+                                                                     "momentum": 0.9})
+    g.add_operator("x", "dp_exchange", [w, d], [o], loc, attrs={"lr": 0.1, "world": 1})

@@ -1,0 +1,167 @@
+"""Parity of the exact path bench.py times: GoogLeNet through the lowered
+exchange (build_rank_sequence), CapturedSequence replay, the fusion plan and
+8 branch streams -- teacher-forced operator by operator (tests/teacher.py).
+
+* batch 32: one captured step, every operator against the CPU oracle:
+  bit-exact kinds bit for bit, contractions / LRN / softmax at the NS bound
+  rel 1e-4 / abs 1e-5, UNSCALED.
+* batch 128 (the headline configuration): one captured step, every
+  contraction against float64 arithmetic of the same formula on the GPU's own
+  inputs (the oracle's einsum would take minutes per layer here), at the
+  unscaled NS bound -- this is where the engines take their batch-128 regimes
+  (tc2 persistent tiles, chain-bounded split-K weight gradients over
+  K = N*P*Q up to 1.6M, paired tc4 CTAs, the kTma1x1 weight gradients).
+
+Both write a per-kind error table to $PURINE_B200_PARITY_OUT (if set).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from teacher import BITWISE, CONTRACTIONS, Tally, dp_exchange_ref, pre_swap_map, teacher_force
+from paper_1412_6249_b200 import SyntheticFeed, TensorStore, init_params
+from paper_1412_6249_b200.dispatcher import _env_lane_cap, _plan
+from paper_1412_6249_b200.exchange import build_rank_sequence
+from paper_1412_6249_b200.executor import CapturedSequence
+from paper_1412_6249_b200.nets import googlenet
+
+pytestmark = pytest.mark.gpu
+
+
+def _captured_step(batch, cache_reads=True):
+    net = googlenet(batch=batch, lr=0.01)
+    st = TensorStore("cuda:0")
+    seq, _ = build_rank_sequence(net, 1, 0, st)
+    init_params(net, st, 7, seq.layout)
+    feed = SyntheticFeed.for_net(net, 7, spread=0.0)
+    x, lab = feed.batch_for(0, 0)
+    st.set(seq.layout.data_names[0], x)
+    st.set(seq.layout.label_names[0], lab)
+    exe = CapturedSequence(seq, st)
+    exe.prepare()  # one eager iteration, then capture
+    exe.step()  # one replayed iteration: the timed path
+    torch.cuda.synchronize()
+    g = seq.graphs[0]
+    plan = _plan(g, _env_lane_cap())
+    swapped = pre_swap_map(seq.graphs[1])
+    cache = {}
+
+    def read(name):
+        if not cache_reads:
+            return st.array(swapped.get(name, name))
+        if name not in cache:
+            cache[name] = st.array(swapped.get(name, name))
+        return cache[name]
+
+    def materialised(name):
+        return st.has(swapped.get(name, name)) and name not in plan.elided
+
+    return seq, g, plan, read, materialised
+
+
+def _report(tally, title):
+    out = os.environ.get("PURINE_B200_PARITY_OUT")
+    if out:
+        with open(out, "a") as f:
+            f.write(f"\n## {title}\n\n{tally.table()}\n")
+    print(tally.table())
+
+
+def test_captured_googlenet_step_batch32_matches_oracle():
+    import oracle
+
+    seq, g, plan, read, materialised = _captured_step(32)
+    assert plan.fused_away and plan.elided  # the fused product schedule ran
+
+    def reference(kind, ins, attrs):
+        if kind == "dp_exchange":
+            return dp_exchange_ref(ins, attrs)
+        return oracle.KERNELS[kind](ins, attrs)
+
+    tally = Tally()
+
+    def on_output(op, name, got, want):
+        if op.kind in BITWISE:
+            tally.exact(op, name, got, want)
+        else:
+            tally.close(op, name, got, want)
+
+    n = teacher_force(g, read, materialised, reference, on_output)
+    _report(tally, "GoogLeNet batch 32, captured step vs CPU oracle (teacher-forced)")
+    assert n > 400
+    assert not tally.fails, "\n".join(tally.fails[:20])
+
+
+def _f64(a):
+    return torch.as_tensor(np.asarray(a), dtype=torch.float64, device="cuda:0")
+
+
+def _fp64_contraction(kind, ins, attrs):
+    """The reference's contraction formulas (ops.py:164-352) in float64."""
+    from paper_1412_6249_b200.kinds import conv_attrs
+
+    if kind.startswith("fc"):
+        if kind == "fc_forward":
+            x, w, b = map(_f64, ins)
+            return [(x @ w + b).cpu().numpy()]
+        if kind == "fc_backward_data":
+            w, dy = map(_f64, ins)
+            return [(dy @ w.T).cpu().numpy()]
+        if kind == "fc_backward_weight":
+            x, dy = map(_f64, ins)
+            return [(x.T @ dy).cpu().numpy()]
+        if kind == "fc_backward_bias":
+            return [_f64(ins[0]).sum(0).cpu().numpy()]
+    stride, pad, floor = conv_attrs(attrs)
+    assert not floor
+    if kind == "conv2d_forward":
+        x, w, b = map(_f64, ins)
+        return [F.conv2d(x, w, b, stride=stride, padding=pad).cpu().numpy()]
+    if kind == "conv2d_backward_data":
+        x, w, dy = map(_f64, ins)
+        return [torch.nn.grad.conv2d_input(x.shape, w, dy, stride=stride, padding=pad)
+                .cpu().numpy()]
+    if kind == "conv2d_backward_weight":
+        x, w, dy = map(_f64, ins)
+        return [torch.nn.grad.conv2d_weight(x, w.shape, dy, stride=stride, padding=pad)
+                .cpu().numpy()]
+    if kind == "conv2d_backward_bias":
+        return [_f64(ins[0]).sum((0, 2, 3)).cpu().numpy()]
+    raise AssertionError(kind)
+
+
+def test_captured_googlenet_step_batch128_contractions_vs_fp64():
+    seq, g, plan, read, materialised = _captured_step(128, cache_reads=False)
+    tally = Tally()
+    checked = 0
+    own = {}  # float64 results of contractions whose output the GPU never stored
+    from oracle.serial import serial_order
+
+    for oid in serial_order(g):
+        op = g.operators[oid]
+        names_in = [g.tensors[t].name for t in op.inputs]
+        names_out = [g.tensors[t].name for t in op.outputs]
+        if op.kind in CONTRACTIONS:
+            if not all(materialised(n) for n in names_in):
+                continue
+            want = _fp64_contraction(op.kind, [read(n) for n in names_in], dict(op.attrs))
+            for name, w in zip(names_out, want):
+                if materialised(name):
+                    tally.close(op, name, read(name), w)
+                    checked += 1
+                else:
+                    own[name] = w
+        elif op.kind == "relu_backward" and names_in[1] in own and materialised(names_out[0]):
+            # a data gradient with relu_backward folded into its epilogue
+            x = read(names_in[0])
+            want = np.where(x > 0, own.pop(names_in[1]), 0.0)
+            tally.close(op, names_out[0], read(names_out[0]), want)
+            checked += 1
+    _report(tally, "GoogLeNet batch 128, captured step: contractions vs float64 "
+                   "(teacher-forced)")
+    assert checked >= 150
+    assert not tally.fails, "\n".join(tally.fails[:20])
