@@ -204,29 +204,85 @@ def cpu_throughput(net_name: str, sample_batch: int, workers: int, steps: int):
     return workers * sample_batch / float(np.mean(times)), times
 
 
+def _reference_dp(net_name: str, peers: int, batch: int, seed: int = 7):
+    """The reference's data-parallel CPU execution: the
+    bi-graph of ``build_data_parallel`` with ``peers`` replicas + the server
+    subgraph, fused backward, run by the oracle's restatement of the
+    reference dispatcher's multi-worker mode (one thread per lane) on the
+    oracle's numpy kernels.  Returns a callable timing one iteration (G_dnn +
+    G_swap) in seconds."""
+    from oracle.serial import run_graph_lanes
+
+    from paper_1412_6249_b200 import (Location, ParallelPlan, SyntheticFeed, build_data_parallel,
+                                      feeder, init_params)
+    from paper_1412_6249_b200.nets import googlenet, nin
+
+    net = (googlenet if net_name == "googlenet" else nin)(batch=batch)
+    plan = ParallelPlan("data", peers=tuple(Location("local", k) for k in range(peers)),
+                        server=Location("local", peers))
+    seq = build_data_parallel(net, plan, split_backward=False)
+
+    class _S(dict):
+        def set(self, name, arr):
+            self[name] = np.array(arr, dtype=np.float32, copy=True)
+
+    st = _S()
+    init_params(net, st, seed, seq.layout)
+    feed = feeder(SyntheticFeed.for_net(net, seed, peers=peers, spread=0.0), seq.layout)
+    it = [0]
+
+    def one():
+        feed(it[0], st)
+        it[0] += 1
+        t = time.perf_counter()
+        for g in seq.graphs:
+            run_graph_lanes(g, st)
+        return time.perf_counter() - t
+
+    return one, st, seq.layout
+
+
 def run_reference(args):
+    """CPU reference arm: BASELINE.md section 4's plan -- P = --gpus peers at
+    batch 8 per peer through the reference's data-parallel graph (replicas on
+    their own lane threads, numpy single-threaded per lane), 1 warm-up and at
+    most 2 timed iterations (a GoogLeNet iteration is ~10 s of CPU per peer)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    # one replica thread per core (numpy releases the GIL in its kernels), capped
-    # so the replicas' activations stay a few GB of host memory
-    cores = min(len(os.sched_getaffinity(0)), 32)
-    sample = 1
-    # warm-up steps are shorter than timed ones only by reuse of numpy buffers
-    cpu_throughput(args.net, sample, cores, max(1, min(args.warmup, 1)))
-    value, times = cpu_throughput(args.net, sample, cores, args.steps)
+    from threadpoolctl import threadpool_limits
+
+    peers = max(1, args.gpus)
+    batch = 8
+    steps = max(1, min(args.steps, 2))
+    warm = max(0, min(args.warmup, 1))
+    with threadpool_limits(limits=1):
+        one, st, layout = _reference_dp(args.net, peers, batch)
+        for _ in range(warm):
+            one()
+        times = [one() for _ in range(steps)]
+    loss = float(np.mean([st[n][0] for n in layout.loss_names]))
+    value = peers * batch / float(np.mean(times))
+    affinity = len(os.sched_getaffinity(0))
+    cores = min(peers + 1, affinity)  # one lane thread per peer + the server lane
     metric = "GoogLeNet train images/sec" if args.net == "googlenet" else "NIN train images/sec"
+    sample = (f"{steps} timed iteration(s) after {warm} warm-up of {args.net} data-parallel SGD, "
+              f"{peers} peer(s) x batch {batch} + server subgraph (build_data_parallel, fused "
+              f"backward), oracle numpy port on the reference's lane-per-thread dispatcher")
     line = {
         "impl": "reference", "metric": metric, "value": value, "unit": "img/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": steps, "steps_requested": args.steps, "warmup": warm,
         "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.net} data-parallel SGD iteration, 224x224, CPU oracle port "
-                               f"(numpy restatement of the reference kernels), {cores} replica "
-                               f"threads x batch {sample}", "global_batch": cores * sample},
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (SyntheticFeed seed 7, spread 0)",
+        "config": {"workload": f"{args.net} data-parallel SGD iteration (G_dnn + G_swap), 224x224, "
+                               f"CPU: {peers} peers x batch {batch} (BASELINE.md section 4)",
+                   "global_batch": peers * batch, "per_peer_batch": batch, "peers": peers,
+                   "parallelism": f"dp{peers} (CPU lanes)"},
         "cpu_baseline": {"value": value, "unit": "img/s", "cores": cores, "kind": "port",
-                         "sample": f"{cores} threads x {sample}-image {args.net} iterations per step"},
+                         "sample": sample, "os_cpu_count": os.cpu_count(),
+                         "affinity_cores": affinity},
         "e2e": {"value": value, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "final_loss": loss,
     }
     print(json.dumps(line), flush=True)
 
@@ -355,6 +411,45 @@ def run_ours(args):
                "overlap": "batch i+1's host->device copy runs on a side stream during step i; "
                           "each step's loss is copied to pinned host memory behind it",
                "losses_finite": bool(np.all(np.isfinite(e2e_losses)))}
+        exe.sync()  # raises if any step produced a non-finite value
+
+        # the same through the drop-in API itself: run_sequence walks the graphs
+        # in Python every iteration (no CUDA-graph replay), feeding the pinned
+        # batch with before_iteration and reading each loss in after_graph
+        from paper_1412_6249_b200 import run_sequence
+
+        rs_reads = []
+
+        def before(it, st):
+            st.set(xname, x_pin)
+            st.set(lname, l_pin)
+
+        def after(rep, st):
+            if rep.graph_index == 0:
+                rs_reads.append(st.read_async(loss_name))
+
+        run_sequence(seq, store, before_iteration=before, after_graph=after, iterations=2,
+                     trace=False)
+        barrier()
+        rs_reads.clear()
+        e0.record()
+        run_sequence(seq, store, before_iteration=before, after_graph=after,
+                     iterations=args.steps, trace=False)
+        e1.record()
+        rs_losses = [float(r.value()[0]) for r in rs_reads]
+        e1.synchronize()
+        rs_ms = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([rs_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            rs_ms = float(t.item())
+        e2e["run_sequence"] = {
+            "value": world * args.batch * args.steps / (rs_ms / 1e3), "unit": "img/s",
+            "api": "run_sequence(seq, store, before_iteration=<pinned batch -> TensorStore.set>, "
+                   "after_graph=<TensorStore.read_async(loss)>, trace=False)",
+            "note": "host walks ~560 operators per iteration in Python; CapturedSequence replays "
+                    "the same launches as CUDA graphs",
+            "losses_finite": bool(np.all(np.isfinite(rs_losses)))}
 
     # traced replay of the same schedule, serialised on one stream per lane
     # (branch streams off) so each operator's interval is its own kernels'
@@ -369,6 +464,11 @@ def run_ours(args):
             del os.environ["PURINE_B200_BRANCH_STREAMS"]
         else:
             os.environ["PURINE_B200_BRANCH_STREAMS"] = prev
+    from paper_1412_6249_b200.dispatcher import _Plan
+
+    # operators the fusion plan turns into no-ops launch nothing: their bytes
+    # are moved (or never moved) by the kernel that absorbed them
+    fused_away = [_Plan(g, texe.cap, 1).fused_away for g in seq.graphs]
     reps = 3
     per_kind: dict[str, float] = {}
     contraction_ms = contraction_flops = 0.0
@@ -388,7 +488,8 @@ def run_ours(args):
             if op.kind in CONTRACTION_KINDS:
                 contraction_ms += t / (reps - 1)
                 contraction_flops += op_flops(g, op) / (reps - 1)
-            elif op.kind not in ("swap", "flatten_forward", "flatten_backward", "copy", "dp_exchange"):
+            elif (op.kind not in ("swap", "flatten_forward", "flatten_backward", "copy",
+                                  "dp_exchange") and op.id not in fused_away[gi]):
                 hbm_ms += t / (reps - 1)
                 hbm_bytes += op_bytes(g, op) / (reps - 1)
     # exposed communication: |union(exchange) minus union(compute)| / T_iter
@@ -396,7 +497,14 @@ def run_ours(args):
     # interval arithmetic, profiler.py:58-102)
     from paper_1412_6249_b200.profiler import _union, exposed_ns
 
-    iv = texe.op_intervals_ns(par)
+    # ... on the schedule that is timed: a traced replay with the branch streams on
+    cexe = CapturedSequence(seq, store, trace=True)
+    cexe.prepare()
+    for _ in range(3):
+        cpar = cexe.parity
+        cexe.step()
+    torch.cuda.synchronize()
+    iv = cexe.op_intervals_ns(cpar)
     comm_sp = [(s0, s1) for _, op, s0, s1 in iv if op.kind in ("dp_exchange", "copy")]
     comp_sp = [(s0, s1) for _, op, s0, s1 in iv if op.kind not in ("dp_exchange", "copy", "swap")]
     t_iter = (max(s1 for *_, s1 in iv) - min(s0 for _, _, s0, _ in iv)) if iv else 0
@@ -404,7 +512,8 @@ def run_ours(args):
                "exchange_ms": sum(b - a for a, b in _union(comm_sp)) / 1e6,
                "traced_iteration_ms": t_iter / 1e6,
                "basis": ("dp_exchange ops on the exchange stream vs compute ops, device "
-                         "intervals of a traced replay" + ("" if world > 1 else
+                         "intervals of a traced replay with the timed schedule's branch "
+                         "streams" + ("" if world > 1 else
                                                            "; world 1: the exchange is the "
                                                            "local fused mean+SGD, no NCCL"))}
     # the virtual-time simulator calibrated with this run's
@@ -447,7 +556,10 @@ def run_ours(args):
                 "share_of_step": contraction_ms / (ms / args.steps),
                 "timing_basis": "per-operator CUDA events of a serialised traced replay",
                 "algorithmic_tflop_per_step": contraction_flops / 1e12,
-                "hbm_kernels": {"achieved_gbs": hbm_bytes / (hbm_ms / 1e3) / 1e9 if hbm_ms else None,
+                "hbm_kernels": {"basis": "algorithmic bytes (SURVEY 8d) of the launched "
+                                         "non-contraction operators (fused-away no-ops "
+                                         "excluded) / their serialised device time",
+                                "achieved_gbs": hbm_bytes / (hbm_ms / 1e3) / 1e9 if hbm_ms else None,
                                 "peak_gbs": peaks.get("hbm_gbs", 6533.8),
                                 "ms_per_step": hbm_ms,
                                 "algorithmic_bytes_per_step": hbm_bytes,
@@ -496,8 +608,35 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def _launch_ranks(args) -> int:
+    """``--gpus N`` (N > 1) started without torchrun: re-launch this script as
+    N ranks, one process per GPU, through torch.distributed.run on 127.0.0.1.
+    Fails loudly when fewer than N GPUs are visible."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} visible CUDA devices, "
+                                   f"found {have}"}), flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = _args()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_launch_ranks(args))
+    if args.impl == "ours" and "WORLD_SIZE" in os.environ and \
+            int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.impl == "reference":
         run_reference(args)
     else:

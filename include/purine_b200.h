@@ -100,6 +100,12 @@ int bf_copy(float* dst, int dst_device, const float* src, int src_device, int64_
             bf_stream_t stream);
 /* sets *flag (device int) to 1 if any element is non-finite (ops.py:61-64) */
 int bf_check_finite(const float* x, int64_t n, int* flag, bf_stream_t stream);
+/* the same over `count` tensors in one pass (host arrays of device pointers and
+   lengths, copied into the launch: capture-safe); the flag is sticky (atomic OR).
+   The dispatcher runs it once per graph over the graph's sink tensors (the loss
+   and the updated parameters), the device form of ops.py:61-64's per-kernel check */
+int bf_check_finite_list(const float* const* ptrs, const int64_t* lens, int count, int* flag,
+                         bf_stream_t stream);
 
 /* softmax cross-entropy, ops.py:394-425 ---------------------------------- */
 /* workspace: >= n floats */

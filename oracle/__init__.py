@@ -26,6 +26,8 @@ Pinning:
 
 from .kernels import *  # noqa: F401,F403
 from .kernels import __all__ as _k_all
-from .serial import serial_order, run_graph_serial, run_sequence_serial  # noqa: F401
+from .serial import (serial_order, run_graph_lanes, run_graph_serial,  # noqa: F401
+                     run_sequence_serial)
 
-__all__ = list(_k_all) + ["serial_order", "run_graph_serial", "run_sequence_serial"]
+__all__ = list(_k_all) + ["serial_order", "run_graph_serial", "run_graph_lanes",
+                          "run_sequence_serial"]

@@ -46,6 +46,7 @@ _SIGS = {
     "bf_aggregate": [_p, _i, _p, _l, _i, _p],
     "bf_copy": [_p, _i, _p, _i, _l, _p],
     "bf_check_finite": [_p, _l, _p, _p],
+    "bf_check_finite_list": [_p, _p, _i, _p, _p],
     "bf_softmax_xent": [_p, _p, _p, _p, _i, _i, _p, _p],
     "bf_fc_fwd": [_p, _p, _p, _p, _i, _i, _i, _p, _l, _p],
     "bf_fc_bwd_data": [_p, _p, _p, _i, _i, _i, _p, _l, _p],

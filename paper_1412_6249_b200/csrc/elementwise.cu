@@ -262,6 +262,39 @@ __global__ void finite_kernel(const float* __restrict__ x, int64_t n, int* flag)
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
 }
 
+// up to kFiniteMax tensors per launch, passed by value (no device-side table:
+// the launch is safe to capture into a CUDA graph and replays with the same
+// buffers).  Blocks stride over the concatenation of the tensors; aligned
+// tensors are read as float4.
+constexpr int kFiniteMax = 96;
+struct FiniteList {
+  const float* ptr[kFiniteMax];
+  int64_t len[kFiniteMax];
+  int count;
+};
+
+__global__ void finite_list_kernel(const FiniteList list, int* flag) {
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int t = 0; t < list.count; ++t) {
+    const float* x = list.ptr[t];
+    const int64_t n = list.len[t];
+    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      const float4* x4 = reinterpret_cast<const float4*>(x);
+      const int64_t n4 = n >> 2;
+      for (int64_t i = tid; i < n4; i += stride) {
+        const float4 v = __ldg(x4 + i);
+        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+      }
+      for (int64_t i = (n4 << 2) + tid; i < n; i += stride) bad |= !isfinite(x[i]);
+    } else {
+      for (int64_t i = tid; i < n; i += stride) bad |= !isfinite(x[i]);
+    }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 }  // namespace
 }  // namespace bf
 
@@ -471,6 +504,30 @@ int bf_check_finite(const float* x, int64_t n, int* flag, bf_stream_t s) {
   if (n <= 0) return 0;
   finite_kernel<<<elementwise_grid(n, kThreads), kThreads, 0, as_stream(s)>>>(x, n, flag);
   return check_launch("check_finite");
+}
+
+int bf_check_finite_list(const float* const* ptrs, const int64_t* lens, int count, int* flag,
+                         bf_stream_t s) {
+  if (count < 0 || (count > 0 && (!ptrs || !lens || !flag))) {
+    set_error("check_finite_list: bad arguments (count %d)", count);
+    return -1;
+  }
+  for (int base = 0; base < count; base += kFiniteMax) {
+    FiniteList list;
+    list.count = count - base < kFiniteMax ? count - base : kFiniteMax;
+    int64_t total = 0;
+    for (int i = 0; i < list.count; ++i) {
+      list.ptr[i] = ptrs[base + i];
+      list.len[i] = lens[base + i];
+      total += lens[base + i];
+    }
+    if (total <= 0) continue;
+    finite_list_kernel<<<elementwise_grid((total + 3) / 4, kThreads), kThreads, 0, as_stream(s)>>>(
+        list, flag);
+    const int rc = check_launch("check_finite_list");
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -57,6 +57,7 @@ __all__ = [
     "WorkerLane",
     "lane_of",
     "merged_trace",
+    "raise_if_nonfinite",
     "run",
     "run_sequence",
     "serial_order",
@@ -466,6 +467,9 @@ class _Plan:
                 self.fusion.setdefault(c, {})["lrn_recompute"] = True
             self.elided.add(graph.tensors[sc].name)
 
+        self.finite_mode = _finite_mode()
+        self.finite_watch = _finite_watch(graph, self, self.finite_mode)
+
     def _split_branches(self, graph: BiGraph, branches: int) -> None:
         """Event-driven device concurrency inside a lane: the lane's operators
         are spread over up to ``branches`` CUDA streams by greedy chain
@@ -508,6 +512,101 @@ class _Plan:
             last_op[chosen] = oid
             last_use[chosen] = i
             done.add(oid)
+
+
+FINITE_ENV = "PURINE_B200_CHECK_FINITE"  # "sinks" (default) | "all" | "0"
+# kinds whose outputs the reference checks for non-finite values (ops.py:61-64 and
+# its call sites ops.py:175-456), plus this library's extension kinds
+FINITE_KINDS = frozenset({
+    "fc_forward", "fc_backward", "fc_backward_data", "fc_backward_weight", "fc_backward_bias",
+    "conv2d_forward", "conv2d_backward", "conv2d_backward_data", "conv2d_backward_weight",
+    "conv2d_backward_bias", "relu_forward", "relu_backward", "softmax_xent", "sgd_update",
+    "aggregate", "sgd_momentum", "dp_exchange", "maxpool_forward", "maxpool_backward",
+    "avgpool_forward", "avgpool_backward", "lrn_forward", "lrn_backward", "concat_forward",
+    "concat_backward"})
+
+
+def _finite_mode() -> str:
+    raw = os.environ.get(FINITE_ENV, "sinks").strip().lower()
+    if raw in ("0", "off", "none", "false"):
+        return "off"
+    if raw not in ("sinks", "all"):
+        raise DispatchError(f"{FINITE_ENV} must be sinks, all or 0, got {raw!r}")
+    return raw
+
+
+def _finite_watch(graph: BiGraph, plan, mode: str) -> list[str]:
+    """Tensors checked for non-finite values after the graph's last kernel.
+
+    The reference checks every kernel output on the host (ops.py:61-64).  Here
+    the check is one device pass per graph into a sticky flag: ``sinks`` (default)
+    covers the outputs nothing in the graph consumes -- the loss and the updated
+    parameters, which every forward / gradient value flows into -- and ``all``
+    every materialised output of a checked kind (the reference's coverage, at
+    the cost of re-reading every activation).  When the flag fires, the first
+    offending operator in serial order is located on the host and reported as
+    the reference reports it (`raise_if_nonfinite`)."""
+    if mode == "off":
+        return []
+    out: list[str] = []
+    seen: set[str] = set()
+    for oid in plan.order:
+        op = graph.operators[oid]
+        if op.kind not in FINITE_KINDS:
+            continue
+        for tid in op.outputs:
+            name = graph.tensors[tid].name
+            if name in seen or name in plan.elided:
+                continue
+            if mode == "sinks" and graph.consumers_of(tid):
+                continue
+            seen.add(name)
+            out.append(name)
+    return out
+
+
+def _launch_finite_check(store: TensorStore, names: list[str], stream) -> None:
+    if not names:
+        return
+    import ctypes as C
+
+    from . import _native
+
+    flag = store.finite_flag()
+    ts = [store.get(n) for n in names]
+    ptrs = (C.c_void_p * len(ts))(*[t.ptr for t in ts])
+    lens = (C.c_int64 * len(ts))(*[t.numel for t in ts])
+    _native.lib()("bf_check_finite_list", ptrs, lens, len(ts), flag.data_ptr(), stream.cuda_stream)
+
+
+def raise_if_nonfinite(store: TensorStore, graphs, *, sync: bool = True,
+                       cap: int | None = None) -> None:
+    """Read the store's sticky non-finite flag; if set, name the first operator
+    (serial order over ``graphs``) holding a non-finite output and raise
+    ``DispatchError("operator 'x' failed: <kind>: non-finite value in output")``
+    -- the reference's first-error report of ops.py:61-64 (dispatcher.py:344-346)."""
+    if not store.has_finite_flag():
+        return
+    if sync:
+        torch.cuda.synchronize(store.device)
+    if not store.finite_flag_set():
+        return
+    store.reset_finite_flag()
+    for g in graphs:
+        plan = _plan(g, _env_lane_cap() if cap is None else cap)
+        for oid in plan.order:
+            op = g.operators[oid]
+            if op.kind not in FINITE_KINDS:
+                continue
+            for tid in op.outputs:
+                name = g.tensors[tid].name
+                if name in plan.elided or not store.has(name):
+                    continue
+                if not bool(torch.isfinite(store.tensor(name)).all()):
+                    raise DispatchError(f"operator {op.name!r} failed: "
+                                        f"{op.kind}: non-finite value in output")
+    raise DispatchError("non-finite value in a graph output (the producing operator's "
+                        "buffers were overwritten before it could be located)")
 
 
 BRANCH_ENV = "PURINE_B200_BRANCH_STREAMS"  # device streams per compute lane (1 = lane-exclusive)
@@ -633,6 +732,8 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
         join = torch.cuda.Event()
         join.record(s)
         cur.wait_event(join)
+    if failure is None:
+        _launch_finite_check(store, plan.finite_watch, cur)
     if failure is not None:
         for s, _ in slots:  # drain what was already enqueued
             s.synchronize()
@@ -677,6 +778,7 @@ def run(graph: BiGraph, store: TensorStore, registry: dict | None = None, *,
             s, e = base.ns(a), base.ns(b)
             records.append(TraceRecord(oid, op.name, lane_of(op), s, max(e, s + 1), iteration))
         records.sort(key=lambda r: (r.start, r.end))
+        raise_if_nonfinite(store, [graph], sync=False, cap=cap)
     return RunReport(trace=records, elapsed=time.monotonic_ns() - host0, iteration=iteration,
                      dispatch_order=names)
 
@@ -709,4 +811,6 @@ def run_sequence(seq: GraphSequence, store: TensorStore, registry: dict | None =
             reports.append(rep)
             if after_graph is not None:
                 after_graph(rep, store)
+    if not trace:  # traced runs checked after every graph; here once, at the end
+        raise_if_nonfinite(store, seq.graphs, cap=max_workers)
     return reports

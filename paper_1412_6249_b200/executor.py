@@ -18,7 +18,7 @@ from __future__ import annotations
 import torch
 
 from .dispatcher import (DispatchError, RunContext, RunReport, _check_sources, _enqueue,
-                         _env_lane_cap, lanes_of)
+                         _env_lane_cap, lanes_of, raise_if_nonfinite)
 from .gpu_ops import HOST_ONLY
 from .graph import GraphSequence
 from .kinds import KINDS
@@ -58,6 +58,7 @@ class CapturedSequence:
         self._pending = None
         self._slot = 0
         self._consumed: list = [None, None]
+        self._flag_host = None  # pinned mirror of the store's non-finite flag
 
     def _ctx(self, g, it=0):
         return RunContext(store=self.store, graph=g, iteration=it)
@@ -164,9 +165,20 @@ class CapturedSequence:
             ev.record(cs)
         self._pending = (staged, ev, slot)
 
+    def sync(self) -> None:
+        """Wait for every enqueued step and raise `DispatchError` if any of them
+        produced a non-finite value (the dispatcher's per-graph device check)."""
+        raise_if_nonfinite(self.store, self.seq.graphs, sync=True, cap=self.cap)
+
     def step(self, after_graph=None, iteration: int = 0) -> None:
         if not self.ready:
             raise DispatchError("CapturedSequence.step() before prepare()")
+        # the non-finite flag of earlier steps, copied to pinned memory behind
+        # them: read without waiting (a step or two late), located and raised
+        # like the reference's per-kernel check once it shows up
+        if self._flag_host is not None and int(self._flag_host[0]) != 0:
+            self._flag_host.zero_()
+            self.sync()
         if self._pending is not None:  # inputs staged by prefetch()
             staged, ev, slot = self._pending
             self._pending = None
@@ -185,4 +197,8 @@ class CapturedSequence:
             if after_graph is not None:
                 after_graph(RunReport(trace=[], elapsed=0, iteration=iteration, graph_index=gi),
                             self.store)
+        if self.store.has_finite_flag():
+            if self._flag_host is None:
+                self._flag_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+            self._flag_host.copy_(self.store.finite_flag(), non_blocking=True)
         self.parity ^= 1

@@ -170,6 +170,23 @@ class TensorStore:
         return len(self._tensors)
 
     # -- device-side extensions --------------------------------------------
+    def finite_flag(self) -> torch.Tensor:
+        """Sticky device int32 set by the dispatcher's per-graph non-finite check."""
+        f = getattr(self, "_finite", None)
+        if f is None:
+            f = torch.zeros(1, dtype=torch.int32, device=self.device)
+            self._finite = f
+        return f
+
+    def has_finite_flag(self) -> bool:
+        return getattr(self, "_finite", None) is not None
+
+    def finite_flag_set(self) -> bool:
+        return bool(int(self.finite_flag().item()))
+
+    def reset_finite_flag(self) -> None:
+        self.finite_flag().zero_()
+
 
     def tensor(self, name: str) -> torch.Tensor:
         return self.get(name).data
