@@ -60,7 +60,8 @@ namespace {
 constexpr int kThreads = 256;
 
 // numpy maximum(x, 0) on finite x: x when x > 0, else +0.0 (-0.0 -> +0.0)
-__device__ __forceinline__ float relu1(float x) { return x > 0.f ? x : 0.f; }
+// np.maximum(x, 0): NaN propagates, -0 -> +0 (ops.py:359-364)
+__device__ __forceinline__ float relu1(float x) { return !(x <= 0.f) ? x : 0.f; }
 __device__ __forceinline__ float relu_g(float x, float g) { return x > 0.f ? g : 0.f; }
 __device__ __forceinline__ float sgd1(float w, float g, float lr) {
   return __fsub_rn(w, __fmul_rn(lr, g));

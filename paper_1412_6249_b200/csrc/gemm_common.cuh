@@ -134,8 +134,9 @@ struct RowPtr {
   int64_t relu_delta = 0;  // EpiNCHW: element offset of the fused ReLU output
 };
 
-// relu_forward's arithmetic (ops.py:359-364; elementwise.cu relu1)
-__device__ __forceinline__ float relu_value(float v) { return v > 0.f ? v : 0.f; }
+// relu_forward's arithmetic, np.maximum(v, 0): NaN propagates, -0 -> +0
+// (ops.py:359-364; elementwise.cu relu1)
+__device__ __forceinline__ float relu_value(float v) { return !(v <= 0.f) ? v : 0.f; }
 
 // out[(img*Cout + n)*PQ + pq] = v (+ bias[n]);  m = img*PQ + pq.
 // With relu_out set the epilogue also writes relu(v) there: the graph's

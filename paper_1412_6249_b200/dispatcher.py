@@ -598,6 +598,12 @@ def raise_if_nonfinite(store: TensorStore, graphs, *, sync: bool = True,
             op = g.operators[oid]
             if op.kind not in FINITE_KINDS:
                 continue
+            if op.kind == "softmax_xent":  # the kernel turns a bad label into a NaN loss
+                lab = store.tensor(g.tensors[op.inputs[1]].name)
+                k = g.tensors[op.inputs[0]].shape[1]
+                if not bool(((lab == lab.floor()) & (lab >= 0) & (lab < k)).all()):
+                    raise DispatchError(f"operator {op.name!r} failed: softmax_xent: labels "
+                                        f"must be integral and in [0, {k})")
             for tid in op.outputs:
                 name = g.tensors[tid].name
                 if name in plan.elided or not store.has(name):

@@ -56,7 +56,8 @@ def test_check_disabled(monkeypatch):
     monkeypatch.setenv("PURINE_B200_CHECK_FINITE", "0")
     _, seq, store = _setup("w1")
     run(seq.graphs[0], store)  # no check: trains on NaNs like a plain numpy loop would
-    assert not np.isfinite(store.array("loss")).all()
+    assert not np.isfinite(store.array("a1")).all()  # the conv output
+    assert not np.isfinite(store.array("w1_new")).all()
 
 
 def test_captured_sequence_raises():

@@ -177,6 +177,18 @@ def test_relu_bitwise(golden_ops):
                    O.relu_backward(x, dy))
 
 
+def test_relu_nan_propagates_like_numpy(monkeypatch):
+    """np.maximum(NaN, 0) is NaN (ops.py:361); the backward's where(x > 0)
+    drops it.  The dispatcher's non-finite check is off so the raw values show."""
+    monkeypatch.setenv("PURINE_B200_CHECK_FINITE", "0")
+    x = rnd(2, 3, 4, 4)
+    x[0, 0, 0, :4] = [np.nan, -np.nan, np.inf, -np.inf]
+    dy = rnd(2, 3, 4, 4)
+    assert_bitwise(run_op("relu_forward", {"x": x}, {"y": x.shape})["y"], O.relu_forward(x))
+    assert_bitwise(run_op("relu_backward", {"x": x, "dy": dy}, {"dx": x.shape})["dx"],
+                   O.relu_backward(x, dy))
+
+
 def test_sgd_momentum_aggregate_bitwise(golden_ops):
     g = golden_ops
     out = run_op("sgd_update", {"w": g["sgd_w"], "g": g["sgd_g"]}, {"o": g["sgd_w"].shape},
