@@ -649,18 +649,20 @@ def _fusion_enabled(registry) -> bool:
                                                       "maxpool_backward", "lrn_backward"))
 
 
-_PLAN_CACHE: dict[tuple[int, int, int], tuple[int, _Plan]] = {}
-
-
 def _plan(graph: BiGraph, cap: int) -> _Plan:
+    """The graph's launch plan, cached on the graph object itself (keyed by the
+    lane cap, branch streams and non-finite mode; rebuilt when the graph grew).
+    An id()-keyed global cache would hand a dead graph's plan to a new graph
+    that happens to reuse its address."""
     branches = _branch_streams()
-    key = (id(graph), cap, branches)
+    key = (cap, branches, _finite_mode())
     stamp = len(graph.insertion_order) * 1_000_003 + len(graph.tensors)
-    hit = _PLAN_CACHE.get(key)
+    cache = graph.__dict__.setdefault("_launch_plans", {})
+    hit = cache.get(key)
     if hit is not None and hit[0] == stamp:
         return hit[1]
     p = _Plan(graph, cap, branches)
-    _PLAN_CACHE[key] = (stamp, p)
+    cache[key] = (stamp, p)
     return p
 
 
