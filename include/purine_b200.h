@@ -177,6 +177,20 @@ int bf_maxpool_bwd(const float* mask, const float* dy, float* dx, int N, int C, 
 int bf_maxpool_bwd_relu(const float* mask, const float* dy, float* dx, const float* relu_x,
                         int N, int C, int H, int W, int P, int Q, int kernel, int stride, int pad,
                         bf_stream_t stream);
+/* 3x3 max pooling staged through shared memory by bulk copies (pool_staged.cu).
+   bf_maxpool_staged_ok: 1 when the shape is supported (backward != 0: the
+   backward's stage, which also holds dy and the recomputed argmax).  The
+   forward writes the mask only when `mask` is non-null; the backward
+   recomputes every window's argmax from x (bit-identical to the forward's) so
+   the mask never has to be stored, and with relu_from_x != 0 applies the
+   relu_backward of the operator that produced x = relu(a): dx = x > 0 ? dx : 0 */
+int bf_maxpool_staged_ok(int N, int C, int H, int W, int P, int Q, int kernel, int stride,
+                         int pad, int backward);
+int bf_maxpool_fwd_staged(const float* x, float* y, float* mask, int N, int C, int H, int W,
+                          int P, int Q, int kernel, int stride, int pad, bf_stream_t stream);
+int bf_maxpool_bwd_x(const float* x, const float* dy, float* dx, int relu_from_x, int N, int C,
+                     int H, int W, int P, int Q, int kernel, int stride, int pad,
+                     bf_stream_t stream);
 int bf_avgpool_fwd(const float* x, float* y, int N, int C, int H, int W, int P, int Q,
                    int kernel, int stride, int pad, bf_stream_t stream);
 int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P, int Q,

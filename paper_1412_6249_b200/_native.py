@@ -61,6 +61,9 @@ _SIGS = {
     "bf_conv2d_bwd_weight_bias": [_p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_bwd_bias": [_p, _p, _i, _i, _i, _p, _l, _p],
     "bf_gemm_workspace_bytes": [_i] * 12,
+    "bf_maxpool_staged_ok": [_i] * 10,
+    "bf_maxpool_fwd_staged": [_p, _p, _p] + [_i] * 9 + [_p],
+    "bf_maxpool_bwd_x": [_p, _p, _p, _i] + [_i] * 9 + [_p],
     "bf_maxpool_fwd": [_p, _p, _p] + [_i] * 9 + [_p],
     "bf_maxpool_bwd": [_p, _p, _p] + [_i] * 9 + [_p],
     "bf_maxpool_bwd_relu": [_p, _p, _p, _p] + [_i] * 9 + [_p],

@@ -1302,8 +1302,10 @@ static void lrn5_bwd_rc_launch(const float* x, const float* dy, float* dx, const
 // bit 2 backward stride 1, bit 3 warp-row kernels (stride 1, pad 1, W <= 32);
 // PURINE_B200_POOL_WALKERS, default all on
 static int pool_walkers() {
+  // bit 0/1: stride-1/2 column walkers, 2: stride-1 backward walker, 3: warp-row
+  // kernels, 4: shared-memory staged kernels (pool_staged.cu)
   const char* e = std::getenv("PURINE_B200_POOL_WALKERS");
-  return e ? std::atoi(e) : 15;
+  return e ? std::atoi(e) : 31;
 }
 
 extern "C" {
@@ -1312,6 +1314,10 @@ int bf_maxpool_fwd(const float* x, float* y, float* mask, int N, int C, int H, i
                    int Q, int kernel, int stride, int pad, bf_stream_t s) {
   int64_t total = (int64_t)N * C * P * Q;
   if (total <= 0) return 0;
+  // staged through shared memory by bulk copies (pool_staged.cu) where it fits
+  if ((pool_walkers() & 16) && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+      bf_maxpool_staged_ok(N, C, H, W, P, Q, kernel, stride, pad, 0))
+    return bf_maxpool_fwd_staged(x, y, mask, N, C, H, W, P, Q, kernel, stride, pad, s);
   if (kernel == 3 && stride == 1 && pad == 1 && W <= 32 && P == H && Q == W &&
       (pool_walkers() & 8)) {
     const int64_t planes = (int64_t)N * C, warps = (planes + 32 / W - 1) / (32 / W);

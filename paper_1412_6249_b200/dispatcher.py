@@ -189,14 +189,14 @@ class ReadinessState:
         return self._executed == len(self.graph.operators) and self.completed_sinks == self.sink_count
 
 
-_ORDER_CACHE: dict[int, tuple[int, list[int]]] = {}
 
 
 def serial_order(graph: BiGraph) -> list[int]:
     """Reference serial-mode (one worker) dispatch order of ``graph``."""
-    key = id(graph)
+    # cached on the graph object (an id()-keyed cache can serve a dead graph's
+    # order to a new graph allocated at the same address)
     stamp = len(graph.insertion_order) * 1_000_003 + len(graph.tensors)
-    hit = _ORDER_CACHE.get(key)
+    hit = graph.__dict__.get("_serial_order")
     if hit is not None and hit[0] == stamp:
         return hit[1]
     st = ReadinessState(graph)
@@ -207,7 +207,7 @@ def serial_order(graph: BiGraph) -> list[int]:
         head += 1
     if len(queue) != len(graph.operators):
         raise DispatchError("graph cannot complete: some operators never become ready")
-    _ORDER_CACHE[key] = (stamp, queue)
+    graph.__dict__["_serial_order"] = (stamp, queue)
     return queue
 
 
@@ -421,6 +421,29 @@ class _Plan:
                     c0 += graph.tensors[t].shape[1]
                 self.fused_away.add(oid)
 
+        # max-pool mask elision: when a maxpool_forward's argmax mask feeds only
+        # maxpool_backward operators of the same x and attributes, and the
+        # shared-memory staged kernels fit the shape, the backward recomputes
+        # every window's argmax from x (the forward's own scan: bit-identical)
+        # and the forward never stores the mask
+        for oid, op in graph.operators.items():
+            if op.kind != "maxpool_forward" or len(op.outputs) != 2:
+                continue
+            mk = op.outputs[1]
+            cons = graph.consumers_of(mk)
+            if not cons or any(
+                    graph.operators[c].kind != "maxpool_backward" or
+                    graph.operators[c].inputs[0] != op.inputs[0] or
+                    graph.operators[c].inputs[1] != mk or
+                    graph.operators[c].attrs != op.attrs for c, _ in cons):
+                continue
+            if not _pool_staged(graph, op):
+                continue
+            self.fusion.setdefault(oid, {})["pool_no_mask"] = True
+            for c, _ in cons:
+                self.fusion.setdefault(c, {})["pool_recompute"] = True
+            self.elided.add(graph.tensors[mk].name)
+
         # relu_backward folded into the operator producing its dy (a data
         # gradient epilogue, the max-pool or LRN backward kernel) when that dy
         # has no other consumer: the producer writes relu_backward's dx directly
@@ -431,11 +454,25 @@ class _Plan:
                 continue
             g = op.inputs[1]
             p = graph.producer_of(g)
-            if (p is None or graph.operators[p].kind not in foldable or p in self.fusion
+            if (p is None or graph.operators[p].kind not in foldable
+                    or (p in self.fusion and set(self.fusion[p]) != {"pool_recompute"})
                     or len(graph.consumers_of(g)) != 1 or p in self.fused_away):
                 continue
             rx = graph.tensors[op.inputs[0]].name
             pk = graph.operators[p]
+            if pk.kind == "maxpool_backward":
+                # staged backward only, and only when the pool's own input is this
+                # ReLU's output: relu(a) > 0 <=> a > 0, so x is the mask
+                if p not in self.fusion or not any(
+                        graph.operators[c].kind == "relu_forward"
+                        and graph.operators[c].outputs[0] == pk.inputs[0]
+                        for c, _ in graph.consumers_of(op.inputs[0])):
+                    continue
+                self.fusion[p].update({"relu_from_x": True,
+                                       "relu_dx": graph.tensors[op.outputs[0]].name})
+                self.fused_away.add(oid)
+                self.elided.add(graph.tensors[g].name)
+                continue
             if pk.kind == "lrn_backward":
                 # the LRN's own input is the ReLU's output: its sign is the
                 # same mask (relu(a) > 0 <=> a > 0) and the kernel already
@@ -633,7 +670,24 @@ FUSE_ENV = "PURINE_B200_FUSE"  # "0" disables epilogue fusion (A/B and debugging
 # producer kinds that may absorb the relu_backward after them (all three have the
 # kernel support; measured net gains decide the default)
 RELU_FOLD_ENV = "PURINE_B200_RELU_FOLD"
-RELU_FOLD_DEFAULT = "conv2d_backward_data,lrn_backward"
+RELU_FOLD_DEFAULT = "conv2d_backward_data,lrn_backward,maxpool_backward"
+
+
+def _pool_staged(graph: BiGraph, op) -> bool:
+    """Whether the shared-memory staged max-pool kernels take this shape (both
+    directions): the condition for eliding the argmax mask."""
+    from .kinds import pool_attrs
+
+    try:
+        from . import _native
+
+        k, s, p = pool_attrs(op.attrs)
+        n, c, h, w = graph.tensors[op.inputs[0]].shape
+        _, _, ph, pw = graph.tensors[op.outputs[0]].shape
+        ok = _native.lib().raw("bf_maxpool_staged_ok")
+        return bool(ok(n, c, h, w, ph, pw, k, s, p, 0) and ok(n, c, h, w, ph, pw, k, s, p, 1))
+    except Exception:  # noqa: BLE001 - no library: the plain kernels run (and fail loudly)
+        return False
 
 
 def _fusion_enabled(registry) -> bool:
@@ -646,7 +700,8 @@ def _fusion_enabled(registry) -> bool:
                                                       "conv2d_backward_bias", "concat_forward",
                                                       "concat_backward", "relu_backward",
                                                       "aggregate", "conv2d_backward_data",
-                                                      "maxpool_backward", "lrn_backward"))
+                                                      "maxpool_forward", "maxpool_backward",
+                                                      "lrn_forward", "lrn_backward"))
 
 
 def _plan(graph: BiGraph, cap: int) -> _Plan:

@@ -334,16 +334,39 @@ def _dp_exchange(ctx, op):
 
 def _maxpool_fwd(ctx, op):
     (x,) = _ins(ctx, op)
-    y, mask = _outs(ctx, op)
     k, s, p = pool_attrs(op.attrs)
     n, c, h, w = x.shape
+    fused = getattr(ctx, "fused", None) or {}
+    g = ctx.graph
+    yv = g.tensors[op.outputs[0]]
+    y = ctx.store.ensure(yv.name, yv.shape)
+    if fused.get("pool_no_mask"):  # only maxpool_backward reads it, and it recomputes it
+        _L()("bf_maxpool_fwd_staged", x.ptr, y.ptr, None, n, c, h, w, y.shape[2], y.shape[3], k,
+             s, p, ctx.stream)
+        return
+    mv = g.tensors[op.outputs[1]]
+    mask = ctx.store.ensure(mv.name, mv.shape)
     _L()("bf_maxpool_fwd", x.ptr, y.ptr, mask.ptr, n, c, h, w, y.shape[2], y.shape[3], k, s, p,
          ctx.stream)
 
 
 def _maxpool_bwd(ctx, op):
-    x, mask, dy = _ins(ctx, op)
     k, s, p = pool_attrs(op.attrs)
+    fused = getattr(ctx, "fused", None) or {}
+    if fused.get("pool_recompute"):  # argmax recomputed from x (the mask is elided)
+        g = ctx.graph
+        x = ctx.store.get(g.tensors[op.inputs[0]].name)
+        dy = ctx.store.get(g.tensors[op.inputs[2]].name)
+        n, c, h, w = x.shape
+        if fused.get("relu_from_x"):  # + the relu_backward of x = relu(a)
+            dx = ctx.store.ensure(fused["relu_dx"], x.shape)
+        else:
+            dxv = g.tensors[op.outputs[0]]
+            dx = ctx.store.ensure(dxv.name, dxv.shape)
+        _L()("bf_maxpool_bwd_x", x.ptr, dy.ptr, dx.ptr, int(bool(fused.get("relu_from_x"))), n, c,
+             h, w, dy.shape[2], dy.shape[3], k, s, p, ctx.stream)
+        return
+    x, mask, dy = _ins(ctx, op)
     n, c, h, w = x.shape
     rx, rdx = _relu_fold(ctx, op)
     if rx is not None:

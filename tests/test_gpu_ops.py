@@ -214,12 +214,15 @@ def test_sgd_momentum_aggregate_bitwise(golden_ops):
                                          ((2, 3, 6, 7), 3, 1, 0), ((2, 64, 7, 7), 3, 1, 1),
                                          ((2, 16, 14, 14), 3, 1, 1), ((1, 3, 9, 32), 3, 1, 1),
                                          ((1, 3, 6, 33), 3, 1, 1), ((3, 5, 4, 1), 3, 1, 1)])
-@pytest.mark.parametrize("walkers", ["15", "7", "0"], ids=["rows", "columns", "planes"])
+@pytest.mark.parametrize("walkers", ["31", "15", "7", "0"],
+                         ids=["staged", "rows", "columns", "planes"])
 @pytest.mark.parametrize("values", ["normal", "coarse"])
 def test_maxpool_bitwise(shape, k, s, p, walkers, values, monkeypatch):
-    """Warp-row kernels (default for stride-1 pad-1 planes <= 32 wide), column
-    walkers and plane-staging kernels (PURINE_B200_POOL_WALKERS=15 / 7 / 0)
-    all bit-exact; "coarse" values make most
+    """Bulk-staged 3x3 forward (default where it fits), warp-row kernels
+    (stride-1 pad-1 planes <= 32 wide), column walkers and plane-staging
+    kernels (PURINE_B200_POOL_WALKERS=31 / 15 / 7 / 0) all bit-exact; the
+    single-operator graph keeps the mask, so the backward here is the
+    mask-reading gather.  "coarse" values make most
     windows hold ties (first maximum in raster order wins) and put a -inf
     block in the corner."""
     monkeypatch.setenv("PURINE_B200_POOL_WALKERS", walkers)
@@ -237,6 +240,68 @@ def test_maxpool_bitwise(shape, k, s, p, walkers, values, monkeypatch):
     dx = run_op("maxpool_backward", {"x": x, "m": m, "dy": dy}, {"dx": x.shape},
                 {"kernel": k, "stride": s, "pad": p})["dx"]
     assert_bitwise(dx, O.maxpool_backward(x, m, dy), "maxpool dx")
+
+
+MAXPOOL_STAGED_SHAPES = [((2, 64, 112, 112), 3, 2, 0), ((2, 192, 56, 56), 3, 2, 0),
+                         ((2, 192, 28, 28), 3, 1, 1), ((3, 480, 28, 28), 3, 2, 0),
+                         ((2, 832, 14, 14), 3, 2, 0), ((2, 528, 14, 14), 3, 1, 1),
+                         ((4, 832, 7, 7), 3, 1, 1), ((2, 8, 14, 14), 3, 2, 1),
+                         ((2, 5, 11, 13), 3, 2, 1), ((4, 7, 5, 5), 3, 1, 1),
+                         ((2, 6, 6, 7), 3, 1, 0), ((4, 3, 9, 33), 3, 1, 1),
+                         ((1, 96, 54, 54), 3, 2, 0), ((4, 6, 6, 7), 3, 2, 0)]
+
+
+@pytest.mark.parametrize("shape,k,s,p", MAXPOOL_STAGED_SHAPES)
+@pytest.mark.parametrize("fold", [False, True], ids=["pool", "relu+pool"])
+@pytest.mark.parametrize("values", ["normal", "coarse"])
+def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values):
+    """The product pairing: maxpool_forward and maxpool_backward in one graph,
+    the mask elided (the backward recomputes each window's argmax from x with
+    the forward's scan) and, after a ReLU, the relu_backward folded in through
+    the pool's own input.  y, dx (or the folded da) bit-exact vs the oracle."""
+    from paper_1412_6249_b200 import BiGraph, Location, TensorStore, run
+    from paper_1412_6249_b200._native import lib
+    from paper_1412_6249_b200.dispatcher import _plan
+
+    loc = Location("local", 0)
+    a = rnd(*shape)
+    a[:, :, ::3, ::3] = 0.5
+    if values == "coarse":
+        a = f32(np.round(a))
+        a[:, :, :3, :3] = -3e38
+    x = O.relu_forward(a) if fold else a
+    y, m = O.maxpool_forward(x, k, s, p)
+    dy = rnd(*y.shape)
+    dx = O.maxpool_backward(x, m, dy)
+    attrs = {"kernel": k, "stride": s, "pad": p}
+    g = BiGraph()
+    tx = g.add_tensor("x", shape, loc)
+    if fold:
+        ta = g.add_tensor("a", shape, loc)
+        g.add_operator("relu", "relu_forward", [ta], [tx], loc)
+    ty, tm = g.add_tensor("y", y.shape, loc), g.add_tensor("m", y.shape, loc)
+    tdy, tdx = g.add_tensor("dy", y.shape, loc), g.add_tensor("dx", shape, loc)
+    g.add_operator("pool", "maxpool_forward", [tx], [ty, tm], loc, attrs=attrs)
+    g.add_operator("bwd_pool", "maxpool_backward", [tx, tm, tdy], [tdx], loc, attrs=attrs)
+    if fold:
+        tda = g.add_tensor("da", shape, loc)
+        g.add_operator("bwd_relu", "relu_backward", [ta, tdx], [tda], loc)
+    n, c, h, w = shape
+    staged = bool(lib().raw("bf_maxpool_staged_ok")(n, c, h, w, y.shape[2], y.shape[3], k, s, p, 1))
+    plan = _plan(g, 8)
+    assert ("m" in plan.elided) == staged
+    st = TensorStore("cuda:0")
+    st.set("a" if fold else "x", a)
+    st.set("dy", dy)
+    run(g, st)
+    assert_bitwise(st.array("y"), y, "maxpool y")
+    if fold:
+        assert_bitwise(st.array("da"), O.relu_backward(a, dx), "relu+maxpool da")
+        assert ("dx" in plan.elided) == staged
+    else:
+        assert_bitwise(st.array("dx"), dx, "maxpool dx")
+    if staged:
+        assert not st.has("m")  # never materialised
 
 
 @pytest.mark.parametrize("shape,k,s,p", [((2, 1024, 7, 7), 7, 1, 0), ((2, 5, 9, 9), 3, 2, 1),
