@@ -26,6 +26,8 @@
 // registers; stride 2 tests the <= 2x2 covering windows directly.  With
 // relu_from_x the ReLU backward of the operator that produced x is folded in:
 // x = relu(a) > 0 <=> a > 0, so dx = x > 0 ? acc : 0 (relu_backward's select).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -36,7 +38,7 @@ namespace pools {
 
 using namespace tcu;
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kMaxStages = 4;
 
 struct Geo {
@@ -44,73 +46,68 @@ struct Geo {
   int64_t planes;
   int G;            // planes per chunk
   int64_t nchunks;
-  int RB;           // output (fwd) / input (bwd) rows per walker run
-  int runs;         // ceil(rows / RB)
+  int RB;           // output rows per walker run (forward, backward phase 1)
+  int runs;         // ceil(P / RB)
+  int RBh, hruns;   // backward phase 2 (stride 1): input rows per run, runs
   int NS;           // ring stages
   int stage_floats; // floats per stage (16-byte multiple)
+  // exact multiply-shift division (x < 2^31) for the per-item index decode:
+  // items per plane (phase 1 / forward), output columns, items per plane
+  // (backward phase 2), its inner extent
+  uint64_t m_pp1, m_q, m_pp2, m_in2;
+  int s_pp1, s_q, s_pp2, s_in2;
 };
 
-__device__ __forceinline__ void row_red(const float* __restrict__ xs, int H, int W, int h, int ws,
-                                        bool c0, bool c1, bool c2, float& m, int& a) {
+__device__ __forceinline__ int fdiv(int x, uint64_t m, int s) {
+  return (int)(((uint64_t)(uint32_t)x * m) >> s);
+}
+
+// first maximum of input row h's window columns ws, ws+1, ws+2 (strict '>'
+// from -inf; out-of-plane taps never win): value and column offset 0..2
+// (-1: none)
+__device__ __forceinline__ void row_red(const float* __restrict__ xs, int W, bool rv, int off,
+                                        bool c0, bool c1, bool c2, float& m, int& d) {
+  const float v0 = (rv && c0) ? xs[off] : -INFINITY;
+  const float v1 = (rv && c1) ? xs[off + 1] : -INFINITY;
+  const float v2 = (rv && c2) ? xs[off + 2] : -INFINITY;
   m = -INFINITY;
-  a = -1;
-  if ((unsigned)h < (unsigned)H) {
-    const float* r = xs + h * W + ws;
-    const int base = h * W + ws;
-    if (c0) {
-      const float v = r[0];
-      if (v > m) { m = v; a = base; }
-    }
-    if (c1) {
-      const float v = r[1];
-      if (v > m) { m = v; a = base + 1; }
-    }
-    if (c2) {
-      const float v = r[2];
-      if (v > m) { m = v; a = base + 2; }
-    }
-  }
+  d = -1;
+  if (v0 > m) { m = v0; d = 0; }
+  if (v1 > m) { m = v1; d = 1; }
+  if (v2 > m) { m = v2; d = 2; }
 }
 
-__device__ __forceinline__ void pick3(const float (&rm)[3], const int (&ra)[3], float& best,
-                                      int& arg) {
-  best = -INFINITY;
-  arg = -1;
-#pragma unroll
-  for (int d = 0; d < 3; ++d)
-    if (rm[d] > best) {
-      best = rm[d];
-      arg = ra[d];
-    }
-}
-
-// walk output column pw of plane xs over output rows [ph0, ph1): emit(ph, best, arg)
+// walk output column pw of one plane over output rows [ph0, ph1); emit(ph, best, arg)
+// with arg the flat index h*W + w of the window's first maximum (-1: none)
 template <int S, class Emit>
-__device__ __forceinline__ void walk_windows(const float* __restrict__ xs, const Geo& g, int pw,
-                                             int ph0, int ph1, const Emit& emit) {
-  const int ws = pw * S - g.pad;
-  const bool c0 = (unsigned)ws < (unsigned)g.W, c1 = (unsigned)(ws + 1) < (unsigned)g.W,
-             c2 = (unsigned)(ws + 2) < (unsigned)g.W;
-  float rm[3];
-  int ra[3];
-  int h = ph0 * S - g.pad;
-#pragma unroll
-  for (int d = 0; d < 3; ++d) row_red(xs, g.H, g.W, h + d, ws, c0, c1, c2, rm[d], ra[d]);
+__device__ __forceinline__ void walk_windows(const float* __restrict__ xs, int H, int W, int pad,
+                                             int pw, int ph0, int ph1, Emit&& emit) {
+  const int ws = pw * S - pad;
+  const bool c0 = (unsigned)ws < (unsigned)W, c1 = (unsigned)(ws + 1) < (unsigned)W,
+             c2 = (unsigned)(ws + 2) < (unsigned)W;
+  float m0, m1, m2;
+  int d0, d1, d2;
+  int h = ph0 * S - pad;  // top row of the current window
+  row_red(xs, W, (unsigned)h < (unsigned)H, h * W + ws, c0, c1, c2, m0, d0);
+  row_red(xs, W, (unsigned)(h + 1) < (unsigned)H, (h + 1) * W + ws, c0, c1, c2, m1, d1);
+  row_red(xs, W, (unsigned)(h + 2) < (unsigned)H, (h + 2) * W + ws, c0, c1, c2, m2, d2);
   for (int ph = ph0;;) {
-    float best;
-    int arg;
-    pick3(rm, ra, best, arg);
+    float best = -INFINITY;
+    int arg = -1;
+    if (m0 > best) { best = m0; arg = h * W + ws + d0; }
+    if (m1 > best) { best = m1; arg = (h + 1) * W + ws + d1; }
+    if (m2 > best) { best = m2; arg = (h + 2) * W + ws + d2; }
     emit(ph, best, arg);
     if (++ph >= ph1) break;
     h += S;
     if (S == 1) {
-      rm[0] = rm[1]; ra[0] = ra[1];
-      rm[1] = rm[2]; ra[1] = ra[2];
-      row_red(xs, g.H, g.W, h + 2, ws, c0, c1, c2, rm[2], ra[2]);
+      m0 = m1; d0 = d1;
+      m1 = m2; d1 = d2;
+      row_red(xs, W, (unsigned)(h + 2) < (unsigned)H, (h + 2) * W + ws, c0, c1, c2, m2, d2);
     } else {
-      rm[0] = rm[2]; ra[0] = ra[2];
-      row_red(xs, g.H, g.W, h + 1, ws, c0, c1, c2, rm[1], ra[1]);
-      row_red(xs, g.H, g.W, h + 2, ws, c0, c1, c2, rm[2], ra[2]);
+      m0 = m2; d0 = d2;
+      row_red(xs, W, (unsigned)(h + 1) < (unsigned)H, (h + 1) * W + ws, c0, c1, c2, m1, d1);
+      row_red(xs, W, (unsigned)(h + 2) < (unsigned)H, (h + 2) * W + ws, c0, c1, c2, m2, d2);
     }
   }
 }
@@ -124,9 +121,10 @@ __device__ __forceinline__ void issue_loads(uint32_t dst, const float* src0, int
 }
 
 template <int S>
-__global__ void __launch_bounds__(kThreads) maxpool3_fwd_staged(const float* __restrict__ x,
-                                                                float* __restrict__ y,
-                                                                float* __restrict__ mask, Geo g) {
+__global__ void __launch_bounds__(kThreads, 2) maxpool3_fwd_staged(const float* __restrict__ x,
+                                                                   float* __restrict__ y,
+                                                                   float* __restrict__ mask,
+                                                                   Geo g) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t full[kMaxStages];
   const int HW = g.H * g.W, PQ = g.P * g.Q;
@@ -135,7 +133,10 @@ __global__ void __launch_bounds__(kThreads) maxpool3_fwd_staged(const float* __r
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto planes_of = [&](int64_t c) { const int64_t left = g.planes - c * g.G; return (int)(left < g.G ? left : g.G); };
+  auto planes_of = [&](int64_t c) {
+    const int64_t left = g.planes - c * g.G;
+    return (int)(left < g.G ? left : g.G);
+  };
   if (threadIdx.x == 0) {
     int64_t c = blockIdx.x;
     for (int s = 0; s < g.NS && c < g.nchunks; ++s, c += gridDim.x)
@@ -144,23 +145,29 @@ __global__ void __launch_bounds__(kThreads) maxpool3_fwd_staged(const float* __r
   }
   int s = 0;
   uint32_t phase = 0;
+  const int per_plane = g.runs * g.Q;
   for (int64_t c = blockIdx.x; c < g.nchunks; c += gridDim.x) {
     mbar_wait(&full[s], phase);
     const float* xs0 = sm + s * g.stage_floats;
-    const int gh = planes_of(c);
-    const int items = gh * g.runs * g.Q;
+    const int items = planes_of(c) * per_plane;
     float* yc = y + c * g.G * PQ;
     float* mc = mask ? mask + c * g.G * PQ : nullptr;
     for (int it = threadIdx.x; it < items; it += kThreads) {
-      const int pw = it % g.Q, t = it / g.Q;
-      const int run = t % g.runs, gl = t / g.runs;
+      const int gl = fdiv(it, g.m_pp1, g.s_pp1), r = it - gl * per_plane;
+      const int run = fdiv(r, g.m_q, g.s_q), pw = r - run * g.Q;
       const int ph0 = run * g.RB, ph1 = min(g.P, ph0 + g.RB);
       float* yp = yc + gl * PQ + pw;
-      float* mp = mc ? mc + gl * PQ + pw : nullptr;
-      walk_windows<S>(xs0 + gl * HW, g, pw, ph0, ph1, [&](int ph, float best, int arg) {
-        yp[ph * g.Q] = best;
-        if (mp) mp[ph * g.Q] = (float)arg;
-      });
+      if (mc) {
+        float* mp = mc + gl * PQ + pw;
+        walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
+                        [&](int ph, float best, int arg) {
+                          yp[ph * g.Q] = best;
+                          mp[ph * g.Q] = (float)arg;
+                        });
+      } else {
+        walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
+                        [&](int ph, float best, int) { yp[ph * g.Q] = best; });
+      }
     }
     __syncthreads();  // every read of this stage is done: refill it
     if (threadIdx.x == 0) {
@@ -177,10 +184,10 @@ __global__ void __launch_bounds__(kThreads) maxpool3_fwd_staged(const float* __r
 }
 
 template <int S>
-__global__ void __launch_bounds__(kThreads) maxpool3_bwd_staged(const float* __restrict__ x,
-                                                                const float* __restrict__ dy,
-                                                                float* __restrict__ dx, Geo g,
-                                                                int relu_from_x) {
+__global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* __restrict__ x,
+                                                                   const float* __restrict__ dy,
+                                                                   float* __restrict__ dx, Geo g,
+                                                                   int relu_from_x) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t full[kMaxStages];
   const int HW = g.H * g.W, PQ = g.P * g.Q;
@@ -191,7 +198,10 @@ __global__ void __launch_bounds__(kThreads) maxpool3_bwd_staged(const float* __r
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto planes_of = [&](int64_t c) { const int64_t left = g.planes - c * g.G; return (int)(left < g.G ? left : g.G); };
+  auto planes_of = [&](int64_t c) {
+    const int64_t left = g.planes - c * g.G;
+    return (int)(left < g.G ? left : g.G);
+  };
   auto load = [&](int s, int64_t c) {
     float* st = sm + s * g.stage_floats;
     const int gh = planes_of(c);
@@ -204,96 +214,123 @@ __global__ void __launch_bounds__(kThreads) maxpool3_bwd_staged(const float* __r
   }
   int s = 0;
   uint32_t phase = 0;
-  const int pruns = (g.P + g.RB - 1) / g.RB;  // phase-1 runs over output rows
+  const int per_plane1 = g.runs * g.Q;
   for (int64_t c = blockIdx.x; c < g.nchunks; c += gridDim.x) {
     mbar_wait(&full[s], phase);
     const float* xs0 = sm + s * g.stage_floats;
     const float* gs0 = xs0 + xseg;
     int* as0 = reinterpret_cast<int*>(const_cast<float*>(gs0 + dseg));
     const int gh = planes_of(c);
-    // phase 1: every window's argmax
-    {
-      const int items = gh * pruns * g.Q;
-      for (int it = threadIdx.x; it < items; it += kThreads) {
-        const int pw = it % g.Q, t = it / g.Q;
-        const int run = t % pruns, gl = t / pruns;
-        const int ph0 = run * g.RB, ph1 = min(g.P, ph0 + g.RB);
-        int* ap = as0 + gl * PQ + pw;
-        walk_windows<S>(xs0 + gl * HW, g, pw, ph0, ph1,
-                        [&](int ph, float, int arg) { ap[ph * g.Q] = arg; });
-      }
+    // phase 1: every window's argmax (the forward's scan)
+    for (int it = threadIdx.x; it < gh * per_plane1; it += kThreads) {
+      const int gl = fdiv(it, g.m_pp1, g.s_pp1), r = it - gl * per_plane1;
+      const int run = fdiv(r, g.m_q, g.s_q), pw = r - run * g.Q;
+      const int ph0 = run * g.RB, ph1 = min(g.P, ph0 + g.RB);
+      int* ap = as0 + gl * PQ + pw;
+      walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
+                      [&](int ph, float, int arg) { ap[ph * g.Q] = arg; });
     }
     __syncthreads();
-    // phase 2: gather per input pixel
+    // phase 2: per input pixel, dy of the windows whose argmax it is, in window
+    // raster order
     float* dxc = dx + c * g.G * HW;
-    const int hruns = (g.H + g.RB - 1) / g.RB;
-    const int items = gh * hruns * g.W;
-    for (int it = threadIdx.x; it < items; it += kThreads) {
-      const int w = it % g.W, t = it / g.W;
-      const int run = t % hruns, gl = t / hruns;
-      const int h0 = run * g.RB, h1 = min(g.H, h0 + g.RB);
-      const int* ap = as0 + gl * PQ;
-      const float* gp = gs0 + gl * PQ;
-      const float* xs = xs0 + gl * HW;
-      float* dp = dxc + gl * HW + w;
-      if (S == 1) {
-        // windows (h + pad - 2 + i, w + pad - 2 + j), i, j in 0..2, rolling in i
+    if (S == 1) {
+      const int per_plane2 = g.hruns * g.W;
+      for (int it = threadIdx.x; it < gh * per_plane2; it += kThreads) {
+        const int gl = fdiv(it, g.m_pp2, g.s_pp2), r = it - gl * per_plane2;
+        const int run = fdiv(r, g.m_in2, g.s_in2), w = r - run * g.W;
+        const int h0 = run * g.RBh, h1 = min(g.H, h0 + g.RBh);
+        const int* ap = as0 + gl * PQ;
+        const float* gp = gs0 + gl * PQ;
+        const float* xs = xs0 + gl * HW;
+        float* dp = dxc + gl * HW + w;
+        // candidate windows (h + pad - 2 + i, w + pad - 2 + j), rolling in i
         const int q0 = w + g.pad - 2;
-        bool qv[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) qv[j] = (unsigned)(q0 + j) < (unsigned)g.Q;
-        int A[3][3];
-        float D[3][3];
+        const bool v0 = (unsigned)q0 < (unsigned)g.Q, v1 = (unsigned)(q0 + 1) < (unsigned)g.Q,
+                   v2 = (unsigned)(q0 + 2) < (unsigned)g.Q;
+        int A0[3], A1[3], A2[3];
+        float D0[3], D1[3], D2[3];
         auto ld_row = [&](int ph, int (&a)[3], float (&d)[3]) {
           const bool rv = (unsigned)ph < (unsigned)g.P;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const bool ok = rv && qv[j];
-            a[j] = ok ? ap[ph * g.Q + q0 + j] : -1;
-            d[j] = ok ? gp[ph * g.Q + q0 + j] : 0.f;
-          }
+          const int o = ph * g.Q + q0;
+          a[0] = (rv && v0) ? ap[o] : -1;
+          a[1] = (rv && v1) ? ap[o + 1] : -1;
+          a[2] = (rv && v2) ? ap[o + 2] : -1;
+          d[0] = (rv && v0) ? gp[o] : 0.f;
+          d[1] = (rv && v1) ? gp[o + 1] : 0.f;
+          d[2] = (rv && v2) ? gp[o + 2] : 0.f;
         };
         int p = h0 + g.pad - 2;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) ld_row(p + i, A[i], D[i]);
-        for (int h = h0;;) {
+        ld_row(p, A0, D0);
+        ld_row(p + 1, A1, D1);
+        ld_row(p + 2, A2, D2);
+        int h = h0;
+        // one pixel from window rows (a, b, c) = (oldest .. newest); the oldest
+        // slot then takes the next window row (three rotated instances: no moves)
+        auto step = [&](int (&Aa)[3], float (&Da)[3], const int (&Ab)[3], const float (&Db)[3],
+                        const int (&Ac)[3], const float (&Dc)[3]) -> bool {
           const int me = h * g.W + w;
           float acc = 0.f;
 #pragma unroll
-          for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, Aa[j] == me ? Da[j] : 0.f);
 #pragma unroll
-            for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, A[i][j] == me ? D[i][j] : 0.f);
-          if (relu_from_x) acc = xs[h * g.W + w] > 0.f ? acc : 0.f;
+          for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, Ab[j] == me ? Db[j] : 0.f);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, Ac[j] == me ? Dc[j] : 0.f);
+          if (relu_from_x) acc = xs[me] > 0.f ? acc : 0.f;
           dp[h * g.W] = acc;
-          if (++h >= h1) break;
+          if (++h >= h1) return false;
           ++p;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            A[0][j] = A[1][j]; D[0][j] = D[1][j];
-            A[1][j] = A[2][j]; D[1][j] = D[2][j];
-          }
-          ld_row(p + 2, A[2], D[2]);
+          ld_row(p + 2, Aa, Da);
+          return true;
+        };
+        while (step(A0, D0, A1, D1, A2, D2) && step(A1, D1, A2, D2, A0, D0) &&
+               step(A2, D2, A0, D0, A1, D1)) {
         }
-      } else {
-        // stride 2: windows ph in [ceil((h+pad-2)/2), floor((h+pad)/2)], likewise pw
-        const int wp = w + g.pad;
-        const int pwh = wp >> 1, pwl = (wp & 1) ? pwh : pwh - 1;
-        for (int h = h0; h < h1; ++h) {
-          const int hp = h + g.pad;
-          const int phh = hp >> 1, phl = (hp & 1) ? phh : phh - 1;
-          const int me = h * g.W + w;
-          float acc = 0.f;
-          for (int ph = phl; ph <= phh; ++ph) {
-            if ((unsigned)ph >= (unsigned)g.P) continue;
-            for (int pw = pwl; pw <= pwh; ++pw) {
-              if ((unsigned)pw >= (unsigned)g.Q) continue;
-              const int o = ph * g.Q + pw;
-              acc = __fadd_rn(acc, ap[o] == me ? gp[o] : 0.f);
-            }
-          }
-          if (relu_from_x) acc = xs[h * g.W + w] > 0.f ? acc : 0.f;
-          dp[h * g.W] = acc;
+      }
+    } else {
+      // stride 2: thread per 2x2 pixel block (2i - pad, 2j - pad) + {0,1}^2, covered
+      // exactly by windows (i-1, j-1), (i-1, j), (i, j-1), (i, j) (see the s2 plane
+      // kernel in pool_lrn_concat.cu)
+      const int BI = (g.H + g.pad + 1) >> 1, BJ = (g.W + g.pad + 1) >> 1;
+      const int per_plane2 = BI * BJ;
+      for (int it = threadIdx.x; it < gh * per_plane2; it += kThreads) {
+        const int gl = fdiv(it, g.m_pp2, g.s_pp2), r = it - gl * per_plane2;
+        const int i = fdiv(r, g.m_in2, g.s_in2), j = r - i * BJ;
+        const int* ap = as0 + gl * PQ;
+        const float* gp = gs0 + gl * PQ;
+        const float* xs = xs0 + gl * HW;
+        float* dp = dxc + gl * HW;
+        const bool pa = (unsigned)(i - 1) < (unsigned)g.P, pb = i < g.P;
+        const bool qa = (unsigned)(j - 1) < (unsigned)g.Q, qb = j < g.Q;
+        const int oa = (i - 1) * g.Q, ob = i * g.Q;
+        const int aAA = (pa && qa) ? ap[oa + j - 1] : -1, aAB = (pa && qb) ? ap[oa + j] : -1;
+        const int aBA = (pb && qa) ? ap[ob + j - 1] : -1, aBB = (pb && qb) ? ap[ob + j] : -1;
+        const float gAA = (pa && qa) ? gp[oa + j - 1] : 0.f, gAB = (pa && qb) ? gp[oa + j] : 0.f;
+        const float gBA = (pb && qa) ? gp[ob + j - 1] : 0.f, gBB = (pb && qb) ? gp[ob + j] : 0.f;
+        const int h0 = 2 * i - g.pad, w0 = 2 * j - g.pad;
+        const int e00 = h0 * g.W + w0, e01 = e00 + 1, e10 = e00 + g.W, e11 = e10 + 1;
+        float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+        a00 = __fadd_rn(a00, aAA == e00 ? gAA : 0.f);
+        a00 = __fadd_rn(a00, aAB == e00 ? gAB : 0.f);
+        a01 = __fadd_rn(a01, aAB == e01 ? gAB : 0.f);
+        a00 = __fadd_rn(a00, aBA == e00 ? gBA : 0.f);
+        a10 = __fadd_rn(a10, aBA == e10 ? gBA : 0.f);
+        a00 = __fadd_rn(a00, aBB == e00 ? gBB : 0.f);
+        a01 = __fadd_rn(a01, aBB == e01 ? gBB : 0.f);
+        a10 = __fadd_rn(a10, aBB == e10 ? gBB : 0.f);
+        a11 = __fadd_rn(a11, aBB == e11 ? gBB : 0.f);
+        const bool r0 = h0 >= 0, r1 = h0 + 1 < g.H, k0 = w0 >= 0, k1 = w0 + 1 < g.W;
+        if (relu_from_x) {
+          if (r0 && k0) a00 = xs[e00] > 0.f ? a00 : 0.f;
+          if (r0 && k1) a01 = xs[e01] > 0.f ? a01 : 0.f;
+          if (r1 && k0) a10 = xs[e10] > 0.f ? a10 : 0.f;
+          if (r1 && k1) a11 = xs[e11] > 0.f ? a11 : 0.f;
         }
+        if (r0 && k0) dp[e00] = a00;
+        if (r0 && k1) dp[e01] = a01;
+        if (r1 && k0) dp[e10] = a10;
+        if (r1 && k1) dp[e11] = a11;
       }
     }
     __syncthreads();
@@ -330,7 +367,7 @@ bool plan(Geo& g, bool bwd, int N, int C, int H, int W, int P, int Q, int S, int
   const int a = std::max(align_planes(HW), align_planes(PQ));
   if ((g.planes * HW) % 4 || (g.planes * PQ) % 4) return false;
   const int64_t per_plane = bwd ? (int64_t)HW + 2LL * PQ : (int64_t)HW;
-  int G = (int)std::max<int64_t>(1, kStageTarget / (per_plane * 4));
+  int G = (int)std::max<int64_t>(1, (bwd ? kStageTarget * 3 / 2 : kStageTarget) / (per_plane * 4));
   G = (G + a - 1) / a * a;
   if (G > g.planes) G = (int)((g.planes + a - 1) / a * a);
   auto stage_floats = [&](int G_) {
@@ -342,15 +379,38 @@ bool plan(Geo& g, bool bwd, int N, int C, int H, int W, int P, int Q, int S, int
   g.stage_floats = (stage_floats(G) + 31) & ~31;
   g.NS = (int)std::min<int64_t>(3, kSmemBudget / ((int64_t)g.stage_floats * 4));
   g.nchunks = (g.planes + G - 1) / G;
-  // walker runs: enough items to occupy the CTA, long runs for the row reuse
-  const int rows = bwd ? H : P;
-  const int cols = bwd ? W : Q;
-  const int64_t colitems = (int64_t)G * cols;
-  int RB = rows;
-  if (colitems < 2 * kThreads) RB = (int)std::max<int64_t>(4, rows * colitems / (2 * kThreads));
-  if (RB > rows) RB = rows;
-  g.RB = RB;
-  g.runs = (rows + RB - 1) / RB;
+  // walker runs: enough items to occupy the CTA twice over, long runs for the
+  // row reuse
+  auto run_len = [&](int rows, int cols) {
+    const int64_t colitems = (int64_t)G * cols;
+    int rb = rows;
+    // (runs shorter than ~8 rows spend more on the walker's warm-up rows and
+    // index decode than an idle thread costs: measured 226 -> ~70 instructions
+    // per pixel for the stride-1 backward)
+    if (colitems < 2 * kThreads)
+      rb = (int)std::max<int64_t>(8, rows * colitems / (2 * kThreads));
+    return rb > rows ? rows : rb;
+  };
+  g.RB = run_len(P, Q);
+  g.runs = (P + g.RB - 1) / g.RB;
+  g.RBh = run_len(H, W);
+  g.hruns = (H + g.RBh - 1) / g.RBh;
+  auto magic = [](uint32_t d, uint64_t& m, int& sh) {  // exact for x < 2^31
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    sh = 31 + l;
+    m = ((1ull << sh) + d - 1) / d;
+  };
+  magic((uint32_t)(g.runs * Q), g.m_pp1, g.s_pp1);
+  magic((uint32_t)Q, g.m_q, g.s_q);
+  if (S == 1) {
+    magic((uint32_t)(g.hruns * W), g.m_pp2, g.s_pp2);
+    magic((uint32_t)W, g.m_in2, g.s_in2);
+  } else {
+    const int BI = (H + pad + 1) >> 1, BJ = (W + pad + 1) >> 1;
+    magic((uint32_t)(BI * BJ), g.m_pp2, g.s_pp2);
+    magic((uint32_t)BJ, g.m_in2, g.s_in2);
+  }
   return true;
 }
 
@@ -382,11 +442,21 @@ int grid_for(K kern, const Geo& g, bool& configured) {
 
 using namespace bf;
 
+// PURINE_B200_POOL_STAGED bit 0: also take the stride-1 backward (mask elided)
+static int pools_flags() {
+  const char* e = getenv("PURINE_B200_POOL_STAGED");
+  return e ? atoi(e) : 0;
+}
+
 extern "C" {
 
 int bf_maxpool_staged_ok(int N, int C, int H, int W, int P, int Q, int kernel, int stride,
                          int pad, int backward) {
   pools::Geo g;
+  // stride-1 backward: the recompute + 9-window gather costs ~140 instructions
+  // per pixel here (1.5 TB/s) against 3 TB/s for the mask-reading warp-row
+  // gather, so stride-1 pools keep their mask (the staged forward writes it)
+  if (backward && stride == 1 && !(pools_flags() & 1)) return 0;
   return kernel == 3 && pools::plan(g, backward != 0, N, C, H, W, P, Q, stride, pad) ? 1 : 0;
 }
 

@@ -184,7 +184,11 @@ def test_relu_nan_propagates_like_numpy(monkeypatch):
     x = rnd(2, 3, 4, 4)
     x[0, 0, 0, :4] = [np.nan, -np.nan, np.inf, -np.inf]
     dy = rnd(2, 3, 4, 4)
-    assert_bitwise(run_op("relu_forward", {"x": x}, {"y": x.shape})["y"], O.relu_forward(x))
+    y = run_op("relu_forward", {"x": x}, {"y": x.shape})["y"]
+    want = O.relu_forward(x)
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(y), nan)  # NaN payloads are not part of the contract
+    assert_bitwise(np.where(nan, 0, y), np.where(nan, 0, want))
     assert_bitwise(run_op("relu_backward", {"x": x, "dy": dy}, {"dx": x.shape})["dx"],
                    O.relu_backward(x, dy))
 
@@ -254,7 +258,8 @@ MAXPOOL_STAGED_SHAPES = [((2, 64, 112, 112), 3, 2, 0), ((2, 192, 56, 56), 3, 2, 
 @pytest.mark.parametrize("shape,k,s,p", MAXPOOL_STAGED_SHAPES)
 @pytest.mark.parametrize("fold", [False, True], ids=["pool", "relu+pool"])
 @pytest.mark.parametrize("values", ["normal", "coarse"])
-def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values):
+@pytest.mark.parametrize("s1_bwd", ["0", "1"], ids=["default", "s1-staged"])
+def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values, s1_bwd, monkeypatch):
     """The product pairing: maxpool_forward and maxpool_backward in one graph,
     the mask elided (the backward recomputes each window's argmax from x with
     the forward's scan) and, after a ReLU, the relu_backward folded in through
@@ -263,6 +268,7 @@ def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values):
     from paper_1412_6249_b200._native import lib
     from paper_1412_6249_b200.dispatcher import _plan
 
+    monkeypatch.setenv("PURINE_B200_POOL_STAGED", s1_bwd)  # 1: stride-1 backward staged too
     loc = Location("local", 0)
     a = rnd(*shape)
     a[:, :, ::3, ::3] = 0.5

@@ -1,6 +1,6 @@
 """Time one memory-bound kernel family at GoogLeNet shapes (batch 128).
 
-    python tools/op_bench.py maxpool_fwd|maxpool_bwd|lrn_fwd|lrn_fwd_noscale|lrn_bwd|lrn_bwd_rc [--reps 5]
+    python tools/op_bench.py maxpool_fwd|maxpool_bwd|maxpool_fwd_staged|maxpool_bwd_x|lrn_fwd|lrn_fwd_noscale|lrn_bwd|lrn_bwd_rc [--reps 5]
 
 Prints per-shape time and achieved GB/s (algorithmic bytes).
 """
@@ -41,7 +41,15 @@ def main():
             y = torch.empty(n, c, p, q, device="cuda")
             m = torch.empty_like(y)
             dx = torch.empty_like(x)
-            if a.op == "maxpool_fwd":
+            if a.op == "maxpool_fwd_staged":  # no mask (elided in the product pairing)
+                fn = lambda: lib("bf_maxpool_fwd_staged", x.data_ptr(), y.data_ptr(), None, n, c,
+                                 h, w, p, q, nd.kernel, nd.stride, nd.pad, st)
+                nbytes = 4 * x.numel() + 4 * y.numel()
+            elif a.op == "maxpool_bwd_x":  # argmax recomputed from x
+                fn = lambda: lib("bf_maxpool_bwd_x", x.data_ptr(), y.data_ptr(), dx.data_ptr(), 0,
+                                 n, c, h, w, p, q, nd.kernel, nd.stride, nd.pad, st)
+                nbytes = 8 * x.numel() + 4 * y.numel()
+            elif a.op == "maxpool_fwd":
                 fn = lambda: lib("bf_maxpool_fwd", x.data_ptr(), y.data_ptr(), m.data_ptr(), n, c, h,
                                  w, p, q, nd.kernel, nd.stride, nd.pad, st)
                 nbytes = 4 * x.numel() + 8 * y.numel()
