@@ -176,25 +176,69 @@ struct EpiNCHW {
     *p = v;
     if (relu_out) p[r.relu_delta] = relu_value(v);
   }
-  // 16 consecutive columns of one row (the tcgen05 epilogues): the folded
-  // ReLU's x values are all loaded before any store, so the loads overlap
+  // 16 consecutive columns of one row (the tcgen05 epilogues).  Column j of
+  // the row lives PQ elements after column j-1, so the address advances by a
+  // constant; each optional feature is tested once per chunk (not per
+  // element), full chunks skip the per-column bound, and the stores are
+  // st.global.  (ncu, 1x1 data gradient: the per-element form cost ~28
+  // instructions per output -- reloaded parameters, 64-bit multiplies, a
+  // branch per column, generic stores -- 67% of the kernel's instructions.)
   __device__ __forceinline__ void store16(const RowPtr& r, int n0, const uint32_t (&v)[16],
                                           int nlim) const {
-    float m[16];
-    if (relu_x) {
-      const float* mx = relu_x + (r.p - out) + (int64_t)n0 * PQ;
+    const int64_t stride = PQ;
+    float* p = r.p + (int64_t)n0 * stride;
+    const float* rx = relu_x;
+    const float* bs = bias;
+    float* ro = relu_out;
+    if (nlim >= 16 && !rx && !ro) {
+      if (bs) {
+        float b[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) m[j] = j < nlim ? __ldg(mx + (int64_t)j * PQ) : 0.f;
+        for (int j = 0; j < 16; ++j) b[j] = __ldg(bs + n0 + j);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) __stcg(p + j * stride, __fadd_rn(__uint_as_float(v[j]), b[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) __stcg(p + j * stride, __uint_as_float(v[j]));
+      }
+      return;
+    }
+    if (nlim >= 16 && !rx) {  // forward with the fused ReLU output
+      const int64_t rd = r.relu_delta;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float x = __uint_as_float(v[j]);
+        if (bs) x = __fadd_rn(x, __ldg(bs + n0 + j));
+        __stcg(p + j * stride, x);
+        __stcg(p + j * stride + rd, relu_value(x));
+      }
+      return;
+    }
+    if (nlim >= 16 && !bs && !ro) {  // data gradient with the ReLU backward folded in:
+      // the folded ReLU's x values are all loaded before any store (overlap)
+      const float* mx = rx + (p - out);
+      float m[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) m[j] = __ldg(mx + j * stride);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) __stcg(p + j * stride, m[j] > 0.f ? __uint_as_float(v[j]) : 0.f);
+      return;
+    }
+    // general form: partial chunk or an unusual feature mix
+    float m[16];
+    if (rx) {
+      const float* mx = rx + (p - out);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) m[j] = j < nlim ? __ldg(mx + j * stride) : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (j >= nlim) continue;
       float x = __uint_as_float(v[j]);
-      if (bias) x = __fadd_rn(x, __ldg(bias + n0 + j));
-      if (relu_x) x = m[j] > 0.f ? x : 0.f;
-      float* p = r.p + (int64_t)(n0 + j) * PQ;
-      *p = x;
-      if (relu_out) p[r.relu_delta] = relu_value(x);
+      if (bs) x = __fadd_rn(x, __ldg(bs + n0 + j));
+      if (rx) x = m[j] > 0.f ? x : 0.f;
+      __stcg(p + j * stride, x);
+      if (ro) __stcg(p + j * stride + r.relu_delta, relu_value(x));
     }
   }
 };
@@ -215,9 +259,20 @@ struct EpiT {
   }
   __device__ __forceinline__ void store16(const RowPtr& r, int n0, const uint32_t (&v)[16],
                                           int nlim) const {
+    float* p = r.p + (int64_t)n0 * ldo;
+    if (bias) {  // (no bias: the value is stored as is, -0 included)
+      const float b = r.bias_row;
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < nlim) store(r, n0 + j, __uint_as_float(v[j]));
+      for (int j = 0; j < 16; ++j)
+        if (j < nlim) __stcg(p + j * ldo, __fadd_rn(__uint_as_float(v[j]), b));
+    } else if (nlim >= 16) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) __stcg(p + j * ldo, __uint_as_float(v[j]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nlim) __stcg(p + j * ldo, __uint_as_float(v[j]));
+    }
   }
 };
 
@@ -233,6 +288,19 @@ struct EpiPartial {
   }
   __device__ __forceinline__ void store(const RowPtr& r, int n, float v) const {
     r.p[(int64_t)n * M] = v;
+  }
+  __device__ __forceinline__ void store16(const RowPtr& r, int n0, const uint32_t (&v)[16],
+                                          int nlim) const {
+    const int64_t stride = M;
+    float* p = r.p + (int64_t)n0 * stride;
+    if (nlim >= 16) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) __stcg(p + j * stride, __uint_as_float(v[j]));
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nlim) __stcg(p + j * stride, __uint_as_float(v[j]));
   }
 };
 

@@ -1090,9 +1090,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         if (live) {
           const int nlim = w.N - (n0 + c0);
           if (w.splits > 1) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (j < nlim) part.store(rp, n0 + c0 + j, __uint_as_float(v[j]));
+            part.store16(rp, n0 + c0, v, nlim);
           } else {
             epi.store16(rp, n0 + c0, v, nlim);
           }
