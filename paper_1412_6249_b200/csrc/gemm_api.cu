@@ -77,6 +77,10 @@ int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, flo
     int rc = tc4_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
     if (rc >= 0) return rc;
   }
+  if (g_gemm_engine == 0) {
+    int rc = s2d_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
+    if (rc >= 0) return rc;
+  }
   if (g_gemm_engine == 3) {
     int rc = tc3_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
     if (rc >= 0) return rc;
@@ -140,7 +144,10 @@ int bf_conv2d_bwd_weight_bias(const float* x, const float* dy, float* dw, float*
   EpiT epi{dw, nullptr, (int64_t)C * R * S};
   int rc = -1;
   bool db_done = false;
-  if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3 || g_gemm_engine == 4)
+  if (g_gemm_engine == 0)
+    rc = s2d_conv_wgrad(g, x, dy, dw, db, &db_done, ws, ws_bytes, as_stream(s),
+                        "conv2d_backward_weight");
+  if (rc < 0 && (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3 || g_gemm_engine == 4))
     rc = tc2_conv_wgrad(la, lb, C * R * S, K, N * P * Q, epi, ws, ws_bytes, as_stream(s),
                         "conv2d_backward_weight", db, &db_done);
   if (rc < 0)

@@ -39,6 +39,14 @@ int tc4_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNC
 int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
                    float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 
+// strided convolutions (C*stride^2 <= 64 channels, kernel wider than the
+// stride) as stride-1 convolutions over a space-to-depth view (conv_s2d.cu)
+int s2d_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNCHW& epi,
+                 float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+int s2d_conv_wgrad(const ConvShape& g, const float* x, const float* dy, float* dw, float* db,
+                   bool* db_done, float* ws, int64_t ws_bytes, cudaStream_t st,
+                   const char* what);
+
 extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in),
                            // 4 auto without v4, 5 auto without the TMA-fed 1x1 weight gradient,
                            // 6 auto with register-prefetched (not cp.async-staged) gathers,

@@ -52,21 +52,25 @@ CONV_CASES = [
 ]
 
 
-@pytest.fixture(params=[0, 3, 4, 5, 6, 7],
+@pytest.fixture(params=[0, 3, 4, 5, 6, 7, 8],
                 ids=["auto", "halo-v3", "no-tma-1x1", "no-tma-wgrad", "reg-prefetch",
-                     "tma-dy-wgrad"])
-def gemm_engine(request):
+                     "tma-dy-wgrad", "s2d"])
+def gemm_engine(request, monkeypatch):
     """0 = default engine choice (1x1 convolutions through the TMA-fed engine
     v4, gemm_tc4.cu); 3 = also route stride-1 R x S convolutions through the
     opt-in halo-staged engine v3 (gemm_tc3.cu); 4 = 1x1 convolutions through
     the gathering engine v2 instead of v4; 5 = 1x1 weight gradients gathered
     instead of TMA-fed; 6 = engine v2 gathers prefetched in registers instead
     of cp.async-staged; 7 = also stream the raw dY by TMA for 16-aligned-row
-    weight gradients (conv1 type, opt-in mode kWgradTma)."""
+    weight gradients (conv1 type, opt-in mode kWgradTma); 8 = engine 0 with
+    strided convolutions through the opt-in space-to-depth view
+    (PURINE_B200_S2D=1, conv_s2d.cu)."""
     from paper_1412_6249_b200 import _native
 
     lib = _native.lib()
-    lib("bf_set_gemm_engine", request.param)
+    if request.param == 8:
+        monkeypatch.setenv("PURINE_B200_S2D", "1")
+    lib("bf_set_gemm_engine", 0 if request.param == 8 else request.param)
     yield request.param
     lib("bf_set_gemm_engine", 0)
 
@@ -78,6 +82,8 @@ def test_conv_forward_backward(case, gemm_engine):
         pytest.skip("engine v3 only takes stride-1 spatial filters")
     if gemm_engine in (4, 5) and r != 1:
         pytest.skip("engine switches 4 and 5 only change 1x1 convolutions")
+    if gemm_engine == 8 and not (s >= 2 and r > s and c * s * s <= 64):
+        pytest.skip("the space-to-depth view only takes strided convolutions on few channels")
     x = rnd(n, c, h, w)
     wt = rnd(k, c, r, r, scale=1.0 / np.sqrt(c * r * r))
     b = rnd(k)
