@@ -60,5 +60,7 @@ inline bool tc2_async_gather_enabled() { return g_gemm_engine != 6; }
 // GoogLeNet step (9700 img/s either way) and 5% slower for conv1 alone: the
 // producers, already issue-bound on the gather, also split the B tile
 inline bool tc2_wgrad_tma_enabled() { return g_gemm_engine == 7; }
+// weight-gradient units split-major (PURINE_B200_SPLIT_OUTER, default 1)
+bool tc2_split_outer();
 
 }  // namespace bf

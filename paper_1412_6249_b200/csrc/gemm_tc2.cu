@@ -30,6 +30,8 @@
 // per instruction even in straight-line code, and 110-150 cycles when each
 // instruction recomputes its descriptors and predicate; the issuer therefore
 // uses precomputed descriptor bases and literal accumulate flags.
+#include <stdlib.h>
+
 #include <algorithm>
 #include <type_traits>
 
@@ -39,6 +41,12 @@
 
 
 namespace bf {
+
+bool tc2_split_outer() {
+  const char* e = getenv("PURINE_B200_SPLIT_OUTER");
+  return !(e && *e && atoi(e) == 0);
+}
+
 namespace tc2 {
 
 constexpr int BK = 32;
@@ -314,6 +322,10 @@ struct Work {
   // weight-gradient fast path: x / (Pp*Qp) = (x * per_m) >> per_s, x / Qp likewise
   uint64_t per_m, qp_m;
   int per_s, qp_s;
+  // weight gradients: units ordered split-major (m-tile fastest), so the
+  // m-tiles sharing a k-range -- and its dY tiles -- run at the same time and
+  // the dY pack is read from L2 once per k-range instead of once per m-tile
+  int split_outer;
 };
 
 // multiply-shift constants for exact unsigned division by d of any x < 2^31
@@ -345,6 +357,11 @@ __device__ __forceinline__ void divmod_u(int x, int d, int& q, int& r) {
 }
 __device__ __forceinline__ void unit_coords(const Work& w, int u, int& mt, int& nt, int& sp) {
   int r;
+  if (w.split_outer) {  // u = (sp * ntiles + nt) * mtiles + mt
+    divmod_u(u, w.mtiles, r, mt);
+    divmod_u(r, w.ntiles, sp, nt);
+    return;
+  }
   divmod_u(u, w.splits, r, sp);
   divmod_u(r, w.ntiles, mt, nt);
 }
@@ -1190,6 +1207,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
   w.splits = (w.nkb + w.kbps - 1) / w.kbps;
   w.units = w.mtiles * w.ntiles * w.splits;
+  w.split_outer = std::is_same_v<LBP, LdWgradDYPad> && tc2_split_outer();
 
   const int smem_cap = 227 * 1024;
   const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
@@ -1315,6 +1333,7 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
   w.splits = (w.nkb + w.kbps - 1) / w.kbps;
   w.units = w.mtiles * w.ntiles * w.splits;
+  w.split_outer = tc2_split_outer();
   constexpr int AD = 4;
   const int smem_cap = 227 * 1024;
   const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
@@ -1392,6 +1411,7 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
   w.splits = (w.nkb + w.kbps - 1) / w.kbps;
   w.units = w.mtiles * w.ntiles * w.splits;
+  w.split_outer = tc2_split_outer();
   const int smem_cap = 227 * 1024;
   const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
   const int ktab_bytes = STAGES * BK * 8;

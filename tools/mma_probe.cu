@@ -45,7 +45,34 @@ __global__ void probe(int n, int iters, int mode, int per, unsigned long long* o
   tc_fence_after();
   const uint32_t tmem = tslot;
   unsigned long long t0 = 0, t1 = 0;
-  if (threadIdx.x == 0) {
+  if (mode >= 8) {  // `per` issuing warps (lane 0 each), each into its own accumulator
+    __shared__ __align__(8) uint64_t bars[4];
+    if (threadIdx.x == 0) {
+      for (int b = 0; b < 4; ++b) mbar_init(&bars[b], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp < per && (threadIdx.x & 31) == 0) {
+      const uint32_t idesc = tf32_idesc(n);
+      const uint32_t bsm = smem_u32(smem);
+      uint64_t bdv[4];
+      for (int k = 0; k < 4; ++k) bdv[k] = sw128_desc(bsm + k * 32);
+      const uint32_t dcol = tmem + (uint32_t)(warp * (256 / per)), acol = tmem + 256 + warp * 32;
+      mma_ts(dcol, acol, bdv[0], idesc, 0u);
+      const unsigned long long s0 = clock64();
+      for (int i = 0; i < iters / per; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(dcol),
+                       "r"(acol + (u & 3) * 8), "l"(bdv[u & 3]), "r"(idesc)
+                       : "memory");
+      }
+      tc_commit(&bars[warp]);
+      mbar_wait(&bars[warp], 0);
+      const unsigned long long s1 = clock64();
+      if (warp == 0) out[blockIdx.x] = s1 - s0;
+    }
+  } else if (threadIdx.x == 0) {
     const uint32_t idesc = tf32_idesc(n);
     const uint32_t bsm = smem_u32(smem);
     const uint32_t asm_ = bsm + 32768;
@@ -135,10 +162,11 @@ int main() {
   struct Cfg { const char* name; int mode, per; };
   const Cfg cfgs[] = {{"ts", 0, 1}, {"ss", 1, 1}, {"ts+sync/12", 2, 12}, {"ts x2 acc", 3, 2},
                       {"ts unrolled", 4, 1}, {"ts unr x2acc", 5, 2}, {"kblk 0 commit", 6, 0},
-                      {"kblk 1 commit", 6, 1}, {"kblk 2 commit", 6, 2}};
+                      {"kblk 1 commit", 6, 1}, {"kblk 2 commit", 6, 2},
+                      {"2 issuers", 8, 2}, {"4 issuers", 8, 4}};
   for (const Cfg& c : cfgs) {
     for (int n : {32, 64, 128, 192, 256}) {
-      if ((c.mode == 3 || c.mode == 5) && c.per * n > 256) continue;
+      if ((c.mode == 3 || c.mode == 5 || c.mode == 8) && c.per * n > 256) continue;
       probe<<<148, 128, 100 * 1024>>>(n, iters, c.mode, c.per, d);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) {
