@@ -50,6 +50,8 @@ def _args():
                     help="route the exchange through NCCL even on one GPU (plumbing test)")
     ap.add_argument("--op-table", default=None,
                     help="write the traced replay's per-operator device times (TSV) here")
+    ap.add_argument("--intervals", default=None,
+                    help="write the branch-concurrent traced replay's operator intervals (TSV)")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="extra replays for an external profiler (ncu); no timing")
     return ap.parse_args()
@@ -505,6 +507,11 @@ def run_ours(args):
         cexe.step()
     torch.cuda.synchronize()
     iv = cexe.op_intervals_ns(cpar)
+    if args.intervals and rank == 0:
+        with open(args.intervals, "w") as f:
+            f.write("op\tkind\tstart_ns\tend_ns\n")
+            for _gi, op, s0, s1 in iv:
+                f.write(f"{op.name}\t{op.kind}\t{s0}\t{s1}\n")
     comm_sp = [(s0, s1) for _, op, s0, s1 in iv if op.kind in ("dp_exchange", "copy")]
     comp_sp = [(s0, s1) for _, op, s0, s1 in iv if op.kind not in ("dp_exchange", "copy", "swap")]
     t_iter = (max(s1 for *_, s1 in iv) - min(s0 for _, _, s0, _ in iv)) if iv else 0

@@ -114,6 +114,16 @@ __global__ void avgpool_fwd_kernel(const float* __restrict__ x, float* __restric
   }
 }
 
+// global average pooling (window = the whole plane, one output per plane):
+// every input pixel gets 0 + dy / f32(H*W), the general kernel's arithmetic
+// without its per-element 64-bit index divisions and window loops
+__global__ void avgpool_global_bwd_kernel(const float* __restrict__ dy, float* __restrict__ dx,
+                                          uint32_t total, uint32_t HW, float cnt) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += gridDim.x * blockDim.x)
+    dx[i] = __fadd_rn(0.f, __fdiv_rn(__ldg(dy + i / HW), cnt));
+}
+
 __global__ void avgpool_bwd_kernel(const float* __restrict__ dy, float* __restrict__ dx,
                                    int64_t total, int H, int W, int P, int Q, int k, int stride,
                                    int pad) {
@@ -1464,6 +1474,11 @@ int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P
                    int kernel, int stride, int pad, bf_stream_t s) {
   int64_t total = (int64_t)N * C * H * W;
   if (total <= 0) return 0;
+  if (P == 1 && Q == 1 && pad == 0 && kernel == H && kernel == W && total < (1LL << 31)) {
+    avgpool_global_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
+        dy, dx, (uint32_t)total, (uint32_t)(H * W), (float)(H * W));
+    return check_launch("avgpool_backward");
+  }
   avgpool_bwd_kernel<<<elementwise_grid(total, kThreads), kThreads, 0, as_stream(s)>>>(
       dy, dx, total, H, W, P, Q, kernel, stride, pad);
   return check_launch("avgpool_backward");
