@@ -29,6 +29,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "gemm_common.cuh"
@@ -36,6 +38,12 @@
 #include "tc_ptx.cuh"
 
 namespace bf {
+
+static bool tc4_sacc_enabled() {
+  const char* e = getenv("PURINE_B200_SACC");
+  return !(e && *e && atoi(e) == 0);
+}
+
 namespace tc4 {
 
 using namespace tcu;
@@ -51,6 +59,8 @@ struct Work {
   int PQ, tiles_img, N_img, Nout, K, BN, ntiles, nkb, kbps, splits, units, nst, nacc;
   int stage_bytes, b_bytes;
   int tmem_cols;  // 512, or 256 when two CTAs share an SM (two MMA issuers)
+  int sacc;       // 1: separate small-term accumulator (see the MMA issuer)
+  int accw;       // TMEM columns per accumulator buffer (BN, or 2*BN with sacc)
 };
 
 // MN-major tf32 operand: the only smem layout the tensor core accepts is
@@ -201,6 +211,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     {
       // A MN-major (bit 15), B K-major; M = 128, N = BN
       const uint32_t idesc = tf32_idesc(BN) | (1u << 15);
+      // sacc: the B stage holds [B big rows | B small rows] contiguously, so ONE
+      // N = 2*BN instruction computes A_big*B_big into columns [0, BN) and
+      // A_big*B_small into [BN, 2BN); A_small*B_big accumulates into [BN, 2BN)
+      // too.  Two instructions per k-step instead of three (the narrow tiles
+      // are issue-bound), and the big accumulator takes one round-toward-zero
+      // accumulation per k-step instead of three (the small terms' own
+      // truncation is 2^-11 smaller); the epilogue adds the halves in fp32 RN.
+      const uint32_t idesc2 = tf32_idesc(2 * BN) | (1u << 15);
       int rs = 0, local = 0;
       uint32_t rph = 0;
       for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
@@ -211,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t use = local / w.nacc;
         mbar_wait(&acc_empty[b], (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t dacc = tmem + (uint32_t)(b * BN);
+        const uint32_t dacc = tmem + (uint32_t)(b * w.accw);
         for (int i = 0; i < nk; ++i) {
           const int s = rs;
           const uint32_t sph = rph;
@@ -227,18 +245,33 @@ __global__ void __launch_bounds__(kThreads, 2)
           const uint64_t bsmall = sw128_desc(st + 2 * kABytes + BN * 128);
           if (elect_one()) {
             // k-step ks (8 K rows): A start + 1 KB (two 4-row atoms), B start + 32 B
-            if (i == 0)
-              mma_ss<0>(dacc, asmall, bbig, idesc);
-            else
-              mma_ss<1>(dacc, asmall, bbig, idesc);
-            mma_ss<1>(dacc, abig, bsmall, idesc);
-            mma_ss<1>(dacc, abig, bbig, idesc);
+            if (w.sacc) {
+              const uint32_t dsm = dacc + (uint32_t)BN;
+              if (i == 0)
+                mma_ss<0>(dacc, abig, bbig, idesc2);
+              else
+                mma_ss<1>(dacc, abig, bbig, idesc2);
+              mma_ss<1>(dsm, asmall, bbig, idesc);
 #pragma unroll
-            for (int ks = 1; ks < BK / 8; ++ks) {
-              const uint64_t ak = (uint64_t)((ks * 1024) >> 4), bk = (uint64_t)((ks * 32) >> 4);
-              mma_ss<1>(dacc, asmall + ak, bbig + bk, idesc);
-              mma_ss<1>(dacc, abig + ak, bsmall + bk, idesc);
-              mma_ss<1>(dacc, abig + ak, bbig + bk, idesc);
+              for (int ks = 1; ks < BK / 8; ++ks) {
+                const uint64_t ak = (uint64_t)((ks * 1024) >> 4), bk = (uint64_t)((ks * 32) >> 4);
+                mma_ss<1>(dacc, abig + ak, bbig + bk, idesc2);
+                mma_ss<1>(dsm, asmall + ak, bbig + bk, idesc);
+              }
+            } else {
+              if (i == 0)
+                mma_ss<0>(dacc, asmall, bbig, idesc);
+              else
+                mma_ss<1>(dacc, asmall, bbig, idesc);
+              mma_ss<1>(dacc, abig, bsmall, idesc);
+              mma_ss<1>(dacc, abig, bbig, idesc);
+#pragma unroll
+              for (int ks = 1; ks < BK / 8; ++ks) {
+                const uint64_t ak = (uint64_t)((ks * 1024) >> 4), bk = (uint64_t)((ks * 32) >> 4);
+                mma_ss<1>(dacc, asmall + ak, bbig + bk, idesc);
+                mma_ss<1>(dacc, abig + ak, bsmall + bk, idesc);
+                mma_ss<1>(dacc, abig + ak, bbig + bk, idesc);
+              }
             }
             tc_commit(&empty[s]);
           }
@@ -266,12 +299,19 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int m = img * w.PQ + pix;
       const int n0 = nt * BN;
       const int cols = BN / 2;
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN);
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * w.accw);
       const RowPtr rp = live ? (w.splits > 1 ? part.row(sp, m) : epi.row(m)) : RowPtr{nullptr, 0.f};
 #pragma unroll 1
       for (int c0 = half * cols; c0 < half * cols + cols; c0 += 16) {
         uint32_t v[16];
         tmem_ld16(taddr + (uint32_t)c0, v);
+        if (w.sacc) {  // big + small halves, fp32 round-to-nearest
+          uint32_t sv[16];
+          tmem_ld16(taddr + (uint32_t)(BN + c0), sv);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(sv[j])));
+        }
         if (live) {
           const int nlim = w.Nout - (n0 + c0);
           if (w.splits > 1) {
@@ -336,6 +376,10 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
   const bool pair = w.BN <= TC4_PAIR_MAX_BN;
   const int cap = pair ? 113 * 1024 : smem_cap;
   w.tmem_cols = pair ? 256 : 512;
+  // separate small-term accumulator where two 2*BN-column buffers fit the
+  // CTA's TMEM (BN <= 64 paired, BN <= 128 alone); PURINE_B200_SACC=0 disables
+  w.sacc = (2 * 2 * w.BN <= w.tmem_cols && tc4_sacc_enabled()) ? 1 : 0;
+  w.accw = w.sacc ? 2 * w.BN : w.BN;
   w.nst = std::min(kMaxStages, (cap - tail) / w.stage_bytes);
   if (w.nst < 2) return -1;
   const int64_t pack_bytes = (int64_t)w.ntiles * w.nkb * w.b_bytes;
