@@ -42,6 +42,11 @@
 
 namespace bf {
 
+bool tc2_sacc_enabled() {
+  const char* e = getenv("PURINE_B200_SACC");
+  return !(e && *e && atoi(e) == 0);
+}
+
 bool tc2_split_outer() {
   const char* e = getenv("PURINE_B200_SPLIT_OUTER");
   return !(e && *e && atoi(e) == 0);
@@ -316,6 +321,7 @@ struct Work {
   int nbst;   // B ring stages
   int abase;  // first TMEM column of the A ring
   int accs;   // TMEM column stride between the accumulator buffers
+  int sacc;   // 1: separate small-term accumulator in columns [BN, 2BN) of each buffer
   int Pp, Qp;  // weight-gradient fast path: padded pixel grid of the K ordering
   int sstride;  // bytes between ring stages (B tile [+ raw A tile in kTma1x1])
   int cpi;      // kTma1x1: 32-pixel k-blocks per image
@@ -335,6 +341,17 @@ inline void divmagic(uint32_t d, uint64_t& m, int& s) {
   while ((1ull << l) < d) ++l;
   s = 31 + l;
   m = ((1ull << s) + d - 1) / d;
+}
+
+// TMEM map: nacc accumulator buffers of accs columns, then the A ring.  With
+// BN <= 64 the buffers carry a separate small-term accumulator (sacc, see the
+// MMA issuer): 2 x 2*BN columns still leave a ring of >= 4 stages.
+inline void setup_tmem(Work& w, int nacc_default, int max_nst) {
+  w.sacc = (w.BN <= 64 && tc2_sacc_enabled()) ? 1 : 0;
+  w.nacc = w.sacc ? 2 : nacc_default;
+  w.accs = w.sacc ? 2 * w.BN : w.BN;  // multiple of 32
+  w.abase = (w.nacc * w.accs + 63) / 64 * 64;
+  w.nst = std::min<int>(max_nst, (512 - w.abase) / 64);
 }
 
 // MODE: 0 generic table gather, 1 channel-chunk fast path (fwd / dgrad),
@@ -954,6 +971,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     // dependent branch made ptxas emit an illegal uniform-register sequence.)
     {
       const uint32_t idesc = tf32_idesc(BN);
+      const uint32_t idesc2 = tf32_idesc(w.sacc ? 2 * BN : BN);
       const uint64_t dtiles = sw128_desc(smem_u32(tiles));  // B stage 0, big image, k-step 0
       const uint64_t dsmall = (uint64_t)((BN * 128) >> 4);   // big -> small image
       // ring positions advance incrementally: a runtime modulo / divide per
@@ -978,6 +996,25 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           const uint64_t ds = db + dsmall;
           const uint32_t ab = tmem + w.abase + stage * 64;
           if (elect_one()) {
+            if (w.sacc) {
+              // the B stage is [B big rows | B small rows]: one N = 2*BN MMA puts
+              // A_big*B_big in columns [0, BN) and A_big*B_small in [BN, 2BN),
+              // where A_small*B_big accumulates too -- two instructions per
+              // k-step, and one round-toward-zero accumulation of the big
+              // accumulator instead of three (tc4 measured 2.3x less error)
+              const uint32_t dsm = dacc + (uint32_t)BN;
+              if (i == 0)
+                mma_ts_flag<0>(dacc, ab, db, idesc2);
+              else
+                mma_ts_flag<1>(dacc, ab, db, idesc2);
+              mma_ts_flag<1>(dsm, ab + 32, db, idesc);
+#pragma unroll
+              for (int ks = 1; ks < BK / 8; ++ks) {
+                const uint64_t k2 = (uint64_t)((ks * 32) >> 4);
+                mma_ts_flag<1>(dacc, ab + ks * 8, db + k2, idesc2);
+                mma_ts_flag<1>(dsm, ab + 32 + ks * 8, db + k2, idesc);
+              }
+            } else {
             // 3xTF32 per k-step of 8: small*big + big*small + big*big
             if (i == 0)
               mma_ts_flag<0>(dacc, ab + 32, db, idesc);
@@ -991,6 +1028,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
               mma_ts_flag<1>(dacc, ab + 32 + ks * 8, db + k2, idesc);
               mma_ts_flag<1>(dacc, ab + ks * 8, ds + k2, idesc);
               mma_ts_flag<1>(dacc, ab + ks * 8, db + k2, idesc);
+            }
             }
             tc_commit(&empty[stage]);
 #if !TC2_ONE_COMMIT
@@ -1104,6 +1142,13 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       for (int c0 = half * cols; c0 < half * cols + cols; c0 += 16) {
         uint32_t v[16];
         tmem_ld16(taddr + (uint32_t)c0, v);
+        if (w.sacc) {  // big + small halves, fp32 round-to-nearest
+          uint32_t sv[16];
+          tmem_ld16(taddr + (uint32_t)(BN + c0), sv);
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(sv[j])));
+        }
         if (live) {
           const int nlim = w.N - (n0 + c0);
           if (w.splits > 1) {
@@ -1156,10 +1201,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
 #endif
   // one accumulator (a deeper TMEM A ring) for long k loops, where the ring
   // depth bounds throughput and the epilogue is a small part of a tile
-  w.nacc = (w.BN <= 128 && w.nkb < TC2_NACC1_MIN_KB) ? 2 : 1;
-  w.accs = w.BN;  // multiple of 32
-  w.abase = (w.nacc * w.BN + 63) / 64 * 64;
-  w.nst = std::min<int>(TC2_MAX_NST, (512 - w.abase) / 64);
+  setup_tmem(w, (w.BN <= 128 && w.nkb < TC2_NACC1_MIN_KB) ? 2 : 1, TC2_MAX_NST);
   const int64_t stage_bytes = 2LL * w.BN * 128;
   w.sstride = (int)stage_bytes;
   const int64_t pack_bytes = (int64_t)w.ntiles * w.nkb * stage_bytes;
@@ -1303,10 +1345,7 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
   divmagic((uint32_t)w.Qp, w.qp_m, w.qp_s);
   w.BN = pick_bn_tma(Kout, w.ntiles);
   w.mtiles = (M + BM - 1) / BM;
-  w.nacc = w.BN <= 128 ? 2 : 1;
-  w.accs = w.BN;
-  w.abase = (w.nacc * w.BN + 63) / 64 * 64;
-  w.nst = std::min<int>(TC2_MAX_NST, (512 - w.abase) / 64);
+  setup_tmem(w, w.BN <= 128 ? 2 : 1, TC2_MAX_NST);
   w.sstride = 2 * w.BN * 128;
   w.full_ktab = 0;
   CUtensorMap bmap;
@@ -1379,10 +1418,7 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
   w.K = w.nkb * BK;
   w.BN = pick_bn_tma(Kout, w.ntiles);
   w.mtiles = (C + BM - 1) / BM;
-  w.nacc = w.BN <= 128 ? 2 : 1;
-  w.accs = w.BN;
-  w.abase = (w.nacc * w.BN + 63) / 64 * 64;
-  w.nst = std::min<int>(7, (512 - w.abase) / 64);
+  setup_tmem(w, w.BN <= 128 ? 2 : 1, 7);
   w.sstride = 2 * w.BN * 128 + BM * 128;
   w.full_ktab = 0;
   CUtensorMap amap, bmap;
