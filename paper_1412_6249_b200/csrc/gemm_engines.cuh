@@ -62,7 +62,8 @@ inline bool tc2_async_gather_enabled() { return g_gemm_engine != 6; }
 inline bool tc2_wgrad_tma_enabled() { return g_gemm_engine == 7; }
 // weight-gradient units split-major (PURINE_B200_SPLIT_OUTER, default 1)
 bool tc2_split_outer();
-// separate small-term accumulators for BN <= 64 tiles (PURINE_B200_SACC, default 1)
-bool tc2_sacc_enabled();
+// widest tile given a separate small-term accumulator (PURINE_B200_SACC=0: none;
+// PURINE_B200_SACC_MAX_BN, default 128)
+int tc2_sacc_max_bn();
 
 }  // namespace bf

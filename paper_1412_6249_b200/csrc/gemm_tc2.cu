@@ -42,9 +42,11 @@
 
 namespace bf {
 
-bool tc2_sacc_enabled() {
+int tc2_sacc_max_bn() {
   const char* e = getenv("PURINE_B200_SACC");
-  return !(e && *e && atoi(e) == 0);
+  if (e && *e && atoi(e) == 0) return 0;
+  const char* m = getenv("PURINE_B200_SACC_MAX_BN");
+  return m && *m ? atoi(m) : 128;
 }
 
 bool tc2_split_outer() {
@@ -344,11 +346,13 @@ inline void divmagic(uint32_t d, uint64_t& m, int& s) {
 }
 
 // TMEM map: nacc accumulator buffers of accs columns, then the A ring.  With
-// BN <= 64 the buffers carry a separate small-term accumulator (sacc, see the
-// MMA issuer): 2 x 2*BN columns still leave a ring of >= 4 stages.
+// BN <= 128 the buffers carry a separate small-term accumulator (sacc, see the
+// MMA issuer): two 2*BN-column buffers while a >= 4-stage ring remains (BN <=
+// 64), else one (BN 96 / 128: measured as fast as two plain buffers).
 inline void setup_tmem(Work& w, int nacc_default, int max_nst) {
-  w.sacc = (w.BN <= 64 && tc2_sacc_enabled()) ? 1 : 0;
-  w.nacc = w.sacc ? 2 : nacc_default;
+  w.sacc = (w.BN <= tc2_sacc_max_bn()) ? 1 : 0;
+  // two 2*BN buffers only while a >= 4-stage ring remains
+  w.nacc = w.sacc ? (4 * w.BN + 256 <= 512 ? 2 : 1) : nacc_default;
   w.accs = w.sacc ? 2 * w.BN : w.BN;  // multiple of 32
   w.abase = (w.nacc * w.accs + 63) / 64 * 64;
   w.nst = std::min<int>(max_nst, (512 - w.abase) / 64);
