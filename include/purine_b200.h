@@ -178,8 +178,8 @@ int bf_maxpool_bwd_relu(const float* mask, const float* dy, float* dx, const flo
                         int N, int C, int H, int W, int P, int Q, int kernel, int stride, int pad,
                         bf_stream_t stream);
 /* 3x3 max pooling staged through shared memory by bulk copies (pool_staged.cu).
-   bf_maxpool_staged_ok: 1 when the shape is supported (backward != 0: the
-   backward's stage, which also holds dy and the recomputed argmax).  The
+   bf_maxpool_staged_ok: 1 when the shape is supported (backward 0: forward,
+   1: the backward recomputing the argmax from x, 2: the backward reading the mask).  The
    forward writes the mask only when `mask` is non-null; the backward
    recomputes every window's argmax from x (bit-identical to the forward's) so
    the mask never has to be stored, and with relu_from_x != 0 applies the
@@ -191,6 +191,11 @@ int bf_maxpool_fwd_staged(const float* x, float* y, float* mask, int N, int C, i
 int bf_maxpool_bwd_x(const float* x, const float* dy, float* dx, int relu_from_x, int N, int C,
                      int H, int W, int P, int Q, int kernel, int stride, int pad,
                      bf_stream_t stream);
+/* the same gather from the forward's mask (backward = 2 for bf_maxpool_staged_ok);
+   bf_maxpool_bwd routes here where it fits */
+int bf_maxpool_bwd_staged(const float* mask, const float* dy, float* dx, int N, int C, int H,
+                          int W, int P, int Q, int kernel, int stride, int pad,
+                          bf_stream_t stream);
 int bf_avgpool_fwd(const float* x, float* y, int N, int C, int H, int W, int P, int Q,
                    int kernel, int stride, int pad, bf_stream_t stream);
 int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P, int Q,

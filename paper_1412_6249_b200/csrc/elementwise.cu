@@ -6,6 +6,7 @@
 #include <stdarg.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "common.cuh"
@@ -274,24 +275,28 @@ struct FiniteList {
   int count;
 };
 
+// grid (chunks, tensors): block (x, t) checks chunk x of tensor t (4096
+// floats); blocks past a tensor's end exit at once.  (A grid-stride walk over
+// the tensors one after another was latency-bound on the ~116 small parameter
+// tensors: 38 us per launch for 14 MB.)
+constexpr int kFiniteChunk = 4096;
 __global__ void finite_list_kernel(const FiniteList list, int* flag) {
+  const int t = blockIdx.y;
+  const float* x = list.ptr[t];
+  const int64_t n = list.len[t];
+  const int64_t lo = (int64_t)blockIdx.x * kFiniteChunk;
+  if (lo >= n) return;
+  const int64_t hi = min(n, lo + kFiniteChunk);
   bool bad = false;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  for (int t = 0; t < list.count; ++t) {
-    const float* x = list.ptr[t];
-    const int64_t n = list.len[t];
-    if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {
-      const float4* x4 = reinterpret_cast<const float4*>(x);
-      const int64_t n4 = n >> 2;
-      for (int64_t i = tid; i < n4; i += stride) {
-        const float4 v = __ldg(x4 + i);
-        bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
-      }
-      for (int64_t i = (n4 << 2) + tid; i < n; i += stride) bad |= !isfinite(x[i]);
-    } else {
-      for (int64_t i = tid; i < n; i += stride) bad |= !isfinite(x[i]);
+  if ((reinterpret_cast<uintptr_t>(x + lo) & 15) == 0 && hi - lo == kFiniteChunk) {
+    const float4* x4 = reinterpret_cast<const float4*>(x + lo);
+#pragma unroll
+    for (int j = 0; j < kFiniteChunk / 4 / 256; ++j) {
+      const float4 v = __ldg(x4 + j * 256 + threadIdx.x);
+      bad |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
     }
+  } else {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) bad |= !isfinite(x[i]);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
@@ -516,15 +521,15 @@ int bf_check_finite_list(const float* const* ptrs, const int64_t* lens, int coun
   for (int base = 0; base < count; base += kFiniteMax) {
     FiniteList list;
     list.count = count - base < kFiniteMax ? count - base : kFiniteMax;
-    int64_t total = 0;
+    int64_t longest = 0;
     for (int i = 0; i < list.count; ++i) {
       list.ptr[i] = ptrs[base + i];
       list.len[i] = lens[base + i];
-      total += lens[base + i];
+      longest = std::max<int64_t>(longest, lens[base + i]);
     }
-    if (total <= 0) continue;
-    finite_list_kernel<<<elementwise_grid((total + 3) / 4, kThreads), kThreads, 0, as_stream(s)>>>(
-        list, flag);
+    if (longest <= 0) continue;
+    const dim3 grid((unsigned)((longest + kFiniteChunk - 1) / kFiniteChunk), (unsigned)list.count);
+    finite_list_kernel<<<grid, 256, 0, as_stream(s)>>>(list, flag);
     const int rc = check_launch("check_finite_list");
     if (rc) return rc;
   }

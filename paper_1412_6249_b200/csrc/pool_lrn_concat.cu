@@ -1313,9 +1313,10 @@ static void lrn5_bwd_rc_launch(const float* x, const float* dy, float* dx, const
 // PURINE_B200_POOL_WALKERS, default all on
 static int pool_walkers() {
   // bit 0/1: stride-1/2 column walkers, 2: stride-1 backward walker, 3: warp-row
-  // kernels, 4: shared-memory staged kernels (pool_staged.cu)
+  // kernels, 4: shared-memory staged forward, 5: staged mask-reading backward
+  // (pool_staged.cu)
   const char* e = std::getenv("PURINE_B200_POOL_WALKERS");
-  return e ? std::atoi(e) : 31;
+  return e ? std::atoi(e) : 63;
 }
 
 extern "C" {
@@ -1398,6 +1399,11 @@ int bf_maxpool_bwd_relu(const float* mask, const float* dy, float* dx, const flo
                         bf_stream_t s) {
   int64_t total = (int64_t)N * C * H * W;
   if (total <= 0) return 0;
+  // mask + dy staged through shared memory (pool_staged.cu) where it fits
+  if (!relu_x && (pool_walkers() & 32) &&
+      ((reinterpret_cast<uintptr_t>(mask) | reinterpret_cast<uintptr_t>(dy)) & 15) == 0 &&
+      bf_maxpool_staged_ok(N, C, H, W, P, Q, kernel, stride, pad, 2))
+    return bf_maxpool_bwd_staged(mask, dy, dx, N, C, H, W, P, Q, kernel, stride, pad, s);
   if (kernel == 3 && stride == 1 && pad == 1 && W <= 32 && P == H && Q == W &&
       (pool_walkers() & 8)) {
     const int64_t planes = (int64_t)N * C, warps = (planes + 32 / W - 1) / (32 / W);

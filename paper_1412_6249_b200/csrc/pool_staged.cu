@@ -183,7 +183,10 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_fwd_staged(const float* 
   }
 }
 
-template <int S>
+// MASK = false: x is the pool input, every window's argmax is recomputed
+// (phase 1); MASK = true: x is the forward's argmax mask (flat indices as
+// float32, [planes][P][Q]) and phase 1 is skipped
+template <int S, bool MASK>
 __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* __restrict__ x,
                                                                    const float* __restrict__ dy,
                                                                    float* __restrict__ dx, Geo g,
@@ -191,8 +194,10 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t full[kMaxStages];
   const int HW = g.H * g.W, PQ = g.P * g.Q;
-  // stage: [x: G*HW][dy: G*PQ][arg: G*PQ ints]; x and dy segments 16-byte aligned
-  const int xseg = (g.G * HW + 3) & ~3, dseg = (g.G * PQ + 3) & ~3;
+  // stage: [x: G*HW][dy: G*PQ][arg: G*PQ ints] (MASK: [mask: G*PQ][dy: G*PQ]);
+  // x / mask and dy segments 16-byte aligned
+  const int XP = MASK ? PQ : HW;
+  const int xseg = (g.G * XP + 3) & ~3, dseg = (g.G * PQ + 3) & ~3;
   if (threadIdx.x == 0) {
     for (int s = 0; s < g.NS; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
   auto load = [&](int s, int64_t c) {
     float* st = sm + s * g.stage_floats;
     const int gh = planes_of(c);
-    issue_loads(smem_u32(st), x + c * g.G * HW, (int64_t)gh * HW, smem_u32(st + xseg),
+    issue_loads(smem_u32(st), x + c * g.G * XP, (int64_t)gh * XP, smem_u32(st + xseg),
                 dy + c * g.G * PQ, (int64_t)gh * PQ, &full[s]);
   };
   if (threadIdx.x == 0) {
@@ -221,7 +226,13 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
     const float* gs0 = xs0 + xseg;
     int* as0 = reinterpret_cast<int*>(const_cast<float*>(gs0 + dseg));
     const int gh = planes_of(c);
+    // window argmax as an int: recomputed (phase 1) or the mask's float
+    const float* mk0 = xs0;
+    auto arg_at = [&](const int* ap, const float* mp, int o) -> int {
+      return MASK ? (int)mp[o] : ap[o];
+    };
     // phase 1: every window's argmax (the forward's scan)
+    if (!MASK)
     for (int it = threadIdx.x; it < gh * per_plane1; it += kThreads) {
       const int gl = fdiv(it, g.m_pp1, g.s_pp1), r = it - gl * per_plane1;
       const int run = fdiv(r, g.m_q, g.s_q), pw = r - run * g.Q;
@@ -230,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
       walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
                       [&](int ph, float, int arg) { ap[ph * g.Q] = arg; });
     }
-    __syncthreads();
+    if (!MASK) __syncthreads();
     // phase 2: per input pixel, dy of the windows whose argmax it is, in window
     // raster order
     float* dxc = dx + c * g.G * HW;
@@ -241,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
         const int run = fdiv(r, g.m_in2, g.s_in2), w = r - run * g.W;
         const int h0 = run * g.RBh, h1 = min(g.H, h0 + g.RBh);
         const int* ap = as0 + gl * PQ;
+        const float* mp = mk0 + gl * PQ;
         const float* gp = gs0 + gl * PQ;
         const float* xs = xs0 + gl * HW;
         float* dp = dxc + gl * HW + w;
@@ -253,9 +265,9 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
         auto ld_row = [&](int ph, int (&a)[3], float (&d)[3]) {
           const bool rv = (unsigned)ph < (unsigned)g.P;
           const int o = ph * g.Q + q0;
-          a[0] = (rv && v0) ? ap[o] : -1;
-          a[1] = (rv && v1) ? ap[o + 1] : -1;
-          a[2] = (rv && v2) ? ap[o + 2] : -1;
+          a[0] = (rv && v0) ? arg_at(ap, mp, o) : -1;
+          a[1] = (rv && v1) ? arg_at(ap, mp, o + 1) : -1;
+          a[2] = (rv && v2) ? arg_at(ap, mp, o + 2) : -1;
           d[0] = (rv && v0) ? gp[o] : 0.f;
           d[1] = (rv && v1) ? gp[o + 1] : 0.f;
           d[2] = (rv && v2) ? gp[o + 2] : 0.f;
@@ -277,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
           for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, Ab[j] == me ? Db[j] : 0.f);
 #pragma unroll
           for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, Ac[j] == me ? Dc[j] : 0.f);
-          if (relu_from_x) acc = xs[me] > 0.f ? acc : 0.f;
+          if (!MASK && relu_from_x) acc = xs[me] > 0.f ? acc : 0.f;
           dp[h * g.W] = acc;
           if (++h >= h1) return false;
           ++p;
@@ -298,14 +310,17 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
         const int gl = fdiv(it, g.m_pp2, g.s_pp2), r = it - gl * per_plane2;
         const int i = fdiv(r, g.m_in2, g.s_in2), j = r - i * BJ;
         const int* ap = as0 + gl * PQ;
+        const float* mp = mk0 + gl * PQ;
         const float* gp = gs0 + gl * PQ;
         const float* xs = xs0 + gl * HW;
         float* dp = dxc + gl * HW;
         const bool pa = (unsigned)(i - 1) < (unsigned)g.P, pb = i < g.P;
         const bool qa = (unsigned)(j - 1) < (unsigned)g.Q, qb = j < g.Q;
         const int oa = (i - 1) * g.Q, ob = i * g.Q;
-        const int aAA = (pa && qa) ? ap[oa + j - 1] : -1, aAB = (pa && qb) ? ap[oa + j] : -1;
-        const int aBA = (pb && qa) ? ap[ob + j - 1] : -1, aBB = (pb && qb) ? ap[ob + j] : -1;
+        const int aAA = (pa && qa) ? arg_at(ap, mp, oa + j - 1) : -1;
+        const int aAB = (pa && qb) ? arg_at(ap, mp, oa + j) : -1;
+        const int aBA = (pb && qa) ? arg_at(ap, mp, ob + j - 1) : -1;
+        const int aBB = (pb && qb) ? arg_at(ap, mp, ob + j) : -1;
         const float gAA = (pa && qa) ? gp[oa + j - 1] : 0.f, gAB = (pa && qb) ? gp[oa + j] : 0.f;
         const float gBA = (pb && qa) ? gp[ob + j - 1] : 0.f, gBB = (pb && qb) ? gp[ob + j] : 0.f;
         const int h0 = 2 * i - g.pad, w0 = 2 * j - g.pad;
@@ -321,7 +336,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
         a10 = __fadd_rn(a10, aBB == e10 ? gBB : 0.f);
         a11 = __fadd_rn(a11, aBB == e11 ? gBB : 0.f);
         const bool r0 = h0 >= 0, r1 = h0 + 1 < g.H, k0 = w0 >= 0, k1 = w0 + 1 < g.W;
-        if (relu_from_x) {
+        if (!MASK && relu_from_x) {
           if (r0 && k0) a00 = xs[e00] > 0.f ? a00 : 0.f;
           if (r0 && k1) a01 = xs[e01] > 0.f ? a01 : 0.f;
           if (r1 && k0) a10 = xs[e10] > 0.f ? a10 : 0.f;
@@ -357,7 +372,8 @@ inline int align_planes(int per_plane_floats) {  // smallest G with G * f % 4 ==
   return 4;
 }
 
-bool plan(Geo& g, bool bwd, int N, int C, int H, int W, int P, int Q, int S, int pad) {
+// bwd: 0 forward, 1 backward recomputing the argmax from x, 2 backward from the mask
+bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int pad) {
   g.H = H; g.W = W; g.P = P; g.Q = Q; g.pad = pad;
   g.planes = (int64_t)N * C;
   if (g.planes <= 0 || pad < 0 || pad > 2 || (S != 1 && S != 2)) return false;
@@ -366,12 +382,13 @@ bool plan(Geo& g, bool bwd, int N, int C, int H, int W, int P, int Q, int S, int
   if ((P - 1) * S - pad >= H || (Q - 1) * S - pad >= W) return false;
   const int a = std::max(align_planes(HW), align_planes(PQ));
   if ((g.planes * HW) % 4 || (g.planes * PQ) % 4) return false;
-  const int64_t per_plane = bwd ? (int64_t)HW + 2LL * PQ : (int64_t)HW;
+  const int64_t per_plane = bwd == 2 ? 2LL * PQ : bwd ? (int64_t)HW + 2LL * PQ : (int64_t)HW;
   int G = (int)std::max<int64_t>(1, (bwd ? kStageTarget * 3 / 2 : kStageTarget) / (per_plane * 4));
   G = (G + a - 1) / a * a;
   if (G > g.planes) G = (int)((g.planes + a - 1) / a * a);
   auto stage_floats = [&](int G_) {
-    return bwd ? ((G_ * HW + 3) & ~3) + ((G_ * PQ + 3) & ~3) + G_ * PQ : G_ * HW;
+    return bwd == 2 ? ((G_ * PQ + 3) & ~3) * 2
+                    : bwd ? ((G_ * HW + 3) & ~3) + ((G_ * PQ + 3) & ~3) + G_ * PQ : G_ * HW;
   };
   const int64_t sb = (int64_t)stage_floats(G) * 4;
   if (sb * 2 > kSmemBudget) return false;
@@ -453,17 +470,17 @@ extern "C" {
 int bf_maxpool_staged_ok(int N, int C, int H, int W, int P, int Q, int kernel, int stride,
                          int pad, int backward) {
   pools::Geo g;
-  // stride-1 backward: the recompute + 9-window gather costs ~140 instructions
-  // per pixel here (1.5 TB/s) against 3 TB/s for the mask-reading warp-row
-  // gather, so stride-1 pools keep their mask (the staged forward writes it)
-  if (backward && stride == 1 && !(pools_flags() & 1)) return 0;
-  return kernel == 3 && pools::plan(g, backward != 0, N, C, H, W, P, Q, stride, pad) ? 1 : 0;
+  // backward 1 (argmax recomputed from x) at stride 1: the recompute + 9-window
+  // gather costs ~140 instructions per pixel (1.5 TB/s), so stride-1 pools keep
+  // their mask unless PURINE_B200_POOL_STAGED bit 0 asks otherwise
+  if (backward == 1 && stride == 1 && !(pools_flags() & 1)) return 0;
+  return kernel == 3 && pools::plan(g, backward, N, C, H, W, P, Q, stride, pad) ? 1 : 0;
 }
 
 int bf_maxpool_fwd_staged(const float* x, float* y, float* mask, int N, int C, int H, int W,
                           int P, int Q, int kernel, int stride, int pad, bf_stream_t s) {
   pools::Geo g;
-  BF_REQUIRE(kernel == 3 && pools::plan(g, false, N, C, H, W, P, Q, stride, pad),
+  BF_REQUIRE(kernel == 3 && pools::plan(g, 0, N, C, H, W, P, Q, stride, pad),
              "maxpool_forward(staged): unsupported shape %dx%dx%dx%d k%d s%d p%d", N, C, H, W,
              kernel, stride, pad);
   BF_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0, "maxpool_forward(staged): x not 16B aligned");
@@ -479,18 +496,36 @@ int bf_maxpool_fwd_staged(const float* x, float* y, float* mask, int N, int C, i
 int bf_maxpool_bwd_x(const float* x, const float* dy, float* dx, int relu_from_x, int N, int C,
                      int H, int W, int P, int Q, int kernel, int stride, int pad, bf_stream_t s) {
   pools::Geo g;
-  BF_REQUIRE(kernel == 3 && pools::plan(g, true, N, C, H, W, P, Q, stride, pad),
+  BF_REQUIRE(kernel == 3 && pools::plan(g, 1, N, C, H, W, P, Q, stride, pad),
              "maxpool_backward(staged): unsupported shape %dx%dx%dx%d k%d s%d p%d", N, C, H, W,
              kernel, stride, pad);
   BF_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(dy) & 15) == 0,
              "maxpool_backward(staged): x / dy not 16B aligned");
   const int smem = g.NS * g.stage_floats * 4;
   static bool cfg[2] = {false, false};
-  auto kern = stride == 1 ? pools::maxpool3_bwd_staged<1> : pools::maxpool3_bwd_staged<2>;
+  auto kern = stride == 1 ? pools::maxpool3_bwd_staged<1, false> : pools::maxpool3_bwd_staged<2, false>;
   const int grid = pools::grid_for(kern, g, cfg[stride - 1]);
   if (grid <= 0) return 1;
   kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(x, dy, dx, g, relu_from_x);
   return check_launch("maxpool_backward(staged)");
+}
+
+int bf_maxpool_bwd_staged(const float* mask, const float* dy, float* dx, int N, int C, int H,
+                          int W, int P, int Q, int kernel, int stride, int pad, bf_stream_t s) {
+  pools::Geo g;
+  BF_REQUIRE(kernel == 3 && pools::plan(g, 2, N, C, H, W, P, Q, stride, pad),
+             "maxpool_backward(staged mask): unsupported shape %dx%dx%dx%d k%d s%d p%d", N, C, H,
+             W, kernel, stride, pad);
+  BF_REQUIRE((reinterpret_cast<uintptr_t>(mask) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(dy) & 15) == 0,
+             "maxpool_backward(staged mask): mask / dy not 16B aligned");
+  const int smem = g.NS * g.stage_floats * 4;
+  static bool cfg[2] = {false, false};
+  auto kern = stride == 1 ? pools::maxpool3_bwd_staged<1, true> : pools::maxpool3_bwd_staged<2, true>;
+  const int grid = pools::grid_for(kern, g, cfg[stride - 1]);
+  if (grid <= 0) return 1;
+  kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(mask, dy, dx, g, 0);
+  return check_launch("maxpool_backward(staged mask)");
 }
 
 }  // extern "C"

@@ -421,11 +421,15 @@ class _Plan:
                     c0 += graph.tensors[t].shape[1]
                 self.fused_away.add(oid)
 
+        foldable = tuple(k for k in os.environ.get(RELU_FOLD_ENV, RELU_FOLD_DEFAULT).split(",") if k)
         # max-pool mask elision: when a maxpool_forward's argmax mask feeds only
         # maxpool_backward operators of the same x and attributes, and the
         # shared-memory staged kernels fit the shape, the backward recomputes
         # every window's argmax from x (the forward's own scan: bit-identical)
-        # and the forward never stores the mask
+        # and the forward never stores the mask -- taken where the backward also
+        # absorbs the relu_backward of the ReLU that produced x (then x is read
+        # anyway, as the ReLU mask); elsewhere reading the mask is less traffic
+        # than re-reading x (a quarter of its size at stride 2)
         for oid, op in graph.operators.items():
             if op.kind != "maxpool_forward" or len(op.outputs) != 2:
                 continue
@@ -437,7 +441,7 @@ class _Plan:
                     graph.operators[c].inputs[1] != mk or
                     graph.operators[c].attrs != op.attrs for c, _ in cons):
                 continue
-            if not _pool_staged(graph, op):
+            if not _pool_staged(graph, op) or not _pool_relu_foldable(graph, cons, foldable):
                 continue
             self.fusion.setdefault(oid, {})["pool_no_mask"] = True
             for c, _ in cons:
@@ -448,7 +452,6 @@ class _Plan:
         # gradient epilogue, the max-pool or LRN backward kernel) when that dy
         # has no other consumer: the producer writes relu_backward's dx directly
         # (bit-identical: the same x > 0 ? g : 0 select), dy is never stored
-        foldable = tuple(k for k in os.environ.get(RELU_FOLD_ENV, RELU_FOLD_DEFAULT).split(",") if k)
         for oid, op in graph.operators.items():
             if op.kind != "relu_backward" or oid in self.fusion or len(op.inputs) != 2:
                 continue
@@ -671,6 +674,23 @@ FUSE_ENV = "PURINE_B200_FUSE"  # "0" disables epilogue fusion (A/B and debugging
 # kernel support; measured net gains decide the default)
 RELU_FOLD_ENV = "PURINE_B200_RELU_FOLD"
 RELU_FOLD_DEFAULT = "conv2d_backward_data,lrn_backward,maxpool_backward"
+
+
+def _pool_relu_foldable(graph: BiGraph, cons, foldable) -> bool:
+    """The single maxpool_backward in ``cons`` feeds exactly one relu_backward
+    whose ReLU produced the pool's input (the fold through x, see _Plan)."""
+    if "maxpool_backward" not in foldable or len(cons) != 1:
+        return False
+    pb = graph.operators[cons[0][0]]
+    users = graph.consumers_of(pb.outputs[0])
+    if len(users) != 1:
+        return False
+    rb = graph.operators[users[0][0]]
+    if rb.kind != "relu_backward" or len(rb.inputs) != 2 or rb.inputs[1] != pb.outputs[0]:
+        return False
+    return any(graph.operators[c].kind == "relu_forward"
+               and graph.operators[c].outputs[0] == pb.inputs[0]
+               for c, _ in graph.consumers_of(rb.inputs[0]))
 
 
 def _pool_staged(graph: BiGraph, op) -> bool:

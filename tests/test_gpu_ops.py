@@ -224,15 +224,14 @@ def test_sgd_momentum_aggregate_bitwise(golden_ops):
                                          ((2, 3, 6, 7), 3, 1, 0), ((2, 64, 7, 7), 3, 1, 1),
                                          ((2, 16, 14, 14), 3, 1, 1), ((1, 3, 9, 32), 3, 1, 1),
                                          ((1, 3, 6, 33), 3, 1, 1), ((3, 5, 4, 1), 3, 1, 1)])
-@pytest.mark.parametrize("walkers", ["31", "15", "7", "0"],
+@pytest.mark.parametrize("walkers", ["63", "15", "7", "0"],
                          ids=["staged", "rows", "columns", "planes"])
 @pytest.mark.parametrize("values", ["normal", "coarse"])
 def test_maxpool_bitwise(shape, k, s, p, walkers, values, monkeypatch):
-    """Bulk-staged 3x3 forward (default where it fits), warp-row kernels
-    (stride-1 pad-1 planes <= 32 wide), column walkers and plane-staging
-    kernels (PURINE_B200_POOL_WALKERS=31 / 15 / 7 / 0) all bit-exact; the
-    single-operator graph keeps the mask, so the backward here is the
-    mask-reading gather.  "coarse" values make most
+    """Bulk-staged 3x3 forward and mask-reading backward (default where they
+    fit), warp-row kernels (stride-1 pad-1 planes <= 32 wide), column walkers
+    and plane-staging kernels (PURINE_B200_POOL_WALKERS=63 / 15 / 7 / 0) all
+    bit-exact.  "coarse" values make most
     windows hold ties (first maximum in raster order wins) and put a -inf
     block in the corner."""
     monkeypatch.setenv("PURINE_B200_POOL_WALKERS", walkers)
@@ -299,7 +298,10 @@ def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values, s1_bwd
         tda = g.add_tensor("da", shape, loc)
         g.add_operator("bwd_relu", "relu_backward", [ta, tdx], [tda], loc)
     n, c, h, w = shape
-    staged = bool(lib().raw("bf_maxpool_staged_ok")(n, c, h, w, y.shape[2], y.shape[3], k, s, p, 1))
+    # the mask is elided where the backward also absorbs the ReLU backward
+    # through x (fold); otherwise the staged backward reads the mask
+    staged = fold and bool(lib().raw("bf_maxpool_staged_ok")(n, c, h, w, y.shape[2], y.shape[3],
+                                                              k, s, p, 1))
     plan = _plan(g, 8)
     assert ("m" in plan.elided) == staged
     st = TensorStore("cuda:0")
