@@ -418,6 +418,36 @@ inline int64_t chain_min_splits(int64_t nkb) {
   return c > 0 ? (nkb + c - 1) / c : 1;
 }
 
+// Weight-gradient split-K factor: at least s_min (SM fill / chain bound), at
+// most s_max (workspace, k-blocks); among those, the fewest k-blocks on the
+// busiest CTA of the persistent grid, ceil(units / sms) * (kbps + ramp) with a
+// unit's pipeline ramp and epilogue counted as kRamp k-blocks -- so the last
+// wave is not a sliver (3a/5x5_reduce: 100 splits = 1.35 waves of 64 k-blocks
+// -> 148 splits = 2 waves of 22).  PURINE_B200_BALANCE_SPLITS=0 keeps s_min.
+bool balance_splits_enabled();
+inline int64_t balance_splits(int64_t tiles, int64_t nkb, int64_t s_min, int64_t s_max,
+                              int sms) {
+  constexpr int64_t kRamp = 2;
+  s_min = std::max<int64_t>(1, s_min);
+  s_max = std::max<int64_t>(s_min, s_max);
+  if (!balance_splits_enabled() || s_min == 1 && tiles >= sms) return s_min;
+  auto cost = [&](int64_t s) {
+    const int64_t kbps = (nkb + s - 1) / s;
+    const int64_t se = (nkb + kbps - 1) / kbps;
+    return ((tiles * se + sms - 1) / sms) * (kbps + kRamp);
+  };
+  int64_t best = s_min, bc = cost(s_min);
+  const int64_t hi = std::min<int64_t>(s_max, 2 * s_min + 8);
+  for (int64_t s = s_min + 1; s <= hi; ++s) {
+    const int64_t c = cost(s);
+    if (c < bc) {
+      bc = c;
+      best = s;
+    }
+  }
+  return best;
+}
+
 enum GemmOp { kConvFwd = 0, kConvDgrad = 1, kConvWgrad = 2, kFcFwd = 3, kFcDgrad = 4, kFcWgrad = 5 };
 
 // choose a split-K factor: fill ~2 waves of SMs, keep >= min_k per split,

@@ -49,6 +49,11 @@ int tc2_sacc_max_bn() {
   return m && *m ? atoi(m) : 128;
 }
 
+bool balance_splits_enabled() {
+  const char* e = getenv("PURINE_B200_BALANCE_SPLITS");
+  return !(e && *e && atoi(e) == 0);
+}
+
 bool tc2_split_outer() {
   const char* e = getenv("PURINE_B200_SPLIT_OUTER");
   return !(e && *e && atoi(e) == 0);
@@ -1242,12 +1247,14 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
       if (wgrad_pack) want = std::max(want, chain_min_splits(w.nkb));
       int64_t by_k = w.nkb / 4;
       int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
-      w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                   std::min<int64_t>(by_ws, kMaxSplits)));
+      const int64_t cap = std::min(by_k, std::min<int64_t>(by_ws, kMaxSplits));
+      w.splits = (int)std::max<int64_t>(1, std::min(want, cap));
+      if (wgrad_pack) w.splits = (int)balance_splits(tiles, w.nkb, w.splits, cap, sms);
     } else if (wgrad_pack) {  // many tiles: split only as far as the chain bound needs
       const int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
-      w.splits = (int)std::max<int64_t>(1, std::min(chain_min_splits(w.nkb),
-                                                   std::min<int64_t>(by_ws, kMaxSplits)));
+      const int64_t cap = std::min<int64_t>(by_ws, kMaxSplits);
+      w.splits = (int)std::max<int64_t>(1, std::min(chain_min_splits(w.nkb), cap));
+      w.splits = (int)balance_splits(tiles, w.nkb, w.splits, cap, sms);
     }
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
@@ -1369,8 +1376,9 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
                                              chain_min_splits(w.nkb));
       const int64_t by_k = std::max<int64_t>(1, w.nkb / 4);
       const int64_t by_ws = part_bytes / ((int64_t)M * Kout * 4);
-      w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                   std::min<int64_t>(by_ws, kMaxSplits)));
+      const int64_t cap = std::min(by_k, std::min<int64_t>(by_ws, kMaxSplits));
+      w.splits = (int)std::max<int64_t>(1, std::min(want, cap));
+      w.splits = (int)balance_splits(tiles, w.nkb, w.splits, cap, sms);
     }
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
@@ -1444,8 +1452,9 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
                                              chain_min_splits(w.nkb));
       const int64_t by_k = std::max<int64_t>(1, w.nkb / 4);
       const int64_t by_ws = part_bytes / ((int64_t)C * Kout * 4);
-      w.splits = (int)std::max<int64_t>(1, std::min(std::min(want, by_k),
-                                                   std::min<int64_t>(by_ws, kMaxSplits)));
+      const int64_t cap = std::min(by_k, std::min<int64_t>(by_ws, kMaxSplits));
+      w.splits = (int)std::max<int64_t>(1, std::min(want, cap));
+      w.splits = (int)balance_splits(tiles, w.nkb, w.splits, cap, sms);
     }
   }
   w.kbps = (w.nkb + w.splits - 1) / w.splits;
