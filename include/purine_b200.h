@@ -163,6 +163,18 @@ int bf_conv2d_bwd_weight_bias(const float* x, const float* dy, float* dw, float*
    (optional: NULL falls back to one CTA per channel) */
 int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, float* workspace,
                        int64_t ws_bytes, bf_stream_t stream);
+/* horizontally fused 1x1 stride-1 convolutions over the same x (Inception's
+   1x1 / 3x3_reduce / 5x5_reduce, dispatcher fusion plan): one GEMM over the
+   concatenated output channels, x read once.  Segment i (< 4): weights w[i]
+   [kout[i]][C], bias b[i] (may be NULL), output y[i] (N, kout[i], H, W) and,
+   if relu[i] != NULL, relu(y) into channels [relu_c0[i], relu_c0[i] + kout[i])
+   of the relu_ctot[i]-channel tensor relu[i] (the fused relu_forward, possibly
+   into a concat slice).  Host arrays of device pointers.  Same arithmetic per
+   output as bf_conv2d_fwd_relu_slice (ops.py:281-297) */
+int bf_conv1x1_fwd_group(const float* x, int N, int C, int H, int W, int nseg,
+                         const float* const* w, const float* const* b, const int* kout,
+                         float* const* y, float* const* relu, const int* relu_c0,
+                         const int* relu_ctot, float* ws, int64_t ws_bytes, bf_stream_t stream);
 /* workspace bytes the conv/fc entry points want for this shape (0 = none) */
 int64_t bf_gemm_workspace_bytes(int op, int N, int C, int H, int W, int K, int R, int S,
                                 int P, int Q, int stride, int pad);

@@ -94,6 +94,39 @@ int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, flo
                   "conv2d_forward");
 }
 
+int bf_conv1x1_fwd_group(const float* x, int N, int C, int H, int W, int nseg,
+                         const float* const* w, const float* const* b, const int* kout,
+                         float* const* y, float* const* relu, const int* relu_c0,
+                         const int* relu_ctot, float* ws, int64_t ws_bytes, bf_stream_t s) {
+  BF_REQUIRE(nseg >= 1 && nseg <= kMaxSeg, "conv1x1 group: 1 <= nseg <= %d, got %d", kMaxSeg,
+             nseg);
+  BF_REQUIRE(N > 0 && C > 0 && H > 0 && W > 0, "conv1x1 group: non-positive dimension");
+  EpiNCHWSeg epi{};
+  epi.PQ = H * W;
+  epi.nseg = nseg;
+  int n = 0;
+  for (int i = 0; i < nseg; ++i) {
+    BF_REQUIRE(kout[i] > 0 && w[i] && y[i], "conv1x1 group: segment %d malformed", i);
+    BF_REQUIRE(!relu[i] || (relu_c0[i] >= 0 && relu_c0[i] + kout[i] <= relu_ctot[i]),
+               "conv1x1 group: segment %d relu channel range", i);
+    epi.start[i] = n;
+    epi.out[i] = y[i];
+    epi.bias[i] = b[i];
+    epi.cout[i] = kout[i];
+    epi.relu[i] = relu[i];
+    epi.relu_img[i] = relu[i] ? (int64_t)relu_ctot[i] * H * W : 0;
+    epi.relu_c0[i] = relu[i] ? relu_c0[i] : 0;
+    n += kout[i];
+  }
+  for (int i = nseg; i <= kMaxSeg; ++i) epi.start[i] = n;
+  BF_REQUIRE((int64_t)N * C * H * W < (1LL << 31) && (int64_t)N * n * H * W < (1LL << 31),
+             "conv1x1 group: tensor too large for 32-bit pixel indexing");
+  const int rc = tc4_conv_fwd_group(x, N, C, H * W, nseg, w, kout, epi, ws, ws_bytes,
+                                    as_stream(s), "conv2d_forward(group)");
+  BF_REQUIRE(rc >= 0, "conv1x1 group: shape not taken by the TMA-fed 1x1 engine");
+  return rc;
+}
+
 int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx, int N, int C, int H, int W,
                        int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
                        int64_t ws_bytes, bf_stream_t s) {

@@ -243,6 +243,67 @@ struct EpiNCHW {
   }
 };
 
+// Horizontally fused sibling convolutions (Inception's 1x1 / 3x3_reduce /
+// 5x5_reduce reading the same x): one GEMM over the concatenated output
+// channels; column n belongs to segment s with start[s] <= n < start[s + 1],
+// whose output is out[s] (cout[s] channels, NCHW) with bias[s] and, if
+// relu[s], relu(v) into channel relu_c0[s] + (n - start[s]) of a tensor with
+// relu_img[s] elements per image.  RowPtr carries the row index m (relu_delta).
+constexpr int kMaxSeg = 4;
+struct EpiNCHWSeg {
+  int PQ, nseg;
+  int start[kMaxSeg + 1];
+  float* out[kMaxSeg];
+  const float* bias[kMaxSeg];
+  int cout[kMaxSeg];
+  float* relu[kMaxSeg];
+  int64_t relu_img[kMaxSeg];
+  int relu_c0[kMaxSeg];
+  __device__ __forceinline__ int seg_of(int n) const {
+    int s = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxSeg; ++i) s += (i < nseg && n >= start[i]) ? 1 : 0;
+    return s;
+  }
+  __device__ __forceinline__ void put(int img, int pq, int n, float v) const {
+    const int s = seg_of(n), j = n - start[s];
+    if (bias[s]) v = __fadd_rn(v, __ldg(bias[s] + j));
+    __stcg(out[s] + ((int64_t)img * cout[s] + j) * PQ + pq, v);
+    if (relu[s]) __stcg(relu[s] + (int64_t)img * relu_img[s] + (int64_t)(relu_c0[s] + j) * PQ + pq,
+                        relu_value(v));
+  }
+  __device__ __forceinline__ void operator()(int m, int n, float v) const {
+    const int img = m / PQ;
+    put(img, m - img * PQ, n, v);
+  }
+  __device__ __forceinline__ RowPtr row(int m) const { return {nullptr, 0.f, (int64_t)m}; }
+  __device__ __forceinline__ void store16(const RowPtr& r, int n0, const uint32_t (&v)[16],
+                                          int nlim) const {
+    const int m = (int)r.relu_delta, img = m / PQ, pq = m - img * PQ;
+    const int s = seg_of(n0);
+    const int64_t stride = PQ;
+    if (nlim >= 16 && n0 + 15 < start[s + 1]) {  // the chunk lies in one segment
+      const int j0 = n0 - start[s];
+      float* p = out[s] + ((int64_t)img * cout[s] + j0) * PQ + pq;
+      const float* bs = bias[s];
+      float* rp = relu[s] ? relu[s] + (int64_t)img * relu_img[s] +
+                                (int64_t)(relu_c0[s] + j0) * PQ + pq
+                          : nullptr;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float x = __uint_as_float(v[j]);
+        if (bs) x = __fadd_rn(x, __ldg(bs + j0 + j));
+        __stcg(p + j * stride, x);
+        if (rp) __stcg(rp + j * stride, relu_value(x));
+      }
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nlim) put(img, pq, n0 + j, __uint_as_float(v[j]));
+  }
+};
+
 // out[n*ldo + m] = v (+ bias[m])
 struct EpiT {
   float* out;

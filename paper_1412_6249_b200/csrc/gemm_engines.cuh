@@ -38,6 +38,10 @@ int tc4_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNC
                  float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
                    float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+// horizontally fused 1x1 forward convolutions over the same x (segmented epilogue)
+int tc4_conv_fwd_group(const float* x, int N, int C, int HW, int nseg, const float* const* w,
+                       const int* kout, const EpiNCHWSeg& epi, float* ws, int64_t ws_bytes,
+                       cudaStream_t st, const char* what);
 
 // strided convolutions (C*stride^2 <= 64 channels, kernel wider than the
 // stride) as stride-1 convolutions over a space-to-depth view (conv_s2d.cu)

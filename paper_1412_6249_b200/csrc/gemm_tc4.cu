@@ -347,8 +347,8 @@ inline int pick_bn(int N, int& ntiles) {
 }
 
 // act: [imgs][K][PQ]; B(n, k) via lbp (pre-packed); D[m = img*PQ + pix][n] -> epi
-template <class LBP>
-int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, const EpiNCHW& epi,
+template <class LBP, class Epi>
+int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, const Epi& epi,
            float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
   if (PQ % 4 || (reinterpret_cast<uintptr_t>(act) & 15) || K < 8) return -1;
   CUtensorMap amap;
@@ -412,7 +412,7 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
 
   static bool configured = false;
   if (!configured) {
-    BF_CUDA(cudaFuncSetAttribute(tc4_kernel<EpiNCHW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    BF_CUDA(cudaFuncSetAttribute(tc4_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem_cap),
             "tc4 smem attribute");
     configured = true;
@@ -423,10 +423,10 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
   const int smem = std::max(tail + w.nst * w.stage_bytes, (pair ? 109 : 120) << 10);
   const int grid = std::min(w.units, pair ? 2 * sms : sms);
   EpiPartial part{part_ws, M, Nout};
-  tc4_kernel<EpiNCHW><<<grid, kThreads, smem, st>>>(amap, w, bpack, epi, part);
+  tc4_kernel<Epi><<<grid, kThreads, smem, st>>>(amap, w, bpack, epi, part);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
-    splitk_reduce<EpiNCHW>(part_ws, w.splits, M, Nout, epi, st);
+    splitk_reduce<Epi>(part_ws, w.splits, M, Nout, epi, st);
     return check_launch(what);
   }
   return 0;
@@ -437,6 +437,17 @@ struct LdW1x1 {  // fwd: B(n = kout, k = c) = w[kout][c]
   int C;
   __device__ __forceinline__ float operator()(int n, int k) const {
     return w[(int64_t)n * C + k];
+  }
+};
+struct LdW1x1Cat {  // grouped fwd: B(n, k) = w[s][n - start[s]][k], n in segment s
+  const float* w[kMaxSeg];
+  int start[kMaxSeg + 1];
+  int nseg, C;
+  __device__ __forceinline__ float operator()(int n, int k) const {
+    int s = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxSeg; ++i) s += (i < nseg && n >= start[i]) ? 1 : 0;
+    return w[s][(int64_t)(n - start[s]) * C + k];
   }
 };
 struct LdW1x1T {  // dgrad: B(n = c, k = kout) = w[kout][c]
@@ -459,6 +470,24 @@ int tc4_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNC
   if (!tc4_eligible(g)) return -1;
   return tc4::launch(x, g.N, g.C, g.H * g.W, g.K, tc4::LdW1x1{w, g.C}, epi, ws, ws_bytes, st,
                      what);
+}
+
+int tc4_conv_fwd_group(const float* x, int N, int C, int HW, int nseg, const float* const* w,
+                       const int* kout, const EpiNCHWSeg& epi, float* ws, int64_t ws_bytes,
+                       cudaStream_t st, const char* what) {
+  if (nseg < 1 || nseg > kMaxSeg || HW % 4) return -1;
+  tc4::LdW1x1Cat lb{};
+  lb.nseg = nseg;
+  lb.C = C;
+  int n = 0;
+  for (int i = 0; i < nseg; ++i) {
+    lb.w[i] = w[i];
+    lb.start[i] = n;
+    n += kout[i];
+  }
+  lb.start[nseg] = n;
+  for (int i = nseg + 1; i <= kMaxSeg; ++i) lb.start[i] = n;
+  return tc4::launch(x, N, C, HW, n, lb, epi, ws, ws_bytes, st, what);
 }
 
 int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,

@@ -507,8 +507,53 @@ class _Plan:
                 self.fusion.setdefault(c, {})["lrn_recompute"] = True
             self.elided.add(graph.tensors[sc].name)
 
+        self._group_1x1(graph)
         self.finite_mode = _finite_mode()
         self.finite_watch = _finite_watch(graph, self, self.finite_mode)
+
+    def _group_1x1(self, graph: BiGraph) -> None:
+        """Horizontal fusion (Inception): the 1x1 stride-1 conv2d_forward
+        operators reading the same x -- 1x1, 3x3_reduce, 5x5_reduce -- run as
+        ONE GEMM over their concatenated output channels (x read once, one
+        launch, a wider N tile), executed by the first of them in serial order
+        with each member's epilogue fusion (ReLU, concat slice) kept.  The
+        other members become no-ops whose streams wait for that leader, so
+        everything downstream of a member still follows its producer.  The
+        wider GEMM tile may change the tensor-core accumulation scheme (the
+        separate small-term accumulator needs BN <= 128), so results agree with
+        the ungrouped kernels at the contraction tolerance, not bit for bit."""
+        if os.environ.get(GROUP_ENV, "1") == "0":
+            return
+        from .kinds import conv_attrs
+
+        pos = {oid: i for i, oid in enumerate(self.order)}
+        by_x: dict[int, list[int]] = {}
+        for oid, op in graph.operators.items():
+            if op.kind != "conv2d_forward" or oid in self.fused_away:
+                continue
+            w = graph.tensors[op.inputs[1]]
+            x = graph.tensors[op.inputs[0]]
+            if len(w.shape) != 4 or w.shape[2:] != (1, 1) or len(x.shape) != 4:
+                continue
+            stride, pad, _floor = conv_attrs(op.attrs)
+            if stride != 1 or pad != 0 or (x.shape[2] * x.shape[3]) % 4:
+                continue
+            if set(self.fusion.get(oid, {})) - {"relu_out", "relu_slice"}:
+                continue
+            by_x.setdefault(op.inputs[0], []).append(oid)
+        for members in by_x.values():
+            if len(members) < 2:
+                continue
+            members = sorted(members, key=pos.__getitem__)[:4]
+            lead = members[0]
+            self.fusion.setdefault(lead, {})["group_fwd"] = [
+                (graph.operators[m], dict(self.fusion.get(m, {}))) for m in members]
+            for m in members[1:]:
+                self.fused_away.add(m)
+                self.fusion.setdefault(m, {})["group_member"] = lead
+                if lead not in self.waits[m]:
+                    self.waits[m].append(lead)
+                self.signals.add(lead)
 
     def _split_branches(self, graph: BiGraph, branches: int) -> None:
         """Event-driven device concurrency inside a lane: the lane's operators
@@ -670,6 +715,7 @@ def _branch_streams() -> int:
 
 
 FUSE_ENV = "PURINE_B200_FUSE"  # "0" disables epilogue fusion (A/B and debugging)
+GROUP_ENV = "PURINE_B200_GROUP_1X1"  # "0" disables the Inception 1x1 horizontal fusion
 # producer kinds that may absorb the relu_backward after them (all three have the
 # kernel support; measured net gains decide the default)
 RELU_FOLD_ENV = "PURINE_B200_RELU_FOLD"
@@ -730,7 +776,8 @@ def _plan(graph: BiGraph, cap: int) -> _Plan:
     An id()-keyed global cache would hand a dead graph's plan to a new graph
     that happens to reuse its address."""
     branches = _branch_streams()
-    key = (cap, branches, _finite_mode())
+    key = (cap, branches, _finite_mode(), os.environ.get(GROUP_ENV, "1"),
+           os.environ.get(RELU_FOLD_ENV, RELU_FOLD_DEFAULT))
     stamp = len(graph.insertion_order) * 1_000_003 + len(graph.tensors)
     cache = graph.__dict__.setdefault("_launch_plans", {})
     hit = cache.get(key)

@@ -99,10 +99,50 @@ def _geom(x, w, attrs):
     return (n, c, h, wd, k, r, s, p, q, stride, pad)
 
 
+def _conv_fwd_group(ctx, members):
+    """Sibling 1x1 convolutions over the same x as one GEMM (dispatcher
+    _Plan._group_1x1): each member keeps its own output, bias and fused ReLU
+    target (its own tensor or a concat slice)."""
+    import ctypes as C
+
+    g = ctx.graph
+    x = ctx.store.get(g.tensors[members[0][0].inputs[0]].name)
+    n, c, h, wd = x.shape
+    k = len(members)
+    ws_, bs, ks, ys, rs, r0, rt = [], [], [], [], [], [], []
+    for mop, mf in members:
+        _x, w, b = _ins(ctx, mop)
+        (y,) = _outs(ctx, mop)
+        ws_.append(w.ptr)
+        bs.append(b.ptr)
+        ks.append(w.shape[0])
+        ys.append(y.ptr)
+        if "relu_slice" in mf:
+            name, shape, c0 = mf["relu_slice"]
+            rs.append(ctx.store.ensure(name, shape).ptr)
+            r0.append(c0)
+            rt.append(shape[1])
+        elif "relu_out" in mf:
+            rs.append(ctx.store.ensure(mf["relu_out"], y.shape).ptr)
+            r0.append(0)
+            rt.append(w.shape[0])
+        else:
+            rs.append(None)
+            r0.append(0)
+            rt.append(w.shape[0])
+    P = C.c_void_p * k
+    I = C.c_int * k
+    _L()("bf_conv1x1_fwd_group", x.ptr, n, c, h, wd, k, P(*ws_), P(*bs), I(*ks), P(*ys), P(*rs),
+         I(*r0), I(*rt), *_ws(ctx), ctx.stream)
+
+
 def _conv_fwd(ctx, op):
+    fused = getattr(ctx, "fused", None)
+    if fused and "group_fwd" in fused:
+        _conv_fwd_group(ctx, fused["group_fwd"])
+        return
     x, w, b = _ins(ctx, op)
     (y,) = _outs(ctx, op)
-    fused = getattr(ctx, "fused", None)
     if fused and "relu_slice" in fused:  # ReLU straight into its slice of the concat output
         name, shape, c0 = fused["relu_slice"]
         cat = ctx.store.ensure(name, shape)

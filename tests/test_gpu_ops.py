@@ -318,6 +318,73 @@ def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values, s1_bwd
         assert not st.has("m")  # never materialised
 
 
+@pytest.mark.parametrize("couts,shape", [((64, 96, 16), (2, 192, 28, 28)),
+                                          ((128, 128, 32), (2, 256, 28, 28)),
+                                          ((160, 112, 24), (3, 512, 14, 14)),
+                                          ((40, 8), (2, 20, 6, 6))])
+def test_conv1x1_group_forward(couts, shape, monkeypatch):
+    """Inception's sibling 1x1 convolutions over one x as one GEMM (dispatcher
+    _Plan._group_1x1, bf_conv1x1_fwd_group): every member's output and fused
+    ReLU -- one into a concat slice -- within the NS bound of the oracle and of
+    the ungrouped kernels."""
+    from paper_1412_6249_b200 import BiGraph, Location, TensorStore, run
+    from paper_1412_6249_b200.dispatcher import _plan
+
+    loc = Location("local", 0)
+    n, c, h, w = shape
+    rng = np.random.default_rng(5)
+    x = f32(rng.standard_normal(shape))
+    ws = [f32(rng.standard_normal((k, c, 1, 1)) / np.sqrt(c)) for k in couts]
+    bs = [f32(rng.standard_normal(k) * 0.1) for k in couts]
+
+    def graph():
+        g = BiGraph()
+        tx = g.add_tensor("x", shape, loc)
+        cat_parts = []
+        for i, k in enumerate(couts):
+            tw = g.add_tensor(f"w{i}", (k, c, 1, 1), loc)
+            tb = g.add_tensor(f"b{i}", (k,), loc)
+            ty = g.add_tensor(f"y{i}", (n, k, h, w), loc)
+            tr = g.add_tensor(f"r{i}", (n, k, h, w), loc)
+            g.add_operator(f"conv{i}", "conv2d_forward", [tx, tw, tb], [ty], loc,
+                           attrs={"stride": 1, "pad": 0})
+            g.add_operator(f"relu{i}", "relu_forward", [ty], [tr], loc)
+            if i == 0:
+                cat_parts.append(tr)
+        # the first branch's ReLU goes straight into a concat (elided slice)
+        other = g.add_tensor("other", (n, 8, h, w), loc)
+        cat = g.add_tensor("cat", (n, couts[0] + 8, h, w), loc)
+        g.add_operator("bias_other", "relu_forward", [g.add_tensor("o_in", (n, 8, h, w), loc)],
+                       [other], loc)
+        g.add_operator("concat", "concat_forward", cat_parts + [other], [cat], loc)
+        return g
+
+    outs = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PURINE_B200_GROUP_1X1", flag)
+        g = graph()
+        plan = _plan(g, 8)
+        grouped = any("group_fwd" in f for f in plan.fusion.values())
+        assert grouped == (flag == "1")
+        st = TensorStore("cuda:0")
+        st.set("x", x)
+        st.set("o_in", f32(rng.standard_normal((n, 8, h, w))))
+        for i in range(len(couts)):
+            st.set(f"w{i}", ws[i])
+            st.set(f"b{i}", bs[i])
+        run(g, st)
+        outs[flag] = {nm: st.array(nm) for nm in
+                      [f"y{i}" for i in range(len(couts))] +
+                      [f"r{i}" for i in range(1, len(couts))] + ["cat"]}
+    for i, k in enumerate(couts):
+        want = O.conv2d_forward(x, ws[i], bs[i], 1, 0)
+        assert_close(outs["1"][f"y{i}"], want, what=f"y{i} vs oracle")
+        assert_close(outs["1"][f"y{i}"], outs["0"][f"y{i}"], what=f"y{i} grouped vs not")
+        if i:
+            assert_bitwise(outs["1"][f"r{i}"], O.relu_forward(outs["1"][f"y{i}"]))
+    assert_bitwise(outs["1"]["cat"][:, :couts[0]], O.relu_forward(outs["1"]["y0"]))
+
+
 @pytest.mark.parametrize("shape,k,s,p", [((2, 1024, 7, 7), 7, 1, 0), ((2, 5, 9, 9), 3, 2, 1),
                                          ((2, 1000, 6, 6), 6, 1, 0)])
 def test_avgpool_bitwise(shape, k, s, p):

@@ -119,7 +119,11 @@ def test_epilogue_fusion_is_neutral(monkeypatch):
     the tensors of the unfused operators (every output of a GoogLeNet step);
     the bias gradients summed inside the weight gradient's dY pass agree with
     the stand-alone bias kernel at the contraction tolerance (different
-    summation blocking, so not bit for bit) and leave everything else exact."""
+    summation blocking, so not bit for bit) and leave everything else exact.
+    (The Inception 1x1 grouping changes the GEMM tile width and with it the
+    tensor-core accumulation scheme, so it is off here and checked at the
+    contraction tolerance in test_gpu_ops.py.)"""
+    monkeypatch.setenv("PURINE_B200_GROUP_1X1", "0")
     net = googlenet(batch=2, lr=0.01)
     seq = build_sgd_iteration(net)
     feed = SyntheticFeed.for_net(net, 5, spread=0.0)
