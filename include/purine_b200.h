@@ -175,6 +175,13 @@ int bf_conv1x1_fwd_group(const float* x, int N, int C, int H, int W, int nseg,
                          const float* const* w, const float* const* b, const int* kout,
                          float* const* y, float* const* relu, const int* relu_c0,
                          const int* relu_ctot, float* ws, int64_t ws_bytes, bf_stream_t stream);
+/* the data gradients of such a group summed in one GEMM: dx = sum_i w[i]^T dy[i]
+   over the K-concatenated dy[i] (N, kout[i], H, W) -- the Inception input
+   gradient's three 1x1 parts, which the graph then aggregates with the pool
+   branch's (ops.py:332-343 per part; the sum is reassociated: tolerance-level) */
+int bf_conv1x1_dgrad_group(int N, int C, int H, int W, int nseg, const float* const* dy,
+                           const float* const* w, const int* kout, float* dx, float* ws,
+                           int64_t ws_bytes, bf_stream_t stream);
 /* workspace bytes the conv/fc entry points want for this shape (0 = none) */
 int64_t bf_gemm_workspace_bytes(int op, int N, int C, int H, int W, int K, int R, int S,
                                 int P, int Q, int stride, int pad);

@@ -53,6 +53,7 @@ _SIGS = {
     "bf_fc_bwd_weight": [_p, _p, _p, _i, _i, _i, _p, _l, _p],
     "bf_fc_bwd_bias": [_p, _p, _i, _i, _p],
     "bf_conv1x1_fwd_group": [_p] + [_i] * 5 + [_p] * 7 + [_p, _l, _p],
+    "bf_conv1x1_dgrad_group": [_i] * 5 + [_p] * 4 + [_p, _l, _p],
     "bf_conv2d_fwd": [_p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_fwd_relu": [_p, _p, _p, _p, _p] + [_i] * 11 + [_p, _l, _p],
     "bf_conv2d_fwd_relu_slice": [_p, _p, _p, _p, _p, _i, _i] + [_i] * 11 + [_p, _l, _p],

@@ -127,6 +127,22 @@ int bf_conv1x1_fwd_group(const float* x, int N, int C, int H, int W, int nseg,
   return rc;
 }
 
+int bf_conv1x1_dgrad_group(int N, int C, int H, int W, int nseg, const float* const* dy,
+                           const float* const* w, const int* kout, float* dx, float* ws,
+                           int64_t ws_bytes, bf_stream_t s) {
+  BF_REQUIRE(nseg >= 1 && nseg <= kMaxSeg, "conv1x1 dgrad group: 1 <= nseg <= %d, got %d",
+             kMaxSeg, nseg);
+  BF_REQUIRE(N > 0 && C > 0 && H > 0 && W > 0, "conv1x1 dgrad group: non-positive dimension");
+  for (int i = 0; i < nseg; ++i)
+    BF_REQUIRE(kout[i] > 0 && dy[i] && w[i], "conv1x1 dgrad group: segment %d malformed", i);
+  BF_REQUIRE((int64_t)N * C * H * W < (1LL << 31), "conv1x1 dgrad group: tensor too large");
+  EpiNCHW epi{dx, nullptr, H * W, C};
+  const int rc = tc4_conv_dgrad_group(N, C, H * W, nseg, dy, w, kout, epi, ws, ws_bytes,
+                                      as_stream(s), "conv2d_backward_data(group)");
+  BF_REQUIRE(rc >= 0, "conv1x1 dgrad group: shape not taken by the TMA-fed 1x1 engine");
+  return rc;
+}
+
 int bf_conv2d_bwd_data(const float* w, const float* dy, float* dx, int N, int C, int H, int W,
                        int K, int R, int S, int P, int Q, int stride, int pad, float* ws,
                        int64_t ws_bytes, bf_stream_t s) {

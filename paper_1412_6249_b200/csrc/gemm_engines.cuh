@@ -38,6 +38,11 @@ int tc4_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNC
                  float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,
                    float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+// grouped 1x1 data gradients of convolutions over the same x: one GEMM over the
+// K-concatenated dy segments (each padded to 32 channels), i.e. their SUM
+int tc4_conv_dgrad_group(int N, int C, int HW, int nseg, const float* const* dy,
+                         const float* const* w, const int* kout, const EpiNCHW& epi, float* ws,
+                         int64_t ws_bytes, cudaStream_t st, const char* what);
 // horizontally fused 1x1 forward convolutions over the same x (segmented epilogue)
 int tc4_conv_fwd_group(const float* x, int N, int C, int HW, int nseg, const float* const* w,
                        const int* kout, const EpiNCHWSeg& epi, float* ws, int64_t ws_bytes,

@@ -61,6 +61,15 @@ struct Work {
   int tmem_cols;  // 512, or 256 when two CTAs share an SM (two MMA issuers)
   int sacc;       // 1: separate small-term accumulator (see the MMA issuer)
   int accw;       // TMEM columns per accumulator buffer (BN, or 2*BN with sacc)
+  // K segments (grouped data gradient): k-block kb < seg_kb[s + 1] of segment s
+  // comes from activation map s at k-block kb - seg_kb[s] (zero-filled rows past
+  // that tensor's channel count)
+  int nseg;
+  int seg_kb[kMaxSeg + 1];
+};
+
+struct ActMaps {
+  CUtensorMap m[kMaxSeg];
 };
 
 // MN-major tf32 operand: the only smem layout the tensor core accepts is
@@ -107,7 +116,7 @@ __device__ __forceinline__ void unit_coords(const Work& w, int u, int& img, int&
 
 template <class Epi>
 __global__ void __launch_bounds__(kThreads, 2)
-    tc4_kernel(const __grid_constant__ CUtensorMap amap, Work w, const uint8_t* __restrict__ bpack,
+    tc4_kernel(const __grid_constant__ ActMaps amaps, Work w, const uint8_t* __restrict__ bpack,
                Epi epi, EpiPartial part) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -138,7 +147,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(&acc_empty[b], kEpiWarps * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
+    for (int i = 0; i < w.nseg; ++i)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amaps.m[i]))
+                   : "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -164,10 +175,15 @@ __global__ void __launch_bounds__(kThreads, 2)
           mbar_wait(&empty[s], sph ^ 1);
           mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(kABytes + w.b_bytes));
           uint8_t* st = base + s * w.stage_bytes;
-          const int kc = (kb0 + i) * BK;
+          const int kb = kb0 + i;
+          int sg = 0;
+#pragma unroll
+          for (int q = 1; q < kMaxSeg; ++q) sg += (q < w.nseg && kb >= w.seg_kb[q]) ? 1 : 0;
+          const CUtensorMap* am = &amaps.m[sg];
+          const int kc = (kb - w.seg_kb[sg]) * BK;
 #pragma unroll
           for (int j = 0; j < BM / 32; ++j)
-            tma_load_3d(smem_u32(st + j * 4096), &amap, pt * BM + j * 32, kc, img, &raw_full[s]);
+            tma_load_3d(smem_u32(st + j * 4096), am, pt * BM + j * 32, kc, img, &raw_full[s]);
           bulk_g2s(smem_u32(st + 2 * kABytes),
                    bpack + ((size_t)nt * w.nkb + kb0 + i) * w.b_bytes, (uint32_t)w.b_bytes,
                    &raw_full[s]);
@@ -347,20 +363,34 @@ inline int pick_bn(int N, int& ntiles) {
 }
 
 // act: [imgs][K][PQ]; B(n, k) via lbp (pre-packed); D[m = img*PQ + pix][n] -> epi
+// act[s]: [imgs][kseg[s]][PQ], K = sum of kseg rounded up to 32 per segment
 template <class LBP, class Epi>
-int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, const Epi& epi,
-           float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
-  if (PQ % 4 || (reinterpret_cast<uintptr_t>(act) & 15) || K < 8) return -1;
-  CUtensorMap amap;
-  if (!make_act_map(&amap, act, PQ, K, imgs)) return -1;
+int launch_seg(int nseg, const float* const* act, const int* kseg, int imgs, int PQ, int Nout,
+               const LBP& lbp, const Epi& epi, float* ws, int64_t ws_bytes, cudaStream_t st,
+               const char* what) {
+  if (PQ % 4 || nseg < 1 || nseg > kMaxSeg) return -1;
+  ActMaps amaps{};
   Work w{};
+  w.nseg = nseg;
+  int kbs = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if ((reinterpret_cast<uintptr_t>(act[i]) & 15) || kseg[i] < 1) return -1;
+    if (!make_act_map(&amaps.m[i], act[i], PQ, kseg[i], imgs)) return -1;
+    w.seg_kb[i] = kbs;
+    kbs += (kseg[i] + BK - 1) / BK;
+  }
+  for (int i = nseg; i <= kMaxSeg; ++i) w.seg_kb[i] = kbs;
+  const int K = kbs * BK;
+  if (nseg == 1) {
+    if (kseg[0] < 8) return -1;
+  }
   w.PQ = PQ;
   w.tiles_img = (PQ + BM - 1) / BM;
   w.N_img = imgs;
   w.Nout = Nout;
-  w.K = K;
+  w.K = nseg == 1 ? kseg[0] : K;
   w.BN = pick_bn(Nout, w.ntiles);
-  w.nkb = (K + BK - 1) / BK;
+  w.nkb = kbs;
   w.nacc = 2;
   w.b_bytes = 2 * w.BN * 128;
   w.stage_bytes = 2 * kABytes + w.b_bytes;
@@ -390,7 +420,7 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
   const int64_t part_bytes = ws_bytes - pack_aligned;
   const int M = imgs * PQ;
 
-  launch_pack_b(lbp, Nout, K, w.BN, w.nkb, w.ntiles, bpack, st);
+  launch_pack_b(lbp, Nout, w.K, w.BN, w.nkb, w.ntiles, bpack, st);
   if (int rc = check_launch(what)) return rc;
 
   const int sms = gemm_sm_budget();
@@ -423,13 +453,19 @@ int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, 
   const int smem = std::max(tail + w.nst * w.stage_bytes, (pair ? 109 : 120) << 10);
   const int grid = std::min(w.units, pair ? 2 * sms : sms);
   EpiPartial part{part_ws, M, Nout};
-  tc4_kernel<Epi><<<grid, kThreads, smem, st>>>(amap, w, bpack, epi, part);
+  tc4_kernel<Epi><<<grid, kThreads, smem, st>>>(amaps, w, bpack, epi, part);
   if (int rc = check_launch(what)) return rc;
   if (w.splits > 1) {
     splitk_reduce<Epi>(part_ws, w.splits, M, Nout, epi, st);
     return check_launch(what);
   }
   return 0;
+}
+
+template <class LBP, class Epi>
+int launch(const float* act, int imgs, int K, int PQ, int Nout, const LBP& lbp, const Epi& epi,
+           float* ws, int64_t ws_bytes, cudaStream_t st, const char* what) {
+  return launch_seg(1, &act, &K, imgs, PQ, Nout, lbp, epi, ws, ws_bytes, st, what);
 }
 
 struct LdW1x1 {  // fwd: B(n = kout, k = c) = w[kout][c]
@@ -448,6 +484,19 @@ struct LdW1x1Cat {  // grouped fwd: B(n, k) = w[s][n - start[s]][k], n in segmen
 #pragma unroll
     for (int i = 1; i < kMaxSeg; ++i) s += (i < nseg && n >= start[i]) ? 1 : 0;
     return w[s][(int64_t)(n - start[s]) * C + k];
+  }
+};
+struct LdW1x1TCat {  // grouped dgrad: B(n = c, k) = w[s][k - kstart[s]][c], zero in the padding
+  const float* w[kMaxSeg];
+  int kstart[kMaxSeg + 1];  // 32-aligned segment starts in the padded K
+  int kout[kMaxSeg];
+  int nseg, C;
+  __device__ __forceinline__ float operator()(int n, int k) const {
+    int s = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxSeg; ++i) s += (i < nseg && k >= kstart[i]) ? 1 : 0;
+    const int kk = k - kstart[s];
+    return kk < kout[s] ? w[s][(int64_t)kk * C + n] : 0.f;
   }
 };
 struct LdW1x1T {  // dgrad: B(n = c, k = kout) = w[kout][c]
@@ -488,6 +537,24 @@ int tc4_conv_fwd_group(const float* x, int N, int C, int HW, int nseg, const flo
   lb.start[nseg] = n;
   for (int i = nseg + 1; i <= kMaxSeg; ++i) lb.start[i] = n;
   return tc4::launch(x, N, C, HW, n, lb, epi, ws, ws_bytes, st, what);
+}
+
+int tc4_conv_dgrad_group(int N, int C, int HW, int nseg, const float* const* dy,
+                         const float* const* w, const int* kout, const EpiNCHW& epi, float* ws,
+                         int64_t ws_bytes, cudaStream_t st, const char* what) {
+  if (nseg < 1 || nseg > kMaxSeg || HW % 4) return -1;
+  tc4::LdW1x1TCat lb{};
+  lb.nseg = nseg;
+  lb.C = C;
+  int k = 0;
+  for (int i = 0; i < nseg; ++i) {
+    lb.w[i] = w[i];
+    lb.kout[i] = kout[i];
+    lb.kstart[i] = k;
+    k += (kout[i] + tc4::BK - 1) / tc4::BK * tc4::BK;
+  }
+  for (int i = nseg; i <= kMaxSeg; ++i) lb.kstart[i] = k;
+  return tc4::launch_seg(nseg, dy, kout, N, HW, C, lb, epi, ws, ws_bytes, st, what);
 }
 
 int tc4_conv_dgrad(const ConvShape& g, const float* dy, const float* w, const EpiNCHW& epi,

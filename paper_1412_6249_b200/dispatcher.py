@@ -508,8 +508,75 @@ class _Plan:
             self.elided.add(graph.tensors[sc].name)
 
         self._group_1x1(graph)
+        self._group_1x1_dgrad(graph)
         self.finite_mode = _finite_mode()
         self.finite_watch = _finite_watch(graph, self, self.finite_mode)
+
+    def _group_1x1_dgrad(self, graph: BiGraph) -> None:
+        """The backward half of the Inception 1x1 grouping: the data gradients
+        of sibling 1x1 convolutions (same x) whose outputs only feed the same
+        aggregate(sum) -- the module's input gradient -- are computed as ONE
+        GEMM over their K-concatenated dy, which IS their sum
+        (bf_conv1x1_dgrad_group): one launch and one dx write instead of three,
+        and the aggregate (or the ReLU-backward slice sums it is folded into)
+        adds two parts instead of four.  The GEMM runs at the LAST member in
+        serial order (every member's dy is ready there) into that member's
+        output buffer; the earlier members become no-ops.  The member outputs
+        are listed in ``elided`` (none holds its own part any more); the sum
+        is reassociated, so it agrees at the contraction tolerance."""
+        if os.environ.get(GROUP_ENV, "1") == "0":
+            return
+        from .kinds import conv_attrs
+
+        pos = {oid: i for i, oid in enumerate(self.order)}
+        for aid, agg in graph.operators.items():
+            if agg.kind != "aggregate" or agg.attrs.get("mode", "mean") != "sum":
+                continue
+            cand: dict[int, list[int]] = {}
+            for t in agg.inputs:
+                p = graph.producer_of(t)
+                if p is None or p in self.fusion or p in self.fused_away:
+                    continue
+                op = graph.operators[p]
+                if op.kind != "conv2d_backward_data" or len(graph.consumers_of(t)) != 1:
+                    continue
+                w = graph.tensors[op.inputs[1]]
+                x = graph.tensors[op.inputs[0]]
+                stride, pad, _floor = conv_attrs(op.attrs)
+                if (len(w.shape) != 4 or w.shape[2:] != (1, 1) or stride != 1 or pad != 0
+                        or (x.shape[2] * x.shape[3]) % 4):
+                    continue
+                cand.setdefault(op.inputs[0], []).append(p)
+            for members in cand.values():
+                if len(members) < 2:
+                    continue
+                members = sorted(members, key=pos.__getitem__)[-4:]
+                lead = members[-1]
+                self.fusion[lead] = {"group_dgrad": [graph.operators[m] for m in members]}
+                for m in members[:-1]:
+                    self.fused_away.add(m)
+                    self.fusion[m] = {"group_member": lead}
+                    # the lead reads every member's dy: wait for their producers
+                    for t in graph.operators[m].inputs:
+                        pr = graph.producer_of(t)
+                        if pr is not None and self.slot[pr] != self.slot[lead] \
+                                and pr not in self.waits[lead]:
+                            self.waits[lead].append(pr)
+                            self.signals.add(pr)
+                gone = {graph.tensors[graph.operators[m].outputs[0]].name for m in members[:-1]}
+                lead_out = graph.tensors[graph.operators[lead].outputs[0]].name
+                for m in members:
+                    self.elided.add(graph.tensors[graph.operators[m].outputs[0]].name)
+                # the aggregate (or the slice sums it is folded into) now adds the
+                # group's sum once, in the lead's place, and skips the others
+                names = [graph.tensors[t].name for t in agg.inputs]
+                kept = [n for n in names if n not in gone]
+                self.fusion.setdefault(aid, {})["agg_parts"] = kept
+                for f in self.fusion.values():
+                    if "dy_parts" in f and f["dy_parts"][0] == names:
+                        _names, c0, ctot = f["dy_parts"]
+                        f["dy_parts"] = (kept, c0, ctot)
+                assert lead_out in kept
 
     def _group_1x1(self, graph: BiGraph) -> None:
         """Horizontal fusion (Inception): the 1x1 stride-1 conv2d_forward

@@ -188,7 +188,32 @@ def _relu_fold(ctx, op):
     return rx, ctx.store.ensure(fused["relu_dx"], rx.shape)
 
 
+def _conv_bwd_data_group(ctx, op, members):
+    """Sibling 1x1 data gradients summed in one GEMM into ``op``'s output
+    (dispatcher _Plan._group_1x1_dgrad)."""
+    import ctypes as C
+
+    g = ctx.graph
+    x = ctx.store.get(g.tensors[op.inputs[0]].name)
+    n, c, h, wd = x.shape
+    (dx,) = _outs(ctx, op)
+    dys, ws_, ks = [], [], []
+    for mop in members:
+        _x, w, dy = _ins(ctx, mop)
+        dys.append(dy.ptr)
+        ws_.append(w.ptr)
+        ks.append(w.shape[0])
+    k = len(members)
+    P = C.c_void_p * k
+    _L()("bf_conv1x1_dgrad_group", n, c, h, wd, k, P(*dys), P(*ws_), (C.c_int * k)(*ks), dx.ptr,
+         *_ws(ctx), ctx.stream)
+
+
 def _conv_bwd_data(ctx, op):
+    fused = getattr(ctx, "fused", None)
+    if fused and "group_dgrad" in fused:
+        _conv_bwd_data_group(ctx, op, fused["group_dgrad"])
+        return
     x, w, dy = _ins(ctx, op)
     rx, rdx = _relu_fold(ctx, op)
     if rx is not None:
@@ -287,7 +312,11 @@ def _sgd_momentum(ctx, op):
 
 
 def _aggregate(ctx, op):
-    parts = _ins(ctx, op)
+    fused = getattr(ctx, "fused", None)
+    if fused and "agg_parts" in fused:  # some parts were summed by a grouped data gradient
+        parts = [ctx.store.get(n) for n in fused["agg_parts"]]
+    else:
+        parts = _ins(ctx, op)
     (out,) = _outs(ctx, op)
     mode = op.attrs.get("mode", "mean")
     if mode not in ("sum", "mean"):
