@@ -193,7 +193,10 @@ int bf_conv2d_bwd_weight_bias(const float* x, const float* dy, float* dw, float*
   EpiT epi{dw, nullptr, (int64_t)C * R * S};
   int rc = -1;
   bool db_done = false;
-  if (g_gemm_engine == 0)
+  if (g_gemm_engine == 0 && C * R * S <= 256 && stride >= 2)
+    rc = wgrad_t_conv(g, x, dy, dw, db, &db_done, ws, ws_bytes, as_stream(s),
+                      "conv2d_backward_weight");
+  if (rc < 0 && g_gemm_engine == 0)
     rc = s2d_conv_wgrad(g, x, dy, dw, db, &db_done, ws, ws_bytes, as_stream(s),
                         "conv2d_backward_weight");
   if (rc < 0 && (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3 || g_gemm_engine == 4))

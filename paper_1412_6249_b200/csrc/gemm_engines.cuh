@@ -56,6 +56,12 @@ int s2d_conv_wgrad(const ConvShape& g, const float* x, const float* dy, float* d
                    bool* db_done, float* ws, int64_t ws_bytes, cudaStream_t st,
                    const char* what);
 
+// transposed weight gradient for few-input-channel convolutions (conv1):
+// D[kout][(c,r,s)] with dY by TMA and the im2col from contiguous windows
+// (gemm_wgrad_t.cu); -1 when not taken
+int wgrad_t_conv(const ConvShape& g, const float* x, const float* dy, float* dw, float* db,
+                 bool* db_done, float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+
 extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in),
                            // 4 auto without v4, 5 auto without the TMA-fed 1x1 weight gradient,
                            // 6 auto with register-prefetched (not cp.async-staged) gathers,

@@ -49,6 +49,8 @@ CONV_CASES = [
     (2, 5, 19, 17, 24, 7, 1, 3, False),           # 7x7 stride 1 on 5 channels
     (1, 2, 16, 16, 40, 8, 3, 2, False),           # 8x8 stride 3
     (2, 8, 32, 32, 256, 3, 1, 1, False),          # TMA-streamed dY wgrad, two dY tiles
+    (3, 4, 32, 32, 16, 5, 2, 2, True),            # transposed wgrad (gemm_wgrad_t.cu), Q = 16
+    (2, 3, 36, 36, 64, 7, 2, 3, True),            # conv1 geometry small: Q = 18, 2 q-blocks
 ]
 
 
