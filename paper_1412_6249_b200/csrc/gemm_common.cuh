@@ -474,8 +474,13 @@ inline void splitk_reduce(const float* ws, int splits, int M, int N, const Epi& 
 // disables the bound.
 constexpr int kMaxSplits = 4096;
 int max_chain_kb();
-inline int64_t chain_min_splits(int64_t nkb) {
-  const int c = max_chain_kb();
+// sacc: the tile keeps its small terms in a separate accumulator (one
+// truncating accumulation of the big part per k-step instead of three), so a
+// chain may be three times as long for the same error (precision_probe,
+// K = 401k: 32-k-block chains 1.7e-6 of max |ref| with it vs 6.4e-6 without;
+// 96-k-block chains 5.1e-6)
+inline int64_t chain_min_splits(int64_t nkb, bool sacc = false) {
+  const int c = max_chain_kb() * (sacc ? 3 : 1);
   return c > 0 ? (nkb + c - 1) / c : 1;
 }
 

@@ -1244,7 +1244,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
     const bool wgrad_pack = std::is_same_v<LBP, LdWgradDYPad>;
     if (tiles < sms && (wgrad_pack || tiles < TC2_NOSPLIT_MIN_TILES)) {
       int64_t want = sms / tiles;  // one wave: units <= SMs (ceil would leave a 2-unit tail)
-      if (wgrad_pack) want = std::max(want, chain_min_splits(w.nkb));
+      if (wgrad_pack) want = std::max(want, chain_min_splits(w.nkb, w.sacc != 0));
       int64_t by_k = w.nkb / 4;
       int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
       const int64_t cap = std::min(by_k, std::min<int64_t>(by_ws, kMaxSplits));
@@ -1253,7 +1253,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
     } else if (wgrad_pack) {  // many tiles: split only as far as the chain bound needs
       const int64_t by_ws = part_bytes / ((int64_t)M * N * 4);
       const int64_t cap = std::min<int64_t>(by_ws, kMaxSplits);
-      w.splits = (int)std::max<int64_t>(1, std::min(chain_min_splits(w.nkb), cap));
+      w.splits = (int)std::max<int64_t>(1, std::min(chain_min_splits(w.nkb, w.sacc != 0), cap));
       w.splits = (int)balance_splits(tiles, w.nkb, w.splits, cap, sms);
     }
   }
@@ -1373,7 +1373,7 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
     const int64_t tiles = (int64_t)w.mtiles * w.ntiles;
     {
       const int64_t want = std::max<int64_t>(tiles < sms ? sms / tiles : 1,
-                                             chain_min_splits(w.nkb));
+                                             chain_min_splits(w.nkb, w.sacc != 0));
       const int64_t by_k = std::max<int64_t>(1, w.nkb / 4);
       const int64_t by_ws = part_bytes / ((int64_t)M * Kout * 4);
       const int64_t cap = std::min(by_k, std::min<int64_t>(by_ws, kMaxSplits));
@@ -1449,7 +1449,7 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
     const int64_t tiles = (int64_t)w.mtiles * w.ntiles;
     {
       const int64_t want = std::max<int64_t>(tiles < sms ? sms / tiles : 1,
-                                             chain_min_splits(w.nkb));
+                                             chain_min_splits(w.nkb, w.sacc != 0));
       const int64_t by_k = std::max<int64_t>(1, w.nkb / 4);
       const int64_t by_ws = part_bytes / ((int64_t)C * Kout * 4);
       const int64_t cap = std::min(by_k, std::min<int64_t>(by_ws, kMaxSplits));

@@ -454,7 +454,7 @@ int wgrad_t_conv(const ConvShape& g, const float* x, const float* dy, float* dw,
   if (smem > smem_cap) return -1;
   // units: chains of at most max_chain_kb() k-blocks, balanced over the grid
   const int sms = gemm_sm_budget();
-  const int64_t chain = std::max<int64_t>(1, chain_min_splits(q.nkb));
+  const int64_t chain = std::max<int64_t>(1, chain_min_splits(q.nkb, true));
   const int64_t bias_bytes = db ? ((int64_t)g.K * kMaxSplits * 4 + 1023) / 1024 * 1024 : 0;
   if (!ws || ws_bytes < bias_bytes) return -1;
   const int64_t by_ws = (ws_bytes - bias_bytes) / ((int64_t)g.K * CRS * 4);
