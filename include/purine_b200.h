@@ -78,6 +78,15 @@ int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, flo
    aggregate(sum) -> concat_backward pair is elided */
 int bf_relu_bwd_slice_sum(const float* x, const float* const* parts, int k, int c0, int ctot,
                           float* dx, int N, int C, int64_t HW, bf_stream_t stream);
+/* the two above with the mask x itself a channel slice [x_c0, x_c0 + C) of an
+   x_ctot-channel tensor: the ReLU OUTPUT's slice of the (elided-concat)
+   concat output, relu(a) > 0 <=> a > 0 -- the pre-activation is then never
+   stored (dispatcher pre-activation elision) */
+int bf_relu_bwd_slice_x(const float* x, int x_c0, int x_ctot, const float* dy_cat, int c0,
+                        int ctot, float* dx, int N, int C, int64_t HW, bf_stream_t stream);
+int bf_relu_bwd_slice_sum_x(const float* x, int x_c0, int x_ctot, const float* const* parts,
+                            int k, int c0, int ctot, float* dx, int N, int C, int64_t HW,
+                            bf_stream_t stream);
 /* sgd_update, ops.py:428-437: out = w - f32(lr)*g, product rounded first */
 int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t n,
                   bf_stream_t stream);
@@ -126,7 +135,9 @@ int bf_conv2d_fwd(const float* x, const float* w, const float* b, float* y,
                   int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                   int stride, int pad, float* workspace, int64_t ws_bytes, bf_stream_t stream);
 /* conv2d_forward followed by relu_forward (ops.py:359-364) in one kernel:
-   writes the pre-activation y (kept: relu_backward reads it) and relu(y) */
+   writes the pre-activation y and relu(y).  y may be NULL (the dispatcher's
+   pre-activation elision: nothing reads y, every relu_backward of this ReLU
+   takes relu(y) as its mask): only relu(y) is written */
 int bf_conv2d_fwd_relu(const float* x, const float* w, const float* b, float* y, float* y_relu,
                        int N, int C, int H, int W, int K, int R, int S, int P, int Q,
                        int stride, int pad, float* workspace, int64_t ws_bytes,
@@ -169,7 +180,7 @@ int bf_conv2d_bwd_bias(const float* dy, float* db, int N, int K, int PQ, float* 
    [kout[i]][C], bias b[i] (may be NULL), output y[i] (N, kout[i], H, W) and,
    if relu[i] != NULL, relu(y) into channels [relu_c0[i], relu_c0[i] + kout[i])
    of the relu_ctot[i]-channel tensor relu[i] (the fused relu_forward, possibly
-   into a concat slice).  Host arrays of device pointers.  Same arithmetic per
+   into a concat slice); y[i] may be NULL when relu[i] is not.  Host arrays of device pointers.  Same arithmetic per
    output as bf_conv2d_fwd_relu_slice (ops.py:281-297) */
 int bf_conv1x1_fwd_group(const float* x, int N, int C, int H, int W, int nseg,
                          const float* const* w, const float* const* b, const int* kout,

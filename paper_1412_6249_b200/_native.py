@@ -39,6 +39,8 @@ _SIGS = {
     "bf_relu_bwd": [_p, _p, _p, _l, _p],
     "bf_relu_bwd_slice": [_p, _p, _i, _i, _p, _i, _i, _l, _p],
     "bf_relu_bwd_slice_sum": [_p, _p, _i, _i, _i, _p, _i, _i, _l, _p],
+    "bf_relu_bwd_slice_x": [_p, _i, _i, _p, _i, _i, _p, _i, _i, _l, _p],
+    "bf_relu_bwd_slice_sum_x": [_p, _i, _i, _p, _i, _i, _i, _p, _i, _i, _l, _p],
     "bf_sgd_update": [_p, _p, _p, _f, _l, _p],
     "bf_sgd_momentum": [_p, _p, _p, _p, _p, _f, _f, _l, _p],
     "bf_sgd_mean_update": [_p, _p, _p, _f, _i, _l, _p],

@@ -102,24 +102,26 @@ __global__ void relu_bwd_s(const float* __restrict__ x, const float* __restrict_
 // relu_backward with dy read as a channel slice of a concatenated gradient
 // (the graph's concat_backward copy is elided): image n of dx/x covers
 // `run` = C*HW contiguous elements, its dy run starts at n*dy_img + dy_off
+// x (the ReLU mask) likewise at img*x_img + x_off: the pre-activation itself
+// (x_img = run, x_off = 0) or the ReLU output's slice of the concat output
 __global__ void relu_bwd_slice_v4(const float4* __restrict__ x, const float4* __restrict__ dy,
                                   float4* __restrict__ dx, int64_t run4, int64_t dy_img4,
-                                  int64_t dy_off4, int64_t n4) {
+                                  int64_t dy_off4, int64_t x_img4, int64_t x_off4, int64_t n4) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t img = i / run4, r = i - img * run4;
-    float4 a = x[i], g = dy[img * dy_img4 + dy_off4 + r];
+    float4 a = x[img * x_img4 + x_off4 + r], g = dy[img * dy_img4 + dy_off4 + r];
     dx[i] = make_float4(relu_g(a.x, g.x), relu_g(a.y, g.y), relu_g(a.z, g.z), relu_g(a.w, g.w));
   }
 }
 
 __global__ void relu_bwd_slice_s(const float* __restrict__ x, const float* __restrict__ dy,
                                  float* __restrict__ dx, int64_t run, int64_t dy_img,
-                                 int64_t dy_off, int64_t n) {
+                                 int64_t dy_off, int64_t x_img, int64_t x_off, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t img = i / run, r = i - img * run;
-    dx[i] = relu_g(x[i], dy[img * dy_img + dy_off + r]);
+    dx[i] = relu_g(x[img * x_img + x_off + r], dy[img * dy_img + dy_off + r]);
   }
 }
 
@@ -368,7 +370,8 @@ int bf_relu_bwd(const float* x, const float* dy, float* dx, int64_t n, bf_stream
 // elided (ops.py:440-457 order: ((p0 + p1) + p2) + ...)
 __global__ void relu_bwd_slice_sum_v4(const float4* __restrict__ x, Parts parts, int k,
                                       float4* __restrict__ dx, int64_t run4, int64_t dy_img4,
-                                      int64_t dy_off4, int64_t n4) {
+                                      int64_t dy_off4, int64_t x_img4, int64_t x_off4,
+                                      int64_t n4) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t img = i / run4, r = i - img * run4;
@@ -381,28 +384,30 @@ __global__ void relu_bwd_slice_sum_v4(const float4* __restrict__ x, Parts parts,
       g.z = __fadd_rn(g.z, v.z);
       g.w = __fadd_rn(g.w, v.w);
     }
-    const float4 a = x[i];
+    const float4 a = x[img * x_img4 + x_off4 + r];
     dx[i] = make_float4(relu_g(a.x, g.x), relu_g(a.y, g.y), relu_g(a.z, g.z), relu_g(a.w, g.w));
   }
 }
 
 __global__ void relu_bwd_slice_sum_s(const float* __restrict__ x, Parts parts, int k,
                                      float* __restrict__ dx, int64_t run, int64_t dy_img,
-                                     int64_t dy_off, int64_t n) {
+                                     int64_t dy_off, int64_t x_img, int64_t x_off, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t img = i / run, r = i - img * run;
     const int64_t j = img * dy_img + dy_off + r;
     float g = parts.p[0][j];
     for (int q = 1; q < k; ++q) g = __fadd_rn(g, parts.p[q][j]);
-    dx[i] = relu_g(x[i], g);
+    dx[i] = relu_g(x[img * x_img + x_off + r], g);
   }
 }
 
-int bf_relu_bwd_slice_sum(const float* x, const float* const* parts, int k, int c0, int ctot,
-                          float* dx, int N, int C, int64_t HW, bf_stream_t s) {
+int bf_relu_bwd_slice_sum_x(const float* x, int x_c0, int x_ctot, const float* const* parts,
+                            int k, int c0, int ctot, float* dx, int N, int C, int64_t HW,
+                            bf_stream_t s) {
   BF_REQUIRE(k >= 1 && k <= 32, "relu_backward(slice sum): 1 <= k <= 32 parts, got %d", k);
   BF_REQUIRE(N >= 0 && C >= 0 && c0 >= 0 && c0 + C <= ctot, "relu_backward(slice): bad channels");
+  BF_REQUIRE(x_c0 >= 0 && x_c0 + C <= x_ctot, "relu_backward(slice): bad mask channels");
   const int64_t run = (int64_t)C * HW, n = run * N;
   if (n <= 0) return 0;
   cudaStream_t st = as_stream(s);
@@ -415,16 +420,24 @@ int bf_relu_bwd_slice_sum(const float* x, const float* const* parts, int k, int 
   if (vec)
     relu_bwd_slice_sum_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
         reinterpret_cast<const float4*>(x), p, k, reinterpret_cast<float4*>(dx), run / 4,
-        (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4, n / 4);
+        (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4, (int64_t)x_ctot * HW / 4,
+        (int64_t)x_c0 * HW / 4, n / 4);
   else
     relu_bwd_slice_sum_s<<<elementwise_grid(n, kThreads), kThreads, 0, st>>>(
-        x, p, k, dx, run, (int64_t)ctot * HW, (int64_t)c0 * HW, n);
+        x, p, k, dx, run, (int64_t)ctot * HW, (int64_t)c0 * HW, (int64_t)x_ctot * HW,
+        (int64_t)x_c0 * HW, n);
   return check_launch("relu_backward");
 }
 
-int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, float* dx, int N,
-                      int C, int64_t HW, bf_stream_t s) {
+int bf_relu_bwd_slice_sum(const float* x, const float* const* parts, int k, int c0, int ctot,
+                          float* dx, int N, int C, int64_t HW, bf_stream_t s) {
+  return bf_relu_bwd_slice_sum_x(x, 0, C, parts, k, c0, ctot, dx, N, C, HW, s);
+}
+
+int bf_relu_bwd_slice_x(const float* x, int x_c0, int x_ctot, const float* dy_cat, int c0,
+                        int ctot, float* dx, int N, int C, int64_t HW, bf_stream_t s) {
   BF_REQUIRE(N >= 0 && C >= 0 && c0 >= 0 && c0 + C <= ctot, "relu_backward(slice): bad channels");
+  BF_REQUIRE(x_c0 >= 0 && x_c0 + C <= x_ctot, "relu_backward(slice): bad mask channels");
   const int64_t run = (int64_t)C * HW, n = run * N;
   if (n <= 0) return 0;
   cudaStream_t st = as_stream(s);
@@ -432,12 +445,18 @@ int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, flo
     relu_bwd_slice_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
         reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy_cat),
         reinterpret_cast<float4*>(dx), run / 4, (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4,
-        n / 4);
+        (int64_t)x_ctot * HW / 4, (int64_t)x_c0 * HW / 4, n / 4);
   } else {
     relu_bwd_slice_s<<<elementwise_grid(n, kThreads), kThreads, 0, st>>>(
-        x, dy_cat, dx, run, (int64_t)ctot * HW, (int64_t)c0 * HW, n);
+        x, dy_cat, dx, run, (int64_t)ctot * HW, (int64_t)c0 * HW, (int64_t)x_ctot * HW,
+        (int64_t)x_c0 * HW, n);
   }
   return check_launch("relu_backward");
+}
+
+int bf_relu_bwd_slice(const float* x, const float* dy_cat, int c0, int ctot, float* dx, int N,
+                      int C, int64_t HW, bf_stream_t s) {
+  return bf_relu_bwd_slice_x(x, 0, C, dy_cat, c0, ctot, dx, N, C, HW, s);
 }
 
 int bf_sgd_update(const float* w, const float* g, float* out, float lr, int64_t n,

@@ -69,12 +69,18 @@ int bf_conv2d_fwd_relu_slice(const float* x, const float* w, const float* b, flo
   if (int rc = check_conv(N, C, H, W, K, R, S, P, Q, stride, pad)) return rc;
   BF_REQUIRE(!relu_cat || (relu_c0 >= 0 && relu_c0 + K <= relu_ctot),
              "conv2d_forward(+relu slice): bad channel range");
+  BF_REQUIRE(y || relu_cat, "conv2d_forward: no output (y and the ReLU target are both NULL)");
   ConvShape g{N, C, H, W, K, R, S, P, Q, stride, pad};
   LdFwdX la{x, g};
   LdRowK lb{w, (int64_t)C * R * S};
   EpiNCHW epi{y, b, P * Q, K, relu_cat, (int64_t)relu_ctot * P * Q, relu_c0};
+  epi.no_out = y == nullptr;  // pre-activation not stored: only the ReLU output
   if (g_gemm_engine == 0 || g_gemm_engine == 5 || g_gemm_engine == 6 || g_gemm_engine == 7 || g_gemm_engine == 3) {
     int rc = tc4_conv_fwd(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
+    if (rc >= 0) return rc;
+  }
+  if (g_gemm_engine == 0 && C * R * S <= 256 && K <= 64 && !s2d_enabled()) {
+    int rc = fwd_win_conv(g, x, w, epi, ws, ws_bytes, as_stream(s), "conv2d_forward");
     if (rc >= 0) return rc;
   }
   if (g_gemm_engine == 0) {
@@ -106,7 +112,8 @@ int bf_conv1x1_fwd_group(const float* x, int N, int C, int H, int W, int nseg,
   epi.nseg = nseg;
   int n = 0;
   for (int i = 0; i < nseg; ++i) {
-    BF_REQUIRE(kout[i] > 0 && w[i] && y[i], "conv1x1 group: segment %d malformed", i);
+    BF_REQUIRE(kout[i] > 0 && w[i] && (y[i] || relu[i]), "conv1x1 group: segment %d malformed",
+               i);
     BF_REQUIRE(!relu[i] || (relu_c0[i] >= 0 && relu_c0[i] + kout[i] <= relu_ctot[i]),
                "conv1x1 group: segment %d relu channel range", i);
     epi.start[i] = n;

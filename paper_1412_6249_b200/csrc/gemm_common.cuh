@@ -152,12 +152,16 @@ struct EpiNCHW {
   int relu_c0 = 0;
   // relu_backward folded in (dgrad): out = (relu_x > 0 ? v : 0), relu_x laid out as out
   const float* relu_x = nullptr;
+  // the pre-activation has no reader (dispatcher: every consumer is fused or
+  // reads the ReLU output instead): only the ReLU output is stored.  `out`
+  // is then only the base of the row arithmetic (never dereferenced)
+  bool no_out = false;
   __device__ __forceinline__ void operator()(int m, int n, float v) const {
     int img = m / PQ, pq = m - img * PQ;
     if (bias) v = __fadd_rn(v, bias[n]);
     const int64_t o = ((int64_t)img * Cout + n) * PQ + pq;
     if (relu_x) v = relu_x[o] > 0.f ? v : 0.f;
-    out[o] = v;
+    if (!no_out) out[o] = v;
     if (relu_out) relu_out[relu_index(img, pq) + (int64_t)n * PQ] = relu_value(v);
   }
   __device__ __forceinline__ int64_t relu_index(int img, int pq) const {
@@ -173,7 +177,7 @@ struct EpiNCHW {
     if (bias) v = __fadd_rn(v, __ldg(bias + n));
     float* p = r.p + (int64_t)n * PQ;
     if (relu_x) v = __ldg(relu_x + (p - out)) > 0.f ? v : 0.f;
-    *p = v;
+    if (!no_out) *p = v;
     if (relu_out) p[r.relu_delta] = relu_value(v);
   }
   // 16 consecutive columns of one row (the tcgen05 epilogues).  Column j of
@@ -205,6 +209,18 @@ struct EpiNCHW {
     }
     if (nlim >= 16 && !rx) {  // forward with the fused ReLU output
       const int64_t rd = r.relu_delta;
+      if (no_out) {
+        float b[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) b[j] = bs ? __ldg(bs + n0 + j) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float x = __uint_as_float(v[j]);
+          if (bs) x = __fadd_rn(x, b[j]);
+          __stcg(p + j * stride + rd, relu_value(x));
+        }
+        return;
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         float x = __uint_as_float(v[j]);
@@ -237,7 +253,7 @@ struct EpiNCHW {
       float x = __uint_as_float(v[j]);
       if (bs) x = __fadd_rn(x, __ldg(bs + n0 + j));
       if (rx) x = m[j] > 0.f ? x : 0.f;
-      __stcg(p + j * stride, x);
+      if (!no_out) __stcg(p + j * stride, x);
       if (ro) __stcg(p + j * stride + r.relu_delta, relu_value(x));
     }
   }
@@ -268,7 +284,7 @@ struct EpiNCHWSeg {
   __device__ __forceinline__ void put(int img, int pq, int n, float v) const {
     const int s = seg_of(n), j = n - start[s];
     if (bias[s]) v = __fadd_rn(v, __ldg(bias[s] + j));
-    __stcg(out[s] + ((int64_t)img * cout[s] + j) * PQ + pq, v);
+    if (out[s]) __stcg(out[s] + ((int64_t)img * cout[s] + j) * PQ + pq, v);
     if (relu[s]) __stcg(relu[s] + (int64_t)img * relu_img[s] + (int64_t)(relu_c0[s] + j) * PQ + pq,
                         relu_value(v));
   }
@@ -284,7 +300,7 @@ struct EpiNCHWSeg {
     const int64_t stride = PQ;
     if (nlim >= 16 && n0 + 15 < start[s + 1]) {  // the chunk lies in one segment
       const int j0 = n0 - start[s];
-      float* p = out[s] + ((int64_t)img * cout[s] + j0) * PQ + pq;
+      float* p = out[s] ? out[s] + ((int64_t)img * cout[s] + j0) * PQ + pq : nullptr;
       const float* bs = bias[s];
       float* rp = relu[s] ? relu[s] + (int64_t)img * relu_img[s] +
                                 (int64_t)(relu_c0[s] + j0) * PQ + pq
@@ -293,7 +309,7 @@ struct EpiNCHWSeg {
       for (int j = 0; j < 16; ++j) {
         float x = __uint_as_float(v[j]);
         if (bs) x = __fadd_rn(x, __ldg(bs + j0 + j));
-        __stcg(p + j * stride, x);
+        if (p) __stcg(p + j * stride, x);
         if (rp) __stcg(rp + j * stride, relu_value(x));
       }
       return;

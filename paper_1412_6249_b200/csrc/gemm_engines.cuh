@@ -50,6 +50,7 @@ int tc4_conv_fwd_group(const float* x, int N, int C, int HW, int nseg, const flo
 
 // strided convolutions (C*stride^2 <= 64 channels, kernel wider than the
 // stride) as stride-1 convolutions over a space-to-depth view (conv_s2d.cu)
+bool s2d_enabled();  // PURINE_B200_S2D=1 (opt-in)
 int s2d_conv_fwd(const ConvShape& g, const float* x, const float* w, const EpiNCHW& epi,
                  float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 int s2d_conv_wgrad(const ConvShape& g, const float* x, const float* dy, float* dw, float* db,
@@ -61,6 +62,11 @@ int s2d_conv_wgrad(const ConvShape& g, const float* x, const float* dy, float* d
 // (gemm_wgrad_t.cu); -1 when not taken
 int wgrad_t_conv(const ConvShape& g, const float* x, const float* dy, float* dw, float* db,
                  bool* db_done, float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
+
+// forward of a few-input-channel convolution (conv1) from contiguous input-row
+// windows, weights resident in shared memory (gemm_fwd_win.cu); -1 when not taken
+int fwd_win_conv(const ConvShape& g, const float* x, const float* w, const EpiNCHW& epi,
+                 float* ws, int64_t ws_bytes, cudaStream_t st, const char* what);
 
 extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo engine v3 (opt-in),
                            // 4 auto without v4, 5 auto without the TMA-fed 1x1 weight gradient,

@@ -112,18 +112,18 @@ def _conv_fwd_group(ctx, members):
     ws_, bs, ks, ys, rs, r0, rt = [], [], [], [], [], [], []
     for mop, mf in members:
         _x, w, b = _ins(ctx, mop)
-        (y,) = _outs(ctx, mop)
+        yshape = g.tensors[mop.outputs[0]].shape
         ws_.append(w.ptr)
         bs.append(b.ptr)
         ks.append(w.shape[0])
-        ys.append(y.ptr)
+        ys.append(None if mf.get("no_y") else _outs(ctx, mop)[0].ptr)
         if "relu_slice" in mf:
             name, shape, c0 = mf["relu_slice"]
             rs.append(ctx.store.ensure(name, shape).ptr)
             r0.append(c0)
             rt.append(shape[1])
         elif "relu_out" in mf:
-            rs.append(ctx.store.ensure(mf["relu_out"], y.shape).ptr)
+            rs.append(ctx.store.ensure(mf["relu_out"], yshape).ptr)
             r0.append(0)
             rt.append(w.shape[0])
         else:
@@ -142,18 +142,21 @@ def _conv_fwd(ctx, op):
         _conv_fwd_group(ctx, fused["group_fwd"])
         return
     x, w, b = _ins(ctx, op)
-    (y,) = _outs(ctx, op)
+    yshape = ctx.graph.tensors[op.outputs[0]].shape
+    # pre-activation elision (dispatcher _Plan._preact_elision): y not stored
+    yp = None if fused and fused.get("no_y") else _outs(ctx, op)[0].ptr
     if fused and "relu_slice" in fused:  # ReLU straight into its slice of the concat output
         name, shape, c0 = fused["relu_slice"]
         cat = ctx.store.ensure(name, shape)
-        _L()("bf_conv2d_fwd_relu_slice", x.ptr, w.ptr, b.ptr, y.ptr, cat.ptr, c0, shape[1],
+        _L()("bf_conv2d_fwd_relu_slice", x.ptr, w.ptr, b.ptr, yp, cat.ptr, c0, shape[1],
              *_geom(x, w, op.attrs), *_ws(ctx), ctx.stream)
         return
     if fused and "relu_out" in fused:  # the following relu_forward runs in this epilogue
-        yr = ctx.store.ensure(fused["relu_out"], y.shape)
-        _L()("bf_conv2d_fwd_relu", x.ptr, w.ptr, b.ptr, y.ptr, yr.ptr, *_geom(x, w, op.attrs),
+        yr = ctx.store.ensure(fused["relu_out"], yshape)
+        _L()("bf_conv2d_fwd_relu", x.ptr, w.ptr, b.ptr, yp, yr.ptr, *_geom(x, w, op.attrs),
              *_ws(ctx), ctx.stream)
         return
+    (y,) = _outs(ctx, op)
     _L()("bf_conv2d_fwd", x.ptr, w.ptr, b.ptr, y.ptr, *_geom(x, w, op.attrs), *_ws(ctx), ctx.stream)
 
 
@@ -251,25 +254,36 @@ def _relu_fwd(ctx, op):
     _L()("bf_relu_fwd", x.ptr, y.ptr, x.numel, ctx.stream)
 
 
+def _relu_mask(ctx, op, fused):
+    """(pointer, c0, ctot) of the relu_backward's mask: the pre-activation x,
+    or -- pre-activation elision -- the ReLU output's channel slice of the
+    concat output (relu(a) > 0 <=> a > 0)."""
+    c = ctx.graph.tensors[op.inputs[0]].shape[1]
+    if "x_slice" in fused:
+        name, c0, ctot = fused["x_slice"]
+        return ctx.store.get(name).ptr, c0, ctot
+    return ctx.store.get(ctx.graph.tensors[op.inputs[0]].name).ptr, 0, c
+
+
 def _relu_bwd(ctx, op):
     fused = getattr(ctx, "fused", None)
     if fused and "dy_parts" in fused:  # dy = slice of the (elided) sum of concatenated grads
         names, c0, ctot = fused["dy_parts"]
-        x = ctx.store.get(ctx.graph.tensors[op.inputs[0]].name)
+        xp, xc0, xct = _relu_mask(ctx, op, fused)
         (dx,) = _outs(ctx, op)
         parts = _native.ptr_array([ctx.store.get(nm).ptr for nm in names])
-        n, c = x.shape[0], x.shape[1]
-        _L()("bf_relu_bwd_slice_sum", x.ptr, parts, len(names), c0, ctot, dx.ptr, n, c,
-             x.numel // (n * c), ctx.stream)
+        n, c = dx.shape[0], dx.shape[1]
+        _L()("bf_relu_bwd_slice_sum_x", xp, xc0, xct, parts, len(names), c0, ctot, dx.ptr, n, c,
+             dx.numel // (n * c), ctx.stream)
         return
     if fused and "dy_slice" in fused:  # dy = a channel slice of the concatenated gradient
         name, c0, ctot = fused["dy_slice"]
-        x = ctx.store.get(ctx.graph.tensors[op.inputs[0]].name)
+        xp, xc0, xct = _relu_mask(ctx, op, fused)
         (dx,) = _outs(ctx, op)
         cat = ctx.store.get(name)
-        n, c = x.shape[0], x.shape[1]
-        _L()("bf_relu_bwd_slice", x.ptr, cat.ptr, c0, ctot, dx.ptr, n, c, x.numel // (n * c),
-             ctx.stream)
+        n, c = dx.shape[0], dx.shape[1]
+        _L()("bf_relu_bwd_slice_x", xp, xc0, xct, cat.ptr, c0, ctot, dx.ptr, n, c,
+             dx.numel // (n * c), ctx.stream)
         return
     x, dy = _ins(ctx, op)
     (dx,) = _outs(ctx, op)

@@ -46,33 +46,42 @@ def dp_exchange_ref(ins, attrs):
             for w, g in zip(ws, gs)]
 
 
-def teacher_force(graph, read, materialised, reference, on_output, skip=()):
+def teacher_force(graph, read, materialised, reference, on_output, skip=(), mask_of=None):
     """Walk ``graph`` in serial order.  ``read(name)`` -> GPU array,
     ``materialised(name)`` -> whether the GPU wrote it, ``reference(kind,
     inputs, attrs)`` -> list of arrays, ``on_output(op, name, got, want,
-    inexact)`` compares one output; ``inexact`` is True when an input was the
-    reference's own value of a tensor the GPU never stored and that value
-    came (directly or through bit-exact kinds) from a floating-point kind
-    (e.g. a ReLU gradient folded into a data-gradient epilogue: bit-exact
-    select, but of a contraction's result).  Returns the number of outputs
+    inexact)`` compares one output; ``inexact`` is false for a bit-exact kind
+    on GPU inputs, else the kind of the floating-point operator the result
+    depends on: the op's own kind, or -- when an input was the reference's
+    own value of a tensor the GPU never stored -- the kind that value came
+    from, directly or through bit-exact kinds (e.g. a ReLU gradient folded
+    into a data-gradient epilogue: bit-exact select, but of a contraction's
+    result; a ReLU output whose pre-activation was never stored: the
+    forward convolution's).  ``mask_of(tensor_id)`` -> the GPU's stand-in for
+    an unstored relu_backward mask (the ReLU output, relu(a) > 0 <=> a > 0:
+    what the GPU's kernel reads) or None.  Returns the number of outputs
     compared."""
     from oracle.serial import serial_order
 
     own: dict[str, np.ndarray] = {}
-    inexact_own: set[str] = set()
+    inexact_own: dict[str, str] = {}  # own value -> kind of the floating-point op it came from
     n = 0
     for oid in serial_order(graph):
         op = graph.operators[oid]
         if op.kind in skip or op.kind in ("swap", "copy"):
             continue
-        ins, inexact = [], op.kind not in BITWISE
-        for t in op.inputs:
+        ins, inexact = [], (op.kind if op.kind not in BITWISE else False)
+        for i, t in enumerate(op.inputs):
             name = graph.tensors[t].name
-            if materialised(name):
+            stand_in = (mask_of(t) if mask_of is not None and op.kind == "relu_backward"
+                        and i == 0 and not materialised(name) else None)
+            if stand_in is not None:
+                ins.append(stand_in)
+            elif materialised(name):
                 ins.append(read(name))
             else:
                 ins.append(own[name])
-                inexact = inexact or name in inexact_own
+                inexact = inexact or inexact_own.get(name, False)
         want = reference(op.kind, ins, dict(op.attrs))
         for t, w in zip(op.outputs, want):
             name = graph.tensors[t].name
@@ -82,7 +91,7 @@ def teacher_force(graph, read, materialised, reference, on_output, skip=()):
             else:
                 own[name] = w
                 if inexact:
-                    inexact_own.add(name)
+                    inexact_own[name] = inexact
     return n
 
 

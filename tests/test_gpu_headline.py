@@ -16,6 +16,7 @@ Both write a per-kind error table to $PURINE_B200_PARITY_OUT (if set).
 """
 
 import os
+from types import SimpleNamespace
 
 import numpy as np
 import pytest
@@ -93,6 +94,22 @@ def test_captured_googlenet_step_batch32_matches_oracle():
         if op.kind in BITWISE and not inexact:
             tally.exact(op, name, got, want)
             return
+        if op.kind in BITWISE and inexact in FORWARD:
+            # a bit-exact kind over a forward contraction's own value (the
+            # conv pre-activation is elided: the ReLU output carries the
+            # convolution's error) -- held to the forward contractions' bound
+            shim = SimpleNamespace(kind=f"{op.kind} (of {inexact})", name=op.name)
+            tally.close(shim, name, got, want)
+            pid = g.producer_of(op.inputs[0])
+            pk = g.operators[pid] if pid is not None else None
+            if (op.kind == "relu_forward" and pk is not None and pk.kind in FORWARD
+                    and all(materialised(g.tensors[t].name) for t in pk.inputs)):
+                ref64 = np.maximum(_fp64_contraction(
+                    pk.kind, [read(g.tensors[t].name) for t in pk.inputs], dict(pk.attrs))[0], 0.0)
+                cshim = SimpleNamespace(kind=pk.kind, name=pk.name)
+                orc64.close(cshim, name, want, ref64)
+                gpu64.close(cshim, name, got, ref64)
+            return
         tally.close(op, name, got, want)
         if op.kind in CONTRACTIONS:  # both float32 results against float64
             kind, ins, attrs = last["call"]
@@ -101,11 +118,28 @@ def test_captured_googlenet_step_batch32_matches_oracle():
             orc64.close(op, name, want, ref64[name])
             gpu64.close(op, name, got, ref64[name])
 
-    n = teacher_force(g, read, materialised, reference_keep, on_output)
+    def mask_of(t):
+        # the ReLU output a relu_backward kernel reads when the pre-activation
+        # is elided: the ReLU's own tensor or its slice of the concat output
+        for c, _ in g.consumers_of(t):
+            if g.operators[c].kind != "relu_forward":
+                continue
+            r = g.tensors[g.operators[c].outputs[0]].name
+            if materialised(r):
+                return read(r)
+            f = plan.fusion.get(g.producer_of(t), {})
+            if "relu_slice" in f:
+                name, shape, c0 = f["relu_slice"]
+                return read(name)[:, c0:c0 + g.tensors[t].shape[1]]
+        return None
+
+    n = teacher_force(g, read, materialised, reference_keep, on_output, mask_of=mask_of)
     _report(tally, "GoogLeNet batch 32, captured step: GPU vs CPU oracle (teacher-forced)")
     _report(orc64, "GoogLeNet batch 32: CPU oracle (float32) vs float64, same inputs")
     _report(gpu64, "GoogLeNet batch 32: GPU vs float64, same inputs")
-    assert n > 400
+    # (the conv pre-activations are elided -- dispatcher _preact_elision -- so
+    # each fused conv+ReLU is compared through its ReLU output)
+    assert n > 350
     _assert_ns(tally)
     _assert_forward_bound(gpu64)
 
@@ -120,9 +154,14 @@ FORWARD_SCALED_BOUND = 2.5e-5
 
 def _assert_ns(tally):
     """Every bit-exact kind bit for bit; every other kind except the forward
-    contractions inside the unscaled NS bound rel 1e-4 / abs 1e-5."""
-    bad = tally.fails_except(FORWARD)
+    contractions (and bit-exact kinds over their elided outputs) inside the
+    unscaled NS bound rel 1e-4 / abs 1e-5; those within the scaled bound."""
+    fwd = [k for k in tally.rows if k in FORWARD or any(k.endswith(f"(of {f})") for f in FORWARD)]
+    bad = tally.fails_except(fwd)
     assert not bad, "\n".join(bad[:20])
+    for k in fwd:
+        if k not in FORWARD:
+            assert tally.rows[k][2] <= FORWARD_SCALED_BOUND, (k, tally.rows[k])
 
 
 def _assert_forward_bound(t64):
@@ -170,6 +209,13 @@ def _fp64_contraction(kind, ins, attrs):
     raise AssertionError(kind)
 
 
+def _relu_out(g, t, read):
+    for c, _ in g.consumers_of(t):
+        if g.operators[c].kind == "relu_forward":
+            return read(g.tensors[g.operators[c].outputs[0]].name)
+    raise AssertionError(f"no ReLU output for the elided {g.tensors[t].name}")
+
+
 def test_captured_googlenet_step_batch128_contractions_vs_fp64():
     seq, g, plan, read, materialised = _captured_step(128, cache_reads=False)
     tally = Tally()
@@ -192,10 +238,17 @@ def test_captured_googlenet_step_batch128_contractions_vs_fp64():
                 else:
                     own[name] = w
         elif op.kind == "relu_backward" and names_in[1] in own and materialised(names_out[0]):
-            # a data gradient with relu_backward folded into its epilogue
-            x = read(names_in[0])
+            # a data gradient with relu_backward folded into its epilogue; its
+            # mask is the pre-activation or, that one elided, the ReLU output
+            x = read(names_in[0]) if materialised(names_in[0]) else _relu_out(g, op.inputs[0], read)
             want = np.where(x > 0, own.pop(names_in[1]), 0.0)
             tally.close(op, names_out[0], read(names_out[0]), want)
+            checked += 1
+        elif op.kind == "relu_forward" and names_in[0] in own and materialised(names_out[0]):
+            # a forward convolution whose pre-activation is elided: its ReLU output
+            pk = g.operators[g.producer_of(op.inputs[0])]
+            tally.close(SimpleNamespace(kind=pk.kind, name=pk.name), names_out[0],
+                        read(names_out[0]), np.maximum(own.pop(names_in[0]), 0.0))
             checked += 1
     _report(tally, "GoogLeNet batch 128, captured step: contractions vs float64 "
                    "(teacher-forced)")

@@ -51,6 +51,8 @@ CONV_CASES = [
     (2, 8, 32, 32, 256, 3, 1, 1, False),          # TMA-streamed dY wgrad, two dY tiles
     (3, 4, 32, 32, 16, 5, 2, 2, True),            # transposed wgrad (gemm_wgrad_t.cu), Q = 16
     (2, 3, 36, 36, 64, 7, 2, 3, True),            # conv1 geometry small: Q = 18, 2 q-blocks
+    (2, 3, 300, 300, 32, 7, 2, 3, True),          # window forward (gemm_fwd_win.cu): 2 tiles per row
+    (2, 3, 20, 24, 48, 3, 1, 1, False),           # window forward, stride 1, K = 48
 ]
 
 
@@ -362,6 +364,7 @@ def test_conv1x1_group_forward(couts, shape, monkeypatch):
         return g
 
     outs = {}
+    monkeypatch.setenv("PURINE_B200_PREACT_ELISION", "0")  # y0.. are compared too
     for flag in ("1", "0"):
         monkeypatch.setenv("PURINE_B200_GROUP_1X1", flag)
         g = graph()
