@@ -76,11 +76,12 @@ extern int g_gemm_engine;  // 0 auto, 1 simt, 2 tcgen05 v1 only, 3 auto + halo e
 inline bool tc2_tma_wgrad_enabled() { return g_gemm_engine != 5; }
 // engine v2's gathers staged AD k-blocks ahead through cp.async unless engine 6
 inline bool tc2_async_gather_enabled() { return g_gemm_engine != 6; }
-// engine 7 (opt-in): weight gradients over 16-aligned pixel rows stream the
-// raw dY by TMA (mode kWgradTma, no dY pack).  Measured neutral in the
-// GoogLeNet step (9700 img/s either way) and 5% slower for conv1 alone: the
-// producers, already issue-bound on the gather, also split the B tile
-inline bool tc2_wgrad_tma_enabled() { return g_gemm_engine == 7; }
+// weight gradients whose output rows are 16-byte multiples stream the raw dY
+// by TMA (mode kWgradTma: no dY pack; the epilogue warps split the B tile).
+// Default on (PURINE_B200_WGRAD_TMA=0 disables); off with engines 4-6.
+// (Round 1's form, with the issue-bound producers splitting the B tile, was
+// neutral in the step and 5% slower alone.)
+bool tc2_wgrad_tma_enabled();
 // weight-gradient units split-major (PURINE_B200_SPLIT_OUTER, default 1)
 bool tc2_split_outer();
 // widest tile given a separate small-term accumulator (PURINE_B200_SACC=0: none;

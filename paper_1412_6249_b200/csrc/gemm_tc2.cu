@@ -54,6 +54,16 @@ bool balance_splits_enabled() {
   return !(e && *e && atoi(e) == 0);
 }
 
+bool tc2_wgrad_tma_enabled() {
+  if (g_gemm_engine != 0 && g_gemm_engine != 3 && g_gemm_engine != 7) return false;
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PURINE_B200_WGRAD_TMA");
+    on = (e && *e && atoi(e) == 0) ? 0 : 1;
+  }
+  return on != 0;
+}
+
 bool tc2_split_outer() {
   const char* e = getenv("PURINE_B200_SPLIT_OUTER");
   return !(e && *e && atoi(e) == 0);
@@ -331,7 +341,10 @@ struct Work {
   int sacc;   // 1: separate small-term accumulator in columns [BN, 2BN) of each buffer
   int Pp, Qp;  // weight-gradient fast path: padded pixel grid of the K ordering
   int sstride;  // bytes between ring stages (B tile [+ raw A tile in kTma1x1])
-  int cpi;      // kTma1x1: 32-pixel k-blocks per image
+  int cpi;      // kTma1x1 / kWgradTma: 32-pixel k-blocks per image
+  // kWgradTma: 0 = dY as [N][K][PQ] (unpadded grid, PQ % 32 == 0); 1 = dY as
+  // [N][K][P][Q] with a box of Qp/32-row or 32-column pieces of the padded grid
+  int tma4;
   // weight-gradient fast path: x / (Pp*Qp) = (x * per_m) >> per_s, x / Qp likewise
   uint64_t per_m, qp_m;
   int per_s, qp_s;
@@ -568,7 +581,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
   uint64_t* bempty = bfull + kBStagesMax;
   uint64_t* acc_full = bempty + kBStagesMax;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* bsplit = acc_empty + 2;  // kWgradTma: the epilogue warps split the raw B tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bsplit + kBStagesMax);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -586,6 +600,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     for (int s = 0; s < kBStagesMax; ++s) {
       mbar_init(&bfull[s], 1);
       mbar_init(&bempty[s], 1);
+      mbar_init(&bsplit[s], kEpiWarps * 32);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -780,29 +795,6 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       int nk, cmt, cnt_, csp;
       unit_coords(w, u, cmt, cnt_, csp);
       nk = min(w.kbps, w.nkb - csp * w.kbps);
-      // kWgradTma: the B stage holds the raw dY tile (TMA); the producers
-      // write its small part next to it and, for m-tile 0, sum it per row
-      // into the bias partials (as in kTma1x1)
-      const int nb = BN / 32;
-      float bsum[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) bsum[j] = 0.f;
-      auto flush_bias = [&]() {
-        if (MODE == kWgradTma && bias_part != nullptr && cmt == 0) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (j < nb) {
-              float a = bsum[j];
-              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
-              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
-              a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 4));
-              const int row = cnt_ * BN + (t >> 3) + 32 * j;
-              if ((t & 7) == 0 && row < w.N) bias_part[(size_t)row * w.splits + csp] = a;
-              bsum[j] = 0.f;
-            }
-          }
-        }
-      };
       while (true) {
         asm volatile("cp.async.wait_group %0;" ::"n"(AD > 0 ? AD - 1 : 0) : "memory");
         float big[16], small[16];
@@ -819,25 +811,6 @@ __global__ void __launch_bounds__(kAllThreads, 1)
           pstage = 0;
           pphase ^= 1;
         }
-        if constexpr (MODE == kWgradTma) {
-          mbar_wait(&bfull[stage], phase);  // the raw dY tile of this k-block landed
-          uint8_t* sb = tiles + stage * sstride;
-          const float4* braw = reinterpret_cast<const float4*>(sb);
-          float4* bsm = reinterpret_cast<float4*>(sb + BN * 128);
-          const bool do_bias = bias_part != nullptr && cmt == 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            if (j < nb) {
-              const int f = t + kProducers * j;
-              const float4 v = braw[f];
-              const float4 r = tf32_small4(v);
-              bsm[f] = r;
-              if (do_bias)
-                bsum[j] = __fadd_rn(bsum[j], __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
-            }
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t acol = w.abase + stage * 64 + kc0;
         tmem_st16(lane_addr + acol, big);
@@ -846,7 +819,6 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         tc_fence_before();
         mbar_arrive(&full[stage]);
         if (++i >= nk) {
-          flush_bias();
           u += gridDim.x;
           i = 0;
           if (u >= w.units) break;
@@ -997,7 +969,8 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         tc_fence_after();
         const uint32_t dacc = tmem + (uint32_t)(b * w.accs);
         for (int i = 0; i < nk; ++i) {
-          mbar_wait(&bfull[bst], bphase);
+          // kWgradTma: the raw tile landed AND its small half is written
+          mbar_wait(MODE == kWgradTma ? &bsplit[bst] : &bfull[bst], bphase);
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           // descriptor start-address field = smem byte address >> 4 (bits 0-13)
@@ -1076,8 +1049,25 @@ __global__ void __launch_bounds__(kAllThreads, 1)
         for (int i = 0; i < nk; ++i) {
           mbar_wait(&TC2_BRELEASE[bst], bphase ^ 1);
           mbar_arrive_expect_tx(&bfull[bst], (uint32_t)(BN * 128));
-          const int kb = kb0 + i, img = kb / w.cpi, pix = (kb - img * w.cpi) * BK;
-          tma_load_3d(smem_u32(tiles + bst * sstride), &bmap, pix, nt * BN, img, &bfull[bst]);
+          const int kb = kb0 + i, img = kb / w.cpi, j = kb - img * w.cpi;
+          if (w.tma4) {
+            // padded grid Pp x Qp: a k-block is 32 / Qp whole rows (Qp <= 32)
+            // or a 32-column piece of one row; pixels past P / Q read as zero
+            int p0, q0;
+            if (w.Qp <= BK) {
+              p0 = j * (BK / w.Qp);
+              q0 = 0;
+            } else {
+              const int per_row = w.Qp / BK;
+              p0 = j / per_row;
+              q0 = (j - p0 * per_row) * BK;
+            }
+            tma_load_4d(smem_u32(tiles + bst * sstride), &bmap, q0, p0, nt * BN, img,
+                        &bfull[bst]);
+          } else {
+            tma_load_3d(smem_u32(tiles + bst * sstride), &bmap, j * BK, nt * BN, img,
+                        &bfull[bst]);
+          }
           if (++bst == w.nbst) {
             bst = 0;
             bphase ^= 1;
@@ -1133,8 +1123,7 @@ __global__ void __launch_bounds__(kAllThreads, 1)
     const int ew = warp - kMmaWarp - 1;  // 0..kEpiWarps-1
     const int q = warp & 3;
     const int half = kEpiWarps == 8 ? (ew >> 2) : 0;
-    int local = 0;
-    for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) {
+    auto drain = [&](int u, int local) {
       int mt, nt, sp;
       unit_coords(w, u, mt, nt, sp);
       const int b = local % w.nacc;
@@ -1169,6 +1158,114 @@ __global__ void __launch_bounds__(kAllThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[b]);
+    };
+    if constexpr (MODE == kWgradTma) {
+      // The epilogue warps, idle between accumulator drains in a weight
+      // gradient, also turn each raw dY tile (TMA) into the B stage: its
+      // small part next to it (the raw tile is the big part: the tensor core
+      // drops the low 13 bits itself) and, for m-tile 0, its per-row sums into
+      // the bias partials -- no dY pack pass, and none of it on the issue-bound
+      // im2col producers.  Drains interleave with the splits: before blocking
+      // on a tile whose TMA waits for the MMA to free its stage, a unit whose
+      // k-blocks are all split is drained as soon as its accumulator is ready
+      // (the MMA may be waiting for that buffer).
+      static_assert(MODE != kWgradTma || kEpiWarps == 8,
+                    "the B split maps 256 epilogue threads onto the tile");
+      const int te = threadIdx.x - (kMmaWarp + 1) * 32;  // 0..255
+      const int nb = BN / 32;
+      int su = blockIdx.x, si = 0, s_nk = 0, s_mt = 0, s_nt = 0, s_sp = 0;
+      auto load_unit = [&]() {
+        if (su < w.units) {
+          unit_coords(w, su, s_mt, s_nt, s_sp);
+          s_nk = min(w.kbps, w.nkb - s_sp * w.kbps);
+        }
+      };
+      load_unit();
+      int bst = 0, du = blockIdx.x, dlocal = 0, split_done = 0;
+      uint32_t bphase = 0;
+      float bsum[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bsum[j] = 0.f;
+      while (su < w.units || du < w.units) {
+        if (du < w.units && dlocal < split_done) {
+          bool ready = su >= w.units;
+          if (!ready) {
+            uint32_t ok = 0;
+            const int b = dlocal % w.nacc;
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;"
+                "\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+                : "=r"(ok)
+                : "r"(smem_u32(&acc_full[b])), "r"((uint32_t)((dlocal / w.nacc) & 1))
+                : "memory");
+            ready = __shfl_sync(0xffffffffu, ok, 0) != 0;
+          }
+          if (ready) {
+            drain(du, dlocal);
+            du += gridDim.x;
+            ++dlocal;
+            continue;
+          }
+        }
+        if (su >= w.units) continue;
+        {
+          uint32_t ok = 0;
+          asm volatile(
+              "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;"
+              "\n\tselp.u32 %0, 1, 0, P1;\n\t}"
+              : "=r"(ok)
+              : "r"(smem_u32(&bfull[bst])), "r"(bphase)
+              : "memory");
+          if (__shfl_sync(0xffffffffu, ok, 0) == 0) continue;  // timed out: poll the drain
+        }
+        mbar_wait(&bfull[bst], bphase);  // complete: acquire for every lane
+        {
+          uint8_t* sb = tiles + bst * sstride;
+          const float4* braw = reinterpret_cast<const float4*>(sb);
+          float4* bsm = reinterpret_cast<float4*>(sb + BN * 128);
+          const bool do_bias = bias_part != nullptr && s_mt == 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (j < nb) {
+              const int f = te + kEpiWarps * 32 * j;
+              const float4 v = braw[f];
+              bsm[f] = tf32_small4(v);
+              if (do_bias)
+                bsum[j] = __fadd_rn(bsum[j], __fadd_rn(__fadd_rn(v.x, v.y), __fadd_rn(v.z, v.w)));
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&bsplit[bst]);
+        }
+        if (++bst == w.nbst) {
+          bst = 0;
+          bphase ^= 1;
+        }
+        if (++si >= s_nk) {
+          if (bias_part != nullptr && s_mt == 0) {
+            // 16-byte chunk f of the tile is row f / 8: lanes te^1, te^2, te^4 share a row
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (j < nb) {
+                float a = bsum[j];
+                a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
+                a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
+                a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 4));
+                const int row = s_nt * BN + (te >> 3) + 32 * j;
+                if ((te & 7) == 0 && row < w.N) bias_part[(size_t)row * w.splits + s_sp] = a;
+                bsum[j] = 0.f;
+              }
+            }
+          }
+          ++split_done;
+          su += gridDim.x;
+          si = 0;
+          load_unit();
+        }
+      }
+    } else {
+      int local = 0;
+      for (int u = blockIdx.x; u < w.units; u += gridDim.x, ++local) drain(u, local);
     }
   }
   tc_fence_before();
@@ -1263,7 +1360,7 @@ int launch(const LA& la, const LB& lb, const LBP& lbp, int M, int N, int K, cons
   w.split_outer = std::is_same_v<LBP, LdWgradDYPad> && tc2_split_outer();
 
   const int smem_cap = 227 * 1024;
-  const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
+  const int tail = 1024 + (2 * STAGES + 3 * kBStagesMax + 4) * 8 + 64;
   w.full_ktab = (mode == kChannel || (mode == kGeneric && K <= kKtabMax)) ? 1 : 0;
   const int ktab_bytes = (w.full_ktab ? w.nkb * BK : STAGES * BK) * 8;  // as the kernel carves it
   // async-staged gather depth: 4 k-blocks (64 KB of staging) when that still
@@ -1333,25 +1430,37 @@ inline int pick_bn_tma(int N, int& ntiles) {  // <= 192: >= 3 ring stages of 64 
   return (per + 31) / 32 * 32;
 }
 
-// weight gradient, mode kWgradTma (conv1: 3x224x224 -> 64 x 112x112, 7x7/2):
-// M = C*R*S rows gathered from x (kWgrad16 + cp.async staging), B = the raw
-// dY tile streamed by TMA -- no dY pack pass (which read dY and wrote twice
-// its size) and half the B bytes in the GEMM.  Needs Q % 16 == 0 (the
-// pixel-row K order has no padding) and P*Q % 32 == 0 (k-blocks stay inside
-// one image).
+// weight gradient, mode kWgradTma (default for the 3x3 / 5x5 layers whose
+// output rows are a 16-byte multiple: GoogLeNet conv2/3x3, inception 3a / 3b):
+// M = C*R*S rows gathered from x (kWgrad16 + cp.async staging) over the padded
+// pixel grid Pp x Qp, B = the raw dY tile streamed by TMA -- a 4-D box of
+// 32 / Qp whole rows or a 32-column piece of one row, zero past P / Q -- and
+// split by the epilogue warps.  No dY pack pass (which read dY and wrote
+// twice its size: 0.53 ms of the step) and half the B bytes in the GEMM.
 int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi, float* ws,
                      int64_t ws_bytes, cudaStream_t st, const char* what, float* bias_out) {
   const ConvShape& g = la.g;
   const int PQ = g.P * g.Q, imgs = g.N, Kout = g.K;
-  if (g.Q % 16 || PQ % 32 || (reinterpret_cast<uintptr_t>(dy) & 15)) return -1;
+  const WgradGeom wg = wgrad_geom(g);
+  // measured per layer (conv_bench, batch 128, incl. the pack it replaces):
+  // 56-wide rows 0.655 -> 0.620 ms (conv2/3x3), 28-wide rows 5-10% slower
+  // (inception 3a / 3b: partial 32-column boxes, and the split step adds to
+  // each stage's latency in a 3-stage ring) -- so rows >= 48 only, unless
+  // engine 7 asks for every eligible shape (tests)
+  if (g.Q < 48 && g_gemm_engine != 7) return -1;
+  if (wg.Qp < 16 || (wg.Pp * wg.Qp) % BK || (reinterpret_cast<uintptr_t>(dy) & 15)) return -1;
+  const bool flat = wg.Qp == g.Q && wg.Pp == g.P && PQ % BK == 0;
+  // a row-box map needs 16-byte row strides and whole 32-pixel pieces per row
+  if (!flat && (g.Q % 4 || !(wg.Qp <= BK || wg.Qp % BK == 0))) return -1;
   Work w{};
   w.M = M;
   w.N = Kout;
-  w.cpi = PQ / BK;
+  w.cpi = wg.Pp * wg.Qp / BK;
   w.nkb = imgs * w.cpi;
   w.K = w.nkb * BK;
-  w.Pp = g.P;
-  w.Qp = g.Q;
+  w.Pp = wg.Pp;
+  w.Qp = wg.Qp;
+  w.tma4 = flat ? 0 : 1;
   divmagic((uint32_t)(w.Pp * w.Qp), w.per_m, w.per_s);
   divmagic((uint32_t)w.Qp, w.qp_m, w.qp_s);
   w.BN = pick_bn_tma(Kout, w.ntiles);
@@ -1360,7 +1469,21 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
   w.sstride = 2 * w.BN * 128;
   w.full_ktab = 0;
   CUtensorMap bmap;
-  if (!make_nchw_map(&bmap, dy, PQ, Kout, imgs, w.BN, CU_TENSOR_MAP_SWIZZLE_128B)) return -1;
+  if (flat) {
+    if (!make_nchw_map(&bmap, dy, PQ, Kout, imgs, w.BN, CU_TENSOR_MAP_SWIZZLE_128B)) return -1;
+  } else {
+    auto fn = tma_encode_fn();
+    if (!fn) return -1;
+    const int bx = wg.Qp <= BK ? wg.Qp : BK, by = wg.Qp <= BK ? BK / wg.Qp : 1;
+    cuuint64_t dims[4] = {(cuuint64_t)g.Q, (cuuint64_t)g.P, (cuuint64_t)Kout, (cuuint64_t)imgs};
+    cuuint64_t strides[3] = {(cuuint64_t)g.Q * 4, (cuuint64_t)PQ * 4, (cuuint64_t)Kout * PQ * 4};
+    cuuint32_t box[4] = {(cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)w.BN, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (fn(&bmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(dy), dims, strides, box,
+           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -1;
+  }
   // workspace: [bias partials: Kout x <= kMaxSplits splits][split-K partials]
   const int64_t bias_bytes = bias_out ? ((int64_t)Kout * kMaxSplits * 4 + 1023) / 1024 * 1024 : 0;
   if (!ws || ws_bytes < bias_bytes) return -1;
@@ -1387,7 +1510,7 @@ int launch_wgrad_tma(const LdWgradX& la, const float* dy, int M, const EpiT& epi
   w.split_outer = tc2_split_outer();
   constexpr int AD = 4;
   const int smem_cap = 227 * 1024;
-  const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
+  const int tail = 1024 + (2 * STAGES + 3 * kBStagesMax + 4) * 8 + 64;
   const int ktab_bytes = STAGES * BK * 8;
   const int stg_bytes = AD * 16 * kProducers * 4;
   w.nbst = std::min(kBStagesMax, (smem_cap - tail - ktab_bytes - stg_bytes) / w.sstride);
@@ -1462,7 +1585,7 @@ int launch_tma1x1(const LdWgradX& la, const float* x, const float* dy, int C, in
   w.units = w.mtiles * w.ntiles * w.splits;
   w.split_outer = tc2_split_outer();
   const int smem_cap = 227 * 1024;
-  const int tail = 1024 + (2 * STAGES + 2 * kBStagesMax + 4) * 8 + 64;
+  const int tail = 1024 + (2 * STAGES + 3 * kBStagesMax + 4) * 8 + 64;
   const int ktab_bytes = STAGES * BK * 8;
   w.nbst = std::min(kBStagesMax, (smem_cap - tail - ktab_bytes) / w.sstride);
   if (TC2_ONE_COMMIT) w.nst = w.nbst = std::min(w.nst, w.nbst);
@@ -1516,7 +1639,7 @@ int tc2_conv_wgrad(const LdWgradX& la, const LdWgradDY& lb, int M, int N, int K,
     }
     if (rc > 0) return rc;
   }
-  if (tc2_wgrad_tma_enabled() && g.Q % 16 == 0 && (g.P * g.Q) % 32 == 0) {
+  if (tc2_wgrad_tma_enabled()) {
     const int rc = tc2::launch_wgrad_tma(la, lb.dy, M, epi, ws, ws_bytes, st, what, db);
     if (rc == 0) {
       if (db_done) *db_done = db != nullptr;
