@@ -81,7 +81,17 @@ struct Geo {
   int win_floats;       // staged floats per window (16-byte multiple)
   int kimg;             // bytes of one k-block's B image: [big K rows | small K rows] x 128B
   int abase;            // first TMEM column of the A ring (after 2 x 2K accumulator columns)
+  uint64_t pi_m, nq_m;  // multiply-shift constants: x / (P*nqt), x / nqt
+  int pi_s, nq_s;
 };
+
+// m = ceil(2^(31+l) / d), l = ceil(log2 d): exact x / d for every x < 2^31
+inline void fwin_divmagic(uint32_t d, uint64_t& m, int& s) {
+  int l = 0;
+  while ((1ull << l) < d) ++l;
+  s = 31 + l;
+  m = ((1ull << s) + d - 1) / d;
+}
 
 
 // B operand column k = 8*(c*R + r) + s: w[n][c][r][s] for s < S, else 0
@@ -154,11 +164,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // tile u -> (image, output row, 128-pixel block): multiply-shift divisions
+  // (exact for u < 2^31; the host checks), no integer-division sequences
   auto tile_coords = [&](int u, int& img, int& p, int& q0) {
     const int per_img = g.P * g.nqt;
-    img = u / per_img;
+    img = (int)(((uint64_t)(uint32_t)u * g.pi_m) >> g.pi_s);
     const int rem = u - img * per_img;
-    p = rem / g.nqt;
+    p = (int)(((uint64_t)(uint32_t)rem * g.nq_m) >> g.nq_s);
     q0 = (rem - p * g.nqt) * BM;
   };
 
@@ -407,6 +419,8 @@ int fwd_win_conv(const ConvShape& g, const float* x, const float* w, const EpiNC
   const int64_t tiles = (int64_t)g.N * g.P * q.nqt;
   if (tiles > (1LL << 30)) return -1;
   q.tiles = (int)tiles;
+  fwin_divmagic((uint32_t)(q.P * q.nqt), q.pi_m, q.pi_s);
+  fwin_divmagic((uint32_t)q.nqt, q.nq_m, q.nq_s);
   q.win_floats = (3 + g.stride * (BM - 1) + g.S + 3) / 4 * 4;
   q.kimg = 2 * g.K * 128;
   q.abase = (2 * kAccMul * g.K + 63) / 64 * 64;

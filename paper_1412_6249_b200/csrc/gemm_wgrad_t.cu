@@ -42,8 +42,13 @@ namespace wgt {
 using namespace tcu;
 
 constexpr int BK = 32;
-constexpr int kStages = 3;    // B (smem) and A (TMEM) stages, consumed together per k-block
-constexpr int kRawStages = 6; // raw dY tiles (smem), TMA'd this far ahead of the MMA
+#ifndef WGT_SACC
+#define WGT_SACC 1
+#endif
+// with the separate small-term accumulator the accumulator takes 2*NP TMEM
+// columns and three A stages fit; without it NP columns and four
+constexpr int kStages = WGT_SACC ? 3 : 4;     // B (smem) and A (TMEM) stages, per k-block
+constexpr int kRawStages = WGT_SACC ? 6 : 4;  // raw dY tiles (smem), TMA'd ahead of the MMA
 // warps: 0 TMA, 1 MMA (+ TMEM allocation), 4-5 split (TMEM lane quarters 0-1 =
 // kout rows 0-63), 2-3 and 6-13 producers (10), 14-17 epilogue (all four lane
 // quarters)
@@ -68,6 +73,16 @@ struct Geo {
   int abase;            // first TMEM column of the A ring (after the 2*NP accumulator columns)
 };
 
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_v4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                "r"(ok ? 16 : 0)
@@ -151,11 +166,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < g.splits; u += gridDim.x) {
         const int kb0 = u * g.kbps, nk = min(g.kbps, g.nkb - kb0);
+        int img, p, q0;
+        kb_coords(kb0, img, p, q0);  // then advanced incrementally
         for (int i = 0; i < nk; ++i) {
           mbar_wait(&raw_free[s], ph ^ 1);
           mbar_arrive_expect_tx(&raw_full[s], (uint32_t)(g.K * 128));
-          int img, p, q0;
-          kb_coords(kb0 + i, img, p, q0);
+          if (i > 0 && (q0 += BK) == g.nq * BK) {
+            q0 = 0;
+            if (++p == g.P) {
+              p = 0;
+              ++img;
+            }
+          }
           asm volatile(
               "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
               " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(rawbuf + s * kRawBytes)),
@@ -235,20 +257,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t bb = sw128_desc(st), bs = sw128_desc(st + NP * 128);
         const uint32_t ab = tmem + (uint32_t)(g.abase + s * 64), as = ab + 32;
         if (elect_one()) {
-          if (i == 0) {
-            mma_ts_flag<0>(dbig, ab, bb, idesc);
-            mma_ts_flag<0>(dsm, ab, bs, idesc);
-          } else {
-            mma_ts_flag<1>(dbig, ab, bb, idesc);
-            mma_ts_flag<1>(dsm, ab, bs, idesc);
-          }
-          mma_ts_flag<1>(dsm, as, bb, idesc);
+          if (WGT_SACC) {
+            if (i == 0) {
+              mma_ts_flag<0>(dbig, ab, bb, idesc);
+              mma_ts_flag<0>(dsm, ab, bs, idesc);
+            } else {
+              mma_ts_flag<1>(dbig, ab, bb, idesc);
+              mma_ts_flag<1>(dsm, ab, bs, idesc);
+            }
+            mma_ts_flag<1>(dsm, as, bb, idesc);
 #pragma unroll
-          for (int ks = 1; ks < BK / 8; ++ks) {
-            const uint64_t k2 = (uint64_t)((ks * 32) >> 4);
-            mma_ts_flag<1>(dbig, ab + ks * 8, bb + k2, idesc);
-            mma_ts_flag<1>(dsm, ab + ks * 8, bs + k2, idesc);
-            mma_ts_flag<1>(dsm, as + ks * 8, bb + k2, idesc);
+            for (int ks = 1; ks < BK / 8; ++ks) {
+              const uint64_t k2 = (uint64_t)((ks * 32) >> 4);
+              mma_ts_flag<1>(dbig, ab + ks * 8, bb + k2, idesc);
+              mma_ts_flag<1>(dsm, ab + ks * 8, bs + k2, idesc);
+              mma_ts_flag<1>(dsm, as + ks * 8, bb + k2, idesc);
+            }
+          } else {  // all three products into one accumulator (small terms first)
+            if (i == 0)
+              mma_ts_flag<0>(dbig, as, bb, idesc);
+            else
+              mma_ts_flag<1>(dbig, as, bb, idesc);
+            mma_ts_flag<1>(dbig, ab, bs, idesc);
+            mma_ts_flag<1>(dbig, ab, bb, idesc);
+#pragma unroll
+            for (int ks = 1; ks < BK / 8; ++ks) {
+              const uint64_t k2 = (uint64_t)((ks * 32) >> 4);
+              mma_ts_flag<1>(dbig, as + ks * 8, bb + k2, idesc);
+              mma_ts_flag<1>(dbig, ab + ks * 8, bs + k2, idesc);
+              mma_ts_flag<1>(dbig, ab + ks * 8, bb + k2, idesc);
+            }
           }
           tc_commit(&empty[s]);
         }
@@ -277,40 +315,60 @@ __global__ void __launch_bounds__(kThreads, 1)
       id_f[nid] = f;
       id_dst[nid] = (cr * wf + 4 * f) * 4;
     }
-    // stage the (c, r) windows of k-block kb into staging slot `slot`
-    auto issue = [&](int kb, int slot) {
-      if (kb >= 0) {
-        int img, p, q0;
-        kb_coords(kb, img, p, q0);
-        const int a0 = (g.st * q0 - g.pad) & ~3;  // 16-byte aligned window start
+    // k-block cursors over this CTA's sequence (unit u's kb0 .. kb0+nk-1, then
+    // unit u + gridDim.x's): (img, p, q-block) advance incrementally -- the
+    // per-k-block divisions cost the producers ~100 instructions per k-block
+    struct Cur {
+      int u, i, nk, img, p, qb;
+    };
+    auto cur_init = [&](Cur& c, int u) {
+      c.u = u;
+      c.i = 0;
+      if (u < g.splits) {
+        const int kb0 = u * g.kbps;
+        c.nk = min(g.kbps, g.nkb - kb0);
+        int q0;
+        kb_coords(kb0, c.img, c.p, q0);
+        c.qb = q0 / BK;
+      }
+    };
+    auto cur_next = [&](Cur& c) {
+      if (++c.i >= c.nk) {
+        cur_init(c, c.u + gridDim.x);
+      } else if (++c.qb == g.nq) {
+        c.qb = 0;
+        if (++c.p == g.P) {
+          c.p = 0;
+          ++c.img;
+        }
+      }
+    };
+    // stage the (c, r) windows of the cursor's k-block into staging slot `slot`
+    auto issue = [&](const Cur& c, int slot) {
+      if (c.u < g.splits) {
+        const int a0 = (g.st * c.qb * BK - g.pad) & ~3;  // 16-byte aligned window start
         const uint32_t sbase = stg0 + (uint32_t)(slot * g.CR * wf * 4);
+        const int ih0 = g.st * c.p - g.pad;
+        const float* ximg = x + (int64_t)c.img * g.C * g.H * g.W;
 #pragma unroll
         for (int j = 0; j < kMaxIds; ++j) {
           if (j < nid) {
-            const int ih = g.st * p + id_r[j] - g.pad, iw = a0 + 4 * id_f[j];
+            const int ih = ih0 + id_r[j], iw = a0 + 4 * id_f[j];
             const bool ok = (unsigned)ih < (unsigned)g.H && iw >= 0 && iw < g.W;
-            const float* src =
-                ok ? x + (((int64_t)img * g.C + id_c[j]) * g.H + ih) * g.W + iw : x;
+            const float* src = ok ? ximg + ((int64_t)id_c[j] * g.H + ih) * g.W + iw : x;
             cp_async16(sbase + (uint32_t)id_dst[j], src, ok);
           }
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // the k-blocks this CTA consumes, in order: unit u's kb0 .. kb0+nk-1, then
-    // unit u + gridDim.x's; the cursor walks them kWinSlots-1 ahead of use
-    int cu = blockIdx.x, ci = 0;
-    auto next_kb = [&]() -> int {
-      while (cu < g.splits) {
-        const int kb0 = cu * g.kbps, nk = min(g.kbps, g.nkb - kb0);
-        if (ci < nk) return kb0 + ci++;
-        cu += gridDim.x;
-        ci = 0;
-      }
-      return -1;
-    };
+    Cur ic;  // the issue cursor runs kWinSlots-1 k-blocks ahead of use
+    cur_init(ic, blockIdx.x);
 #pragma unroll 1
-    for (int d = 0; d < kWinSlots - 1; ++d) issue(next_kb(), d);
+    for (int d = 0; d < kWinSlots - 1; ++d) {
+      issue(ic, d);
+      if (ic.u < g.splits) cur_next(ic);
+    }
     // B-image work: thread t writes 16-byte chunk c = t & 7 (pixels 4c..4c+3) of
     // rows n = (t >> 3) + 32 j, n = cr*S + s -- the window offsets and
     // swizzled destinations are fixed for every k-block, so precomputed
@@ -320,37 +378,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c = t & 7;
       for (int n = t >> 3; n < g.CRS && nrow < kMaxRows; n += kProducers / 8, ++nrow) {
         const int cr = n / g.S, ss = n - cr * g.S;
-        row_win[nrow] = cr * wf + ss + g.st * 4 * c;
+        row_win[nrow] = (cr * wf + ss + g.st * 4 * c) * 4;  // bytes
         row_dst[nrow] = (int)sw_off(n, c);
       }
     }
     int s = 0, slot = 0;
     uint32_t ph = 0;
-    for (int u = blockIdx.x; u < g.splits; u += gridDim.x) {
-      const int kb0 = u * g.kbps, nk = min(g.kbps, g.nkb - kb0);
-      for (int i = 0; i < nk; ++i) {
-        const int kb = kb0 + i;
+    Cur mc;
+    cur_init(mc, blockIdx.x);
+    while (mc.u < g.splits) {
+      {
         // this k-block's windows are the oldest of kWinSlots-1 groups in flight;
         // the barrier also retires every thread's reads of the previous k-block,
         // whose slot the next issue refills
         asm volatile("cp.async.wait_group %0;" ::"n"(kWinSlots - 2) : "memory");
         named_sync(1, kProducers);
-        issue(next_kb(), (slot + kWinSlots - 1) % kWinSlots);
-        int img, p, q0;
-        kb_coords(kb, img, p, q0);
+        issue(ic, (slot + kWinSlots - 1) % kWinSlots);
+        if (ic.u < g.splits) cur_next(ic);
+        const int q0 = mc.qb * BK;
         const int o = (g.st * q0 - g.pad) - ((g.st * q0 - g.pad) & ~3);
+        cur_next(mc);
         mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* bbig = base + s * g.stage_bytes;
-        uint8_t* bsml = bbig + NP * 128;
-        const float* win0 = staging + slot * g.CR * wf + o;
-        const int st1 = g.st;
+        // shared-space 32-bit addressing (generic pointers cost 64-bit address
+        // arithmetic and generic loads / stores per element)
+        const uint32_t bbig = smem_u32(base + s * g.stage_bytes), bsml = bbig + NP * 128;
+        const uint32_t win_a = smem_u32(staging) + (uint32_t)((slot * g.CR * wf + o) * 4);
+        const uint32_t st4 = (uint32_t)g.st * 4;
 #pragma unroll
         for (int j = 0; j < kMaxRows; ++j) {
           if (j < nrow) {
-            const float* wp = win0 + row_win[j];
-            const float4 v = make_float4(wp[0], wp[st1], wp[2 * st1], wp[3 * st1]);
-            *reinterpret_cast<float4*>(bbig + row_dst[j]) = v;
-            *reinterpret_cast<float4*>(bsml + row_dst[j]) = tf32_small4(v);
+            const uint32_t a = win_a + (uint32_t)row_win[j];
+            const float4 v = make_float4(lds_f32(a), lds_f32(a + st4), lds_f32(a + 2 * st4),
+                                         lds_f32(a + 3 * st4));
+            sts_v4(bbig + (uint32_t)row_dst[j], v);
+            sts_v4(bsml + (uint32_t)row_dst[j], tf32_small4(v));
           }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -378,10 +439,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c0 = 0; c0 < NP; c0 += 16) {
         uint32_t v[16], sv[16];
         tmem_ld16(taddr + (uint32_t)c0, v);
-        tmem_ld16(taddr + (uint32_t)(NP + c0), sv);
+        if (WGT_SACC) {
+          tmem_ld16(taddr + (uint32_t)(NP + c0), sv);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(sv[j])));
+          for (int j = 0; j < 16; ++j)
+            v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(sv[j])));
+        }
         if (live) part.store16(rp, c0, v, g.CRS - c0);
       }
       tc_fence_before();
@@ -445,7 +508,7 @@ int wgrad_t_conv(const ConvShape& g, const float* x, const float* dy, float* dw,
   q.nch = (3 + g.stride * (BK - 1) + g.S + 3) / 4;
   q.win_floats = q.nch * 4;
   q.stage_bytes = 2 * q.NP * 128;
-  q.abase = (2 * q.NP + 63) / 64 * 64;
+  q.abase = ((WGT_SACC ? 2 : 1) * q.NP + 63) / 64 * 64;
   if (g.K > 64 || q.abase + kStages * 64 > 512 || q.CR * q.nch > 4 * kProducers) return -1;
   const int smem_cap = 227 * 1024;
   const int smem = 1024 + kStages * q.stage_bytes + kRawStages * kRawBytes +
@@ -454,7 +517,7 @@ int wgrad_t_conv(const ConvShape& g, const float* x, const float* dy, float* dw,
   if (smem > smem_cap) return -1;
   // units: chains of at most max_chain_kb() k-blocks, balanced over the grid
   const int sms = gemm_sm_budget();
-  const int64_t chain = std::max<int64_t>(1, chain_min_splits(q.nkb, true));
+  const int64_t chain = std::max<int64_t>(1, chain_min_splits(q.nkb, WGT_SACC != 0));
   const int64_t bias_bytes = db ? ((int64_t)g.K * kMaxSplits * 4 + 1023) / 1024 * 1024 : 0;
   if (!ws || ws_bytes < bias_bytes) return -1;
   const int64_t by_ws = (ws_bytes - bias_bytes) / ((int64_t)g.K * CRS * 4);

@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--net", default="googlenet", choices=["googlenet", "nin"])
     ap.add_argument("--batch", type=int, default=128)
     ap.add_argument("--top", type=int, default=60)
+    ap.add_argument("--tail", type=int, default=25, help="print the chain's last N operators")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     net = (googlenet if a.net == "googlenet" else nin)(batch=a.batch, lr=0.01)
@@ -89,6 +90,17 @@ def main():
         by_kind[op.kind] += (s1 - s0) / 1e6
     for k, v in sorted(by_kind.items(), key=lambda kv: -kv[1]):
         print(f"  {k:26s} {v:7.3f} ms")
+    print(f"\nlast {a.tail} operators of the chain (start ms, device ms, gap us):")
+    for op, s0, s1, gap in chain[-a.tail:]:
+        print(f"  {op.name:34s} {op.kind:24s} {s0 / 1e6:7.3f} {(s1 - s0) / 1e6:7.3f}  gap {gap / 1e3:7.1f}")
+    # what else runs during the chain's last operators
+    t_end = chain[-1][2]
+    t0 = chain[-min(a.tail, len(chain))][1]
+    others = sorted((r for r in iv if r[2] > t0 and r[0].name not in {c[0].name for c in chain}),
+                    key=lambda r: r[1])
+    print(f"\noff-chain operators overlapping the last {(t_end - t0) / 1e6:.3f} ms:")
+    for op, s0, s1 in others[:40]:
+        print(f"  {op.name:34s} {op.kind:24s} {s0 / 1e6:7.3f} {(s1 - s0) / 1e6:7.3f}")
     rows = sorted(chain, key=lambda r: -(r[2] - r[1]))[:a.top]
     print("\nlongest operators on the chain (device ms, idle gap before it us):")
     for op, s0, s1, gap in rows:
