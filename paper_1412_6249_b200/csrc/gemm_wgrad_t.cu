@@ -302,17 +302,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (is_producer(warp)) {
     // ======================= B: the im2col of x =======================
     const int t = (warp < kProdWarp0 ? warp - 2 : warp - kProdWarp0 + 2) * 32 + lane;
-    const uint32_t stg0 = smem_u32(staging);
+    const uint32_t stg0 = smem_u32(staging), base_a = smem_u32(base);
     const int wf = g.win_floats;
     // this thread's window chunks (fixed for every k-block): ids t, t + 256, ...
     // of the CR x nch chunks -> (c, r, f); only the k-block's (img, p, q0) vary
     constexpr int kMaxIds = 4;
-    int id_c[kMaxIds], id_r[kMaxIds], id_f[kMaxIds], id_dst[kMaxIds], nid = 0;
+    // per chunk: its row r and column 4f (bounds), its offset from the
+    // k-block's window origin x[img][0][st*p - pad][a0] and its staging slot
+    int id_r[kMaxIds], id_f4[kMaxIds], id_off[kMaxIds], id_dst[kMaxIds], nid = 0;
     for (int id = t; id < g.CR * g.nch && nid < kMaxIds; id += kProducers, ++nid) {
-      const int cr = id / g.nch, f = id - cr * g.nch;
-      id_c[nid] = cr / g.R;
-      id_r[nid] = cr - id_c[nid] * g.R;
-      id_f[nid] = f;
+      const int cr = id / g.nch, f = id - cr * g.nch, c = cr / g.R;
+      id_r[nid] = cr - c * g.R;
+      id_f4[nid] = 4 * f;
+      id_off[nid] = (c * g.H + id_r[nid]) * g.W + 4 * f;
       id_dst[nid] = (cr * wf + 4 * f) * 4;
     }
     // k-block cursors over this CTA's sequence (unit u's kb0 .. kb0+nk-1, then
@@ -349,14 +351,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int a0 = (g.st * c.qb * BK - g.pad) & ~3;  // 16-byte aligned window start
         const uint32_t sbase = stg0 + (uint32_t)(slot * g.CR * wf * 4);
         const int ih0 = g.st * c.p - g.pad;
-        const float* ximg = x + (int64_t)c.img * g.C * g.H * g.W;
+        const float* xo = x + ((int64_t)c.img * g.C * g.H + ih0) * g.W + a0;
 #pragma unroll
         for (int j = 0; j < kMaxIds; ++j) {
           if (j < nid) {
-            const int ih = ih0 + id_r[j], iw = a0 + 4 * id_f[j];
-            const bool ok = (unsigned)ih < (unsigned)g.H && iw >= 0 && iw < g.W;
-            const float* src = ok ? ximg + ((int64_t)id_c[j] * g.H + ih) * g.W + iw : x;
-            cp_async16(sbase + (uint32_t)id_dst[j], src, ok);
+            const bool ok = (unsigned)(ih0 + id_r[j]) < (unsigned)g.H &&
+                            (unsigned)(a0 + id_f4[j]) < (unsigned)g.W;
+            cp_async16(sbase + (uint32_t)id_dst[j], ok ? xo + id_off[j] : x, ok);
           }
         }
       }
@@ -401,8 +402,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&empty[s], ph ^ 1);
         // shared-space 32-bit addressing (generic pointers cost 64-bit address
         // arithmetic and generic loads / stores per element)
-        const uint32_t bbig = smem_u32(base + s * g.stage_bytes), bsml = bbig + NP * 128;
-        const uint32_t win_a = smem_u32(staging) + (uint32_t)((slot * g.CR * wf + o) * 4);
+        const uint32_t bbig = base_a + (uint32_t)(s * g.stage_bytes), bsml = bbig + NP * 128;
+        const uint32_t win_a = stg0 + (uint32_t)((slot * g.CR * wf + o) * 4);
         const uint32_t st4 = (uint32_t)g.st * 4;
 #pragma unroll
         for (int j = 0; j < kMaxRows; ++j) {
