@@ -38,8 +38,10 @@
 // variants: a per-column offset table with 8 producer warps (0.36 ms, ~10
 // issue slots per value); window staging by a single loader warp (cp.async:
 // 0.69 ms) or by cp.async.bulk per window (0.53 ms) -- their issue is serial;
-// TMA tiled 4-D boxes of the rows faulted (illegal instruction) and were not
-// pursued.
+// TMA tiled 4-D boxes of the rows faulted: a TMA box's innermost start must
+// be a 16-byte multiple (tools/tma4d_probe.cu), the window start st*q0 - pad
+// is not -- an aligned start with the offset applied by the producers would
+// work, but the window staging is not what bounds this kernel.
 #include <stdlib.h>
 
 #include <algorithm>

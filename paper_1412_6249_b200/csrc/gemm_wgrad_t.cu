@@ -78,6 +78,13 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ float4 lds_v4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
 __device__ __forceinline__ void sts_v4(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
@@ -197,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // thread = kout row m = TMEM lane (quarters 0, 1)
     const int m = (warp & 3) * 32 + lane;
     const bool live = m < g.K;
+    const uint32_t raw_a = smem_u32(rawbuf);
     const uint32_t la = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     int rs = 0, s = 0;
     uint32_t rph = 0, ph = 0;
@@ -206,11 +214,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nk; ++i) {
         mbar_wait(&raw_full[rs], rph);
         float big[32], small[32];
-        const uint8_t* row = rawbuf + rs * kRawBytes + m * 128;
+        const uint32_t row = raw_a + (uint32_t)(rs * kRawBytes + m * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (live) v = *reinterpret_cast<const float4*>(row + ((c ^ (m & 7)) << 4));
+          if (live) v = lds_v4(row + (uint32_t)((c ^ (m & 7)) << 4));
           big[4 * c + 0] = v.x; big[4 * c + 1] = v.y; big[4 * c + 2] = v.z; big[4 * c + 3] = v.w;
           const float4 r = tf32_small4(v);
           small[4 * c + 0] = r.x; small[4 * c + 1] = r.y; small[4 * c + 2] = r.z;
