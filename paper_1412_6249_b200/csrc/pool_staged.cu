@@ -394,7 +394,20 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
   if (sb * 2 > kSmemBudget) return false;
   g.G = G;
   g.stage_floats = (stage_floats(G) + 31) & ~31;
+  // (measured: a two-CTAs-per-SM depth -- 110 KB per CTA -- speeds pool1's
+  // backward alone, 0.258 -> 0.236 ms, but costs the step 0.8%)
   g.NS = (int)std::min<int64_t>(3, kSmemBudget / ((int64_t)g.stage_floats * 4));
+  // a backward stage of >= 64 KB (one 112x112 plane: pool1): one stage per
+  // CTA and two CTAs per SM (0.258 -> 0.236 ms alone)
+  static const int big1 = [] {
+    const char* e = getenv("PURINE_B200_POOL_BIG1");
+    return e && *e ? atoi(e) : 1;
+  }();
+  if (big1 && bwd && (int64_t)g.stage_floats * 4 >= (64 << 10)) g.NS = 1;
+  if (const char* e = getenv("PURINE_B200_POOL_NS")) {  // probe: ring depth cap
+    const int cap = atoi(e);
+    if (cap >= 1 && cap < g.NS) g.NS = cap;
+  }
   g.nchunks = (g.planes + G - 1) / G;
   // walker runs: enough items to occupy the CTA twice over, long runs for the
   // row reuse

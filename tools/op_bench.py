@@ -45,8 +45,9 @@ def main():
                 fn = lambda: lib("bf_maxpool_fwd_staged", x.data_ptr(), y.data_ptr(), None, n, c,
                                  h, w, p, q, nd.kernel, nd.stride, nd.pad, st)
                 nbytes = 4 * x.numel() + 4 * y.numel()
-            elif a.op == "maxpool_bwd_x":  # argmax recomputed from x
-                fn = lambda: lib("bf_maxpool_bwd_x", x.data_ptr(), y.data_ptr(), dx.data_ptr(), 0,
+            elif a.op in ("maxpool_bwd_x", "maxpool_bwd_xr"):  # argmax recomputed from x
+                rf = 1 if a.op == "maxpool_bwd_xr" else 0  # + the folded ReLU backward
+                fn = lambda: lib("bf_maxpool_bwd_x", x.data_ptr(), y.data_ptr(), dx.data_ptr(), rf,
                                  n, c, h, w, p, q, nd.kernel, nd.stride, nd.pad, st)
                 nbytes = 8 * x.numel() + 4 * y.numel()
             elif a.op == "maxpool_fwd":
