@@ -17,6 +17,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import functools
+import itertools
+
 import numpy as np
 import torch
 
@@ -85,13 +88,33 @@ class PendingRead:
         return self._host.numpy().reshape(self._shape)
 
 
+@functools.lru_cache(maxsize=65536)
+def _pair_code(a: str, b: str) -> int:
+    """Deterministic 64-bit code of a swapped name pair (the swap signature)."""
+    import hashlib
+
+    return int.from_bytes(hashlib.blake2b(f"{a}\0{b}".encode(), digest_size=8).digest(), "little")
+
+
 class TensorStore:
     """Named device buffers shared by every graph of a run."""
+
+    _serials = itertools.count(1)
 
     def __init__(self, device=None) -> None:
         self.device = torch.device(device) if device is not None else _default_device()
         self._tensors: dict[str, Tensor] = {}
         self._alias_of: dict[str, str] = {}
+        # buffer-binding signature (the dispatcher's replay cache key): a
+        # process-unique store serial, an epoch bumped whenever a name is
+        # (re)bound to memory, and an order-free accumulator of swaps (a swap
+        # graph is an involution: swapping a pair twice restores the value)
+        self._serial = next(TensorStore._serials)
+        self._epoch = 0
+        self._swap_sig = 0
+
+    def binding_sig(self) -> tuple[int, int, int]:
+        return (self._serial, self._epoch, self._swap_sig)
 
     # -- reference API ------------------------------------------------------
 
@@ -123,6 +146,7 @@ class TensorStore:
         if cur is None:
             t = Tensor(shape, src.contiguous().clone())  # the store owns its buffers
             self._tensors[name] = t
+            self._epoch += 1
             return t
         if cur.shape != shape:
             raise KernelError(f"store: shape mismatch writing {name!r}: {shape} vs existing {cur.shape}")
@@ -158,10 +182,13 @@ class TensorStore:
 
     def swap(self, name_a: str, name_b: str) -> None:
         swap(self.get(name_a), self.get(name_b))
+        lo, hi = sorted((name_a, name_b))
+        self._swap_sig ^= _pair_code(lo, hi)
 
     def remove(self, name: str) -> None:
         self._tensors.pop(name, None)
         self._alias_of.pop(name, None)
+        self._epoch += 1
 
     def __contains__(self, name: str) -> bool:
         return name in self._tensors
@@ -198,6 +225,7 @@ class TensorStore:
         if cur is None:
             cur = Tensor(shape, torch.empty(shape, dtype=torch.float32, device=self.device))
             self._tensors[name] = cur
+            self._epoch += 1
         elif cur.shape != shape:
             raise KernelError(f"store: shape mismatch for {name!r}: {shape} vs existing {cur.shape}")
         return cur
@@ -216,6 +244,7 @@ class TensorStore:
                 raise KernelError(f"store: shape mismatch aliasing {name!r}")
             cur.data = view
         self._alias_of[name] = src
+        self._epoch += 1
         return cur
 
     def place(self, name: str, view: torch.Tensor) -> Tensor:
@@ -228,9 +257,11 @@ class TensorStore:
                 raise KernelError(f"store: shape mismatch placing {name!r}")
             view.copy_(cur.data)
             cur.data = view
+            self._epoch += 1
             return cur
         t = Tensor(shape, view)
         self._tensors[name] = t
+        self._epoch += 1
         return t
 
     def is_alias_of(self, name: str, src: str) -> bool:
