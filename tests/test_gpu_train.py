@@ -304,3 +304,45 @@ def test_prefetched_inputs_match_synchronous_feed():
         results.append({p: st.array(f"{p}_p0") for p, _ in net.param_shapes()})
     for p in results[0]:
         assert np.array_equal(results[0][p], results[1][p]), p
+
+
+@pytest.mark.parametrize("momentum", [0.0, 0.9])
+def test_run_replay_cache_is_bitwise_the_walk(monkeypatch, momentum):
+    """run(trace=False) replays a captured CUDA graph from the second call with
+    a buffer binding on (dispatcher._run_replayed); six iterations of a
+    training sequence -- both swap parities walked, captured and replayed, a
+    new batch written into the store before every iteration -- end bit for bit
+    where walking every graph every call ends."""
+    from paper_1412_6249_b200 import run_sequence
+    from paper_1412_6249_b200.exchange import build_rank_sequence
+
+    net = cifar_convnet(batch=4, lr=0.01, momentum=momentum)
+    feed = SyntheticFeed.for_net(net, 13, spread=0.0)
+    out = []
+    for capture in ("0", "1"):
+        monkeypatch.setenv("PURINE_B200_CAPTURE", capture)
+        st = TensorStore("cuda:0")
+        seq, _ = build_rank_sequence(net, 1, 0, st, bucket_bytes=32 << 10)
+        init_params(net, st, 13, seq.layout)
+        xname, lname = seq.layout.data_names[0], seq.layout.label_names[0]
+        loss_name = seq.layout.loss_names[0]
+        losses = []
+
+        def before(it, s):
+            x, y = feed.batch_for(it, 0)
+            s.set(xname, x)
+            s.set(lname, y)
+
+        def after(rep, s):
+            if rep.graph_index == 0:
+                losses.append(float(s.array(loss_name)[0]))
+
+        run_sequence(seq, st, before_iteration=before, after_graph=after, iterations=6,
+                     trace=False)
+        cached = sum(1 for g in seq.graphs for v in g.__dict__.get("_replays", {}).values()
+                     if v[0] is not None)
+        assert cached == (0 if capture == "0" else 2)  # one capture per swap parity
+        out.append((losses, {p: st.array(f"{p}_p0") for p, _ in net.param_shapes()}))
+    assert out[0][0] == out[1][0]
+    for p in out[0][1]:
+        assert np.array_equal(out[0][1][p], out[1][1][p]), p
