@@ -412,7 +412,11 @@ int bf_relu_bwd_slice_sum_x(const float* x, int x_c0, int x_ctot, const float* c
   if (n <= 0) return 0;
   cudaStream_t st = as_stream(s);
   Parts p;
-  bool vec = aligned16(x) && aligned16(dx) && run % 4 == 0 && HW % 4 == 0;
+  // float4 when every image / slice offset is a multiple of 4 elements (the
+  // 7x7 planes of inception 5a/5b qualify through channel counts that are)
+  bool vec = aligned16(x) && aligned16(dx) && run % 4 == 0 && ((int64_t)ctot * HW) % 4 == 0 &&
+             ((int64_t)c0 * HW) % 4 == 0 && ((int64_t)x_ctot * HW) % 4 == 0 &&
+             ((int64_t)x_c0 * HW) % 4 == 0;
   for (int i = 0; i < k; ++i) {
     p.p[i] = parts[i];
     vec = vec && aligned16(parts[i]);
@@ -441,7 +445,9 @@ int bf_relu_bwd_slice_x(const float* x, int x_c0, int x_ctot, const float* dy_ca
   const int64_t run = (int64_t)C * HW, n = run * N;
   if (n <= 0) return 0;
   cudaStream_t st = as_stream(s);
-  if (aligned16(x) && aligned16(dy_cat) && aligned16(dx) && run % 4 == 0 && HW % 4 == 0) {
+  if (aligned16(x) && aligned16(dy_cat) && aligned16(dx) && run % 4 == 0 &&
+      ((int64_t)ctot * HW) % 4 == 0 && ((int64_t)c0 * HW) % 4 == 0 &&
+      ((int64_t)x_ctot * HW) % 4 == 0 && ((int64_t)x_c0 * HW) % 4 == 0) {
     relu_bwd_slice_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
         reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy_cat),
         reinterpret_cast<float4*>(dx), run / 4, (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4,
