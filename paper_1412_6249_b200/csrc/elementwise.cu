@@ -43,6 +43,14 @@ int max_chain_kb() {
   return v;
 }
 
+int chain_plain_mult() {
+  static const int v = [] {
+    const char* e = getenv("PURINE_B200_CHAIN_PLAIN");
+    return e && *e && atoi(e) > 0 ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 int sm_count_current() {
   int dev = 0;
   cudaGetDevice(&dev);

@@ -495,8 +495,9 @@ int max_chain_kb();
 // chain may be three times as long for the same error (precision_probe,
 // K = 401k: 32-k-block chains 1.7e-6 of max |ref| with it vs 6.4e-6 without;
 // 96-k-block chains 5.1e-6)
+int chain_plain_mult();  // PURINE_B200_CHAIN_PLAIN: chain multiplier without the small accumulator
 inline int64_t chain_min_splits(int64_t nkb, bool sacc = false) {
-  const int c = max_chain_kb() * (sacc ? 3 : 1);
+  const int c = max_chain_kb() * (sacc ? 3 : chain_plain_mult());
   return c > 0 ? (nkb + c - 1) / c : 1;
 }
 
