@@ -1004,6 +1004,7 @@ def _enqueue(graph, store, registry, cap, ctx, trace, base):
 
 
 CAPTURE_ENV = "PURINE_B200_CAPTURE"  # "0": run() walks the graph every call
+_REPLAY_CACHE_MAX = 8  # bindings remembered per graph (a training sequence uses two)
 
 
 def _replayable(graph, store, registry, trace, transport, copy_latency_s) -> bool:
@@ -1031,10 +1032,13 @@ def _run_replayed(graph, store, registry, cap, ctx) -> list[str]:
     cache = graph.__dict__.setdefault("_replays", {})
     ent = cache.get(key)
     if ent is not None and ent[0] is not None:
+        cache[key] = cache.pop(key)  # most recently used last
         ent[0].replay()
         return ent[1]
     if ent is None:
         names, _ = _enqueue(graph, store, registry, cap, ctx, False, None)
+        while len(cache) >= _REPLAY_CACHE_MAX:  # bindings that never recur: evict the oldest
+            cache.pop(next(iter(cache)))
         cache[key] = (None, names)
         return names
     pool = getattr(store, "_replay_pool", None)
