@@ -202,3 +202,62 @@ class CapturedSequence:
                 self._flag_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
             self._flag_host.copy_(self.store.finite_flag(), non_blocking=True)
         self.parity ^= 1
+
+
+class PrefetchFeed:
+    """A ``run_sequence`` ``before_iteration`` hook that overlaps each
+    iteration's host->device input copy with the previous iteration's compute.
+
+    ``batches(it)`` returns ``{name: pinned host float32 tensor}`` for
+    iteration ``it``.  Iteration ``it``'s copy runs on a side stream into one
+    of two device staging sets while iteration ``it - 1`` computes; the hook
+    then waits for it on the current stream and writes the staged tensors into
+    the store with one device-to-device copy each (`TensorStore.set`, in
+    place, so run()'s replay cache keeps its binding).  The reference's feeder
+    writes the store synchronously before each iteration (builders.py:284-365);
+    this is the same data flow with the transfer off the critical path.
+    ``iterations`` (optional) stops the look-ahead after the last iteration."""
+
+    def __init__(self, batches, device, iterations: int | None = None):
+        self.batches = batches
+        self.device = torch.device(device)
+        self.iterations = iterations
+        self._cs = None
+        self._staging: dict = {}
+        self._consumed = [None, None]
+        self._pending = None  # (iteration, staged, event, slot)
+
+    def _issue(self, it: int) -> None:
+        if self._cs is None:
+            self._cs = torch.cuda.Stream(device=self.device)
+        slot = it & 1
+        if self._consumed[slot] is not None:  # the set's previous contents are in the store
+            self._cs.wait_event(self._consumed[slot])
+        else:
+            self._cs.wait_stream(torch.cuda.current_stream(self.device))
+        staged = {}
+        with torch.cuda.stream(self._cs):
+            for name, src in self.batches(it).items():
+                buf = self._staging.get((slot, name))
+                if buf is None or buf.shape != src.shape:
+                    buf = torch.empty(src.shape, dtype=torch.float32, device=self.device)
+                    self._staging[(slot, name)] = buf
+                buf.copy_(src, non_blocking=True)
+                staged[name] = buf
+            ev = torch.cuda.Event()
+            ev.record(self._cs)
+        self._pending = (it, staged, ev, slot)
+
+    def __call__(self, it: int, store) -> None:
+        if self._pending is None or self._pending[0] != it:
+            self._issue(it)  # first iteration (or a restart): nothing to overlap with
+        _, staged, ev, slot = self._pending
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_event(ev)
+        for name, buf in staged.items():
+            store.set(name, buf)
+        done = torch.cuda.Event()
+        done.record(cur)
+        self._consumed[slot] = done
+        if self.iterations is None or it + 1 < self.iterations:
+            self._issue(it + 1)

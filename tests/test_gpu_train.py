@@ -346,3 +346,53 @@ def test_run_replay_cache_is_bitwise_the_walk(monkeypatch, momentum):
     assert out[0][0] == out[1][0]
     for p in out[0][1]:
         assert np.array_equal(out[0][1][p], out[1][1][p]), p
+
+
+def test_prefetch_feed_is_bitwise_the_synchronous_feed():
+    """PrefetchFeed (the look-ahead before_iteration hook: batch i+1 copied on a
+    side stream during iteration i) trains bit for bit like writing each batch
+    into the store synchronously, with a different batch every iteration."""
+    import torch
+
+    from paper_1412_6249_b200 import run_sequence
+    from paper_1412_6249_b200.exchange import build_rank_sequence
+    from paper_1412_6249_b200.executor import PrefetchFeed
+
+    net = cifar_convnet(batch=4, lr=0.01, momentum=0.9)
+    feed = SyntheticFeed.for_net(net, 17, spread=0.0)
+    pinned = {}
+
+    def batches(it):
+        if it not in pinned:
+            x, y = feed.batch_for(it, 0)
+            pinned[it] = (torch.from_numpy(np.ascontiguousarray(x, np.float32)).pin_memory(),
+                          torch.from_numpy(np.ascontiguousarray(y, np.float32)).pin_memory())
+        return pinned[it]
+
+    out = []
+    for mode in ("sync", "prefetch"):
+        st = TensorStore("cuda:0")
+        seq, _ = build_rank_sequence(net, 1, 0, st, bucket_bytes=32 << 10)
+        init_params(net, st, 17, seq.layout)
+        xname, lname = seq.layout.data_names[0], seq.layout.label_names[0]
+        loss_name = seq.layout.loss_names[0]
+        losses = []
+        if mode == "sync":
+            def before(it, s):
+                x, y = batches(it)
+                s.set(xname, x)
+                s.set(lname, y)
+        else:
+            before = PrefetchFeed(lambda it: dict(zip((xname, lname), batches(it))), "cuda:0",
+                                  iterations=6)
+
+        def after(rep, s):
+            if rep.graph_index == 0:
+                losses.append(float(s.array(loss_name)[0]))
+
+        run_sequence(seq, st, before_iteration=before, after_graph=after, iterations=6,
+                     trace=False)
+        out.append((losses, {p: st.array(f"{p}_p0") for p, _ in net.param_shapes()}))
+    assert out[0][0] == out[1][0]
+    for p in out[0][1]:
+        assert np.array_equal(out[0][1][p], out[1][1][p]), p
