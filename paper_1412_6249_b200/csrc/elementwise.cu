@@ -51,6 +51,15 @@ int chain_plain_mult() {
   return v;
 }
 
+// PURINE_B200_RELU_V4K=0: the grid-stride slice kernels instead of the 2-D ones
+static bool v4k_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("PURINE_B200_RELU_V4K");
+    return !(e && *e == '0');
+  }();
+  return v;
+}
+
 int sm_count_current() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -311,6 +320,82 @@ __global__ void finite_list_kernel(const FiniteList list, int* flag) {
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// the float4 path for k <= 4 parts: a 2-D grid (blocks over one image's run x
+// images) needs no index division, and each thread loads every part's float4
+// and the mask's for two elements before summing -- 2 * (K + 1) loads in
+// flight instead of one.  Same summation order as relu_bwd_slice_sum_v4: bitwise
+// the same.
+template <int K>
+__global__ void __launch_bounds__(256)
+    relu_bwd_slice_sum_v4k(const float4* __restrict__ x, Parts parts, float4* __restrict__ dx,
+                           int64_t run4, int64_t dy_img4, int64_t dy_off4, int64_t x_img4,
+                           int64_t x_off4) {
+  const int64_t img = blockIdx.y;
+  const float4* __restrict__ xs = x + img * x_img4 + x_off4;
+  float4* __restrict__ d = dx + img * run4;
+  const int64_t base = img * dy_img4 + dy_off4;
+  const int64_t step = (int64_t)gridDim.x * 2 * blockDim.x;
+  for (int64_t r0 = (int64_t)blockIdx.x * 2 * blockDim.x + threadIdx.x; r0 < run4; r0 += step) {
+    const int64_t r1 = r0 + blockDim.x;
+    const bool h1 = r1 < run4;
+    float4 v0[K], v1[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const float4* __restrict__ pq = reinterpret_cast<const float4*>(parts.p[q]) + base;
+      v0[q] = pq[r0];
+      v1[q] = h1 ? pq[r1] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float4 a0 = xs[r0];
+    const float4 a1 = h1 ? xs[r1] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 g0 = v0[0], g1 = v1[0];
+#pragma unroll
+    for (int q = 1; q < K; ++q) {
+      g0.x = __fadd_rn(g0.x, v0[q].x);
+      g0.y = __fadd_rn(g0.y, v0[q].y);
+      g0.z = __fadd_rn(g0.z, v0[q].z);
+      g0.w = __fadd_rn(g0.w, v0[q].w);
+      g1.x = __fadd_rn(g1.x, v1[q].x);
+      g1.y = __fadd_rn(g1.y, v1[q].y);
+      g1.z = __fadd_rn(g1.z, v1[q].z);
+      g1.w = __fadd_rn(g1.w, v1[q].w);
+    }
+    d[r0] = make_float4(relu_g(a0.x, g0.x), relu_g(a0.y, g0.y), relu_g(a0.z, g0.z),
+                        relu_g(a0.w, g0.w));
+    if (h1)
+      d[r1] = make_float4(relu_g(a1.x, g1.x), relu_g(a1.y, g1.y), relu_g(a1.z, g1.z),
+                          relu_g(a1.w, g1.w));
+  }
+}
+
+// launch relu_bwd_slice_sum_v4k for k in 1..4 parts; false for other k
+inline bool launch_slice_sum_v4k(const float4* x, const Parts& p, int k, float4* dx, int N,
+                                 int64_t run4, int64_t dy_img4, int64_t dy_off4, int64_t x_img4,
+                                 int64_t x_off4, cudaStream_t st) {
+  if (k < 1 || k > 4 || N < 1 || N > 65535 || !v4k_enabled()) return false;
+  const int64_t per_img = (run4 + 2 * kThreads - 1) / (2 * kThreads);
+  const int64_t cap = std::max<int64_t>(1, (int64_t)sm_count_current() * 8 / N);
+  const dim3 grid((unsigned)std::min(per_img, cap), (unsigned)N);
+  switch (k) {
+    case 1:
+      relu_bwd_slice_sum_v4k<1><<<grid, kThreads, 0, st>>>(x, p, dx, run4, dy_img4, dy_off4,
+                                                            x_img4, x_off4);
+      break;
+    case 2:
+      relu_bwd_slice_sum_v4k<2><<<grid, kThreads, 0, st>>>(x, p, dx, run4, dy_img4, dy_off4,
+                                                            x_img4, x_off4);
+      break;
+    case 3:
+      relu_bwd_slice_sum_v4k<3><<<grid, kThreads, 0, st>>>(x, p, dx, run4, dy_img4, dy_off4,
+                                                            x_img4, x_off4);
+      break;
+    default:
+      relu_bwd_slice_sum_v4k<4><<<grid, kThreads, 0, st>>>(x, p, dx, run4, dy_img4, dy_off4,
+                                                            x_img4, x_off4);
+      break;
+  }
+  return true;
+}
+
 }  // namespace
 }  // namespace bf
 
@@ -429,7 +514,11 @@ int bf_relu_bwd_slice_sum_x(const float* x, int x_c0, int x_ctot, const float* c
     p.p[i] = parts[i];
     vec = vec && aligned16(parts[i]);
   }
-  if (vec)
+  if (vec && launch_slice_sum_v4k(reinterpret_cast<const float4*>(x), p, k,
+                                  reinterpret_cast<float4*>(dx), N, run / 4,
+                                  (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4,
+                                  (int64_t)x_ctot * HW / 4, (int64_t)x_c0 * HW / 4, st)) {
+  } else if (vec)
     relu_bwd_slice_sum_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
         reinterpret_cast<const float4*>(x), p, k, reinterpret_cast<float4*>(dx), run / 4,
         (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4, (int64_t)x_ctot * HW / 4,
@@ -456,10 +545,17 @@ int bf_relu_bwd_slice_x(const float* x, int x_c0, int x_ctot, const float* dy_ca
   if (aligned16(x) && aligned16(dy_cat) && aligned16(dx) && run % 4 == 0 &&
       ((int64_t)ctot * HW) % 4 == 0 && ((int64_t)c0 * HW) % 4 == 0 &&
       ((int64_t)x_ctot * HW) % 4 == 0 && ((int64_t)x_c0 * HW) % 4 == 0) {
-    relu_bwd_slice_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
-        reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy_cat),
-        reinterpret_cast<float4*>(dx), run / 4, (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4,
-        (int64_t)x_ctot * HW / 4, (int64_t)x_c0 * HW / 4, n / 4);
+    Parts p;
+    p.p[0] = dy_cat;
+    if (!launch_slice_sum_v4k(reinterpret_cast<const float4*>(x), p, 1,
+                              reinterpret_cast<float4*>(dx), N, run / 4, (int64_t)ctot * HW / 4,
+                              (int64_t)c0 * HW / 4, (int64_t)x_ctot * HW / 4,
+                              (int64_t)x_c0 * HW / 4, st)) {
+      relu_bwd_slice_v4<<<elementwise_grid(n / 4, kThreads), kThreads, 0, st>>>(
+          reinterpret_cast<const float4*>(x), reinterpret_cast<const float4*>(dy_cat),
+          reinterpret_cast<float4*>(dx), run / 4, (int64_t)ctot * HW / 4, (int64_t)c0 * HW / 4,
+          (int64_t)x_ctot * HW / 4, (int64_t)x_c0 * HW / 4, n / 4);
+    }
   } else {
     relu_bwd_slice_s<<<elementwise_grid(n, kThreads), kThreads, 0, st>>>(
         x, dy_cat, dx, run, (int64_t)ctot * HW, (int64_t)c0 * HW, (int64_t)x_ctot * HW,

@@ -495,3 +495,40 @@ def test_flatten_is_zero_copy_alias():
     run(g, st)
     assert st.tensor("f").data_ptr() == st.tensor("a").data_ptr()
     assert np.array_equal(st.array("f"), x.reshape(2, 48))
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("shape", [(3, 8, 7, 7), (2, 12, 14, 14), (2, 3, 7, 7)])
+def test_relu_backward_slice_sum_bitwise(k, shape):
+    """relu_backward on a channel slice of a k-part gradient sum (the elided
+    aggregate -> concat_backward pair), with its mask read from a channel
+    slice of a wider tensor: bitwise relu_backward(x, ((p0 + p1) + ...)[slice])
+    (k <= 4 run the 2-D float4 kernel, k = 5 the grid-stride one)."""
+    import torch
+
+    from paper_1412_6249_b200 import _native
+
+    n, c, h, w = shape
+    ctot, c0, x_ctot, x_c0 = c + 8, 4, c + 4, 4
+    parts = [rnd(n, ctot, h, w) for _ in range(k)]
+    xw = rnd(n, x_ctot, h, w)
+    xw[:, x_c0:x_c0 + c].flat[::7] = 0.0  # masked exactly at zero too
+    acc = parts[0].copy()
+    for p in parts[1:]:
+        acc = f32(acc + p)
+    want = O.relu_backward(O.relu_forward(xw[:, x_c0:x_c0 + c]), acc[:, c0:c0 + c])
+    dev = [torch.from_numpy(p).cuda() for p in parts]
+    xd = torch.from_numpy(O.relu_forward(xw)).cuda()
+    dx = torch.full((n, c, h, w), float("nan"), device="cuda")
+    lib = _native.lib()
+    lib("bf_relu_bwd_slice_sum_x", xd.data_ptr(), x_c0, x_ctot,
+        _native.ptr_array([t.data_ptr() for t in dev]), k, c0, ctot, dx.data_ptr(), n, c, h * w,
+        torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert_bitwise(dx.cpu().numpy(), want)
+    if k == 1:  # the single-part entry point
+        dx.fill_(float("nan"))
+        lib("bf_relu_bwd_slice_x", xd.data_ptr(), x_c0, x_ctot, dev[0].data_ptr(), c0, ctot,
+            dx.data_ptr(), n, c, h * w, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert_bitwise(dx.cpu().numpy(), want)
