@@ -226,6 +226,19 @@ int bf_maxpool_bwd_x(const float* x, const float* dy, float* dx, int relu_from_x
 int bf_maxpool_bwd_staged(const float* mask, const float* dy, float* dx, int N, int C, int H,
                           int W, int P, int Q, int kernel, int stride, int pad,
                           bf_stream_t stream);
+/* signed argmax mask (backward = 3 for bf_maxpool_staged_ok: the forward and
+   this backward both fit).  The forward writes y and, per window, the flat
+   index of the first maximum when that maximum is > 0, -2 - index when it is
+   <= 0, -1 when there is none ([N][C][P][Q] float32).  The backward gathers from
+   it and dy only -- x is not read -- and with relu_from_sign != 0 applies the
+   relu_backward of the operator that produced x = relu(a) from the sign
+   (relu(a) > 0 <=> a > 0 at the argmax pixel; a pixel that is no window's
+   argmax gets 0 either way): bit-identical to bf_maxpool_bwd_x */
+int bf_maxpool_fwd_smask(const float* x, float* y, float* smask, int N, int C, int H, int W,
+                         int P, int Q, int kernel, int stride, int pad, bf_stream_t stream);
+int bf_maxpool_bwd_smask(const float* smask, const float* dy, float* dx, int relu_from_sign,
+                         int N, int C, int H, int W, int P, int Q, int kernel, int stride, int pad,
+                         bf_stream_t stream);
 int bf_avgpool_fwd(const float* x, float* y, int N, int C, int H, int W, int P, int Q,
                    int kernel, int stride, int pad, bf_stream_t stream);
 int bf_avgpool_bwd(const float* dy, float* dx, int N, int C, int H, int W, int P, int Q,

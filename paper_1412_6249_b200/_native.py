@@ -69,6 +69,8 @@ _SIGS = {
     "bf_maxpool_fwd_staged": [_p, _p, _p] + [_i] * 9 + [_p],
     "bf_maxpool_bwd_x": [_p, _p, _p, _i] + [_i] * 9 + [_p],
     "bf_maxpool_bwd_staged": [_p, _p, _p] + [_i] * 9 + [_p],
+    "bf_maxpool_fwd_smask": [_p, _p, _p] + [_i] * 9 + [_p],
+    "bf_maxpool_bwd_smask": [_p, _p, _p, _i] + [_i] * 9 + [_p],
     "bf_maxpool_fwd": [_p, _p, _p] + [_i] * 9 + [_p],
     "bf_maxpool_bwd": [_p, _p, _p] + [_i] * 9 + [_p],
     "bf_maxpool_bwd_relu": [_p, _p, _p, _p] + [_i] * 9 + [_p],

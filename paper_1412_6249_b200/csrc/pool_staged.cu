@@ -77,8 +77,9 @@ __device__ __forceinline__ void row_red(const float* __restrict__ xs, int W, boo
   if (v2 > m) { m = v2; d = 2; }
 }
 
-// walk output column pw of one plane over output rows [ph0, ph1); emit(ph, best, arg)
-// with arg the flat index h*W + w of the window's first maximum (-1: none)
+// walk output column pw of one plane over output rows [ph0, ph1); emit(ph, best, arg, li)
+// with arg the flat index h*W + w of the window's first maximum (-1: none) and li
+// its index 0..8 inside the 3x3 window (row-major)
 template <int S, class Emit>
 __device__ __forceinline__ void walk_windows(const float* __restrict__ xs, int H, int W, int pad,
                                              int pw, int ph0, int ph1, Emit&& emit) {
@@ -93,11 +94,11 @@ __device__ __forceinline__ void walk_windows(const float* __restrict__ xs, int H
   row_red(xs, W, (unsigned)(h + 2) < (unsigned)H, (h + 2) * W + ws, c0, c1, c2, m2, d2);
   for (int ph = ph0;;) {
     float best = -INFINITY;
-    int arg = -1;
-    if (m0 > best) { best = m0; arg = h * W + ws + d0; }
-    if (m1 > best) { best = m1; arg = (h + 1) * W + ws + d1; }
-    if (m2 > best) { best = m2; arg = (h + 2) * W + ws + d2; }
-    emit(ph, best, arg);
+    int arg = -1, li = -1;
+    if (m0 > best) { best = m0; arg = h * W + ws + d0; li = d0; }
+    if (m1 > best) { best = m1; arg = (h + 1) * W + ws + d1; li = 3 + d1; }
+    if (m2 > best) { best = m2; arg = (h + 2) * W + ws + d2; li = 6 + d2; }
+    emit(ph, best, arg, li);
     if (++ph >= ph1) break;
     h += S;
     if (S == 1) {
@@ -120,11 +121,25 @@ __device__ __forceinline__ void issue_loads(uint32_t dst, const float* src0, int
   if (n1) bulk_g2s(dst1, src1, (uint32_t)(n1 * 4), bar);
 }
 
+// signed argmax mask (smask): the flat index of the window's first maximum
+// when that maximum is > 0, -2 - index when it is <= 0, -1 when there is none.
+// The sign is x's at the argmax pixel -- all a folded relu_backward of
+// x = relu(a) needs there (relu(a) > 0 <=> a > 0; a pixel that is no window's
+// argmax gets 0 either way) -- so the backward reads neither x nor a
+__device__ __forceinline__ float enc_signed(int arg, float best) {
+  return arg < 0 ? -1.f : (float)(best > 0.f ? arg : -2 - arg);
+}
+// argmax from a signed entry (without the fold)
+__device__ __forceinline__ int dec_signed(float v) {
+  const int a = (int)v;
+  return a >= -1 ? a : -2 - a;
+}
+
 template <int S>
 __global__ void __launch_bounds__(kThreads, 2) maxpool3_fwd_staged(const float* __restrict__ x,
                                                                    float* __restrict__ y,
                                                                    float* __restrict__ mask,
-                                                                   Geo g) {
+                                                                   Geo g, int signed_mask) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t full[kMaxStages];
   const int HW = g.H * g.W, PQ = g.P * g.Q;
@@ -159,14 +174,21 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_fwd_staged(const float* 
       float* yp = yc + gl * PQ + pw;
       if (mc) {
         float* mp = mc + gl * PQ + pw;
-        walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
-                        [&](int ph, float best, int arg) {
-                          yp[ph * g.Q] = best;
-                          mp[ph * g.Q] = (float)arg;
-                        });
+        if (signed_mask)
+          walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
+                          [&](int ph, float best, int arg, int) {
+                            yp[ph * g.Q] = best;
+                            mp[ph * g.Q] = enc_signed(arg, best);
+                          });
+        else
+          walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
+                          [&](int ph, float best, int arg, int) {
+                            yp[ph * g.Q] = best;
+                            mp[ph * g.Q] = (float)arg;
+                          });
       } else {
         walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
-                        [&](int ph, float best, int) { yp[ph * g.Q] = best; });
+                        [&](int ph, float best, int, int) { yp[ph * g.Q] = best; });
       }
     }
     __syncthreads();  // every read of this stage is done: refill it
@@ -183,18 +205,22 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_fwd_staged(const float* 
   }
 }
 
-// MASK = false: x is the pool input, every window's argmax is recomputed
-// (phase 1); MASK = true: x is the forward's argmax mask (flat indices as
-// float32, [planes][P][Q]) and phase 1 is skipped
-template <int S, bool MASK>
+// MODE 0: x is the pool input, every window's argmax is recomputed (phase 1);
+// MODE 1: x is the forward's argmax mask (flat indices as float32,
+// [planes][P][Q]); MODE 2: x is the forward's signed mask (enc_signed);
+// MODE 3: the same with the folded relu_backward, which needs no decode: the
+// negative entries of windows whose maximum is <= 0 match no pixel, so those
+// windows drop out.  Modes 1-3 skip phase 1.
+template <int S, int MODE>
 __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* __restrict__ x,
                                                                    const float* __restrict__ dy,
                                                                    float* __restrict__ dx, Geo g,
                                                                    int relu_from_x) {
   extern __shared__ __align__(128) float sm[];
   __shared__ uint64_t full[kMaxStages];
+  constexpr bool MASK = MODE != 0;
   const int HW = g.H * g.W, PQ = g.P * g.Q;
-  // stage: [x: G*HW][dy: G*PQ][arg: G*PQ ints] (MASK: [mask: G*PQ][dy: G*PQ]);
+  // stage: [x: G*HW][dy: G*PQ][arg: G*PQ ints] (MODE 1, 2: [mask: G*PQ][dy: G*PQ]);
   // x / mask and dy segments 16-byte aligned
   const int XP = MASK ? PQ : HW;
   const int xseg = (g.G * XP + 3) & ~3, dseg = (g.G * PQ + 3) & ~3;
@@ -226,9 +252,11 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
     const float* gs0 = xs0 + xseg;
     int* as0 = reinterpret_cast<int*>(const_cast<float*>(gs0 + dseg));
     const int gh = planes_of(c);
-    // window argmax as an int: recomputed (phase 1) or the mask's float
+    // window argmax as an int: recomputed (phase 1), the mask's float, or the
+    // signed mask's
     const float* mk0 = xs0;
     auto arg_at = [&](const int* ap, const float* mp, int o) -> int {
+      if (MODE == 2) return dec_signed(mp[o]);
       return MASK ? (int)mp[o] : ap[o];
     };
     // phase 1: every window's argmax (the forward's scan)
@@ -239,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
       const int ph0 = run * g.RB, ph1 = min(g.P, ph0 + g.RB);
       int* ap = as0 + gl * PQ + pw;
       walk_windows<S>(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
-                      [&](int ph, float, int arg) { ap[ph * g.Q] = arg; });
+                      [&](int ph, float, int arg, int) { ap[ph * g.Q] = arg; });
     }
     if (!MASK) __syncthreads();
     // phase 2: per input pixel, dy of the windows whose argmax it is, in window
@@ -289,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
           for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, Ab[j] == me ? Db[j] : 0.f);
 #pragma unroll
           for (int j = 0; j < 3; ++j) acc = __fadd_rn(acc, Ac[j] == me ? Dc[j] : 0.f);
-          if (!MASK && relu_from_x) acc = xs[me] > 0.f ? acc : 0.f;
+          if (MODE == 0 && relu_from_x) acc = xs[me] > 0.f ? acc : 0.f;
           dp[h * g.W] = acc;
           if (++h >= h1) return false;
           ++p;
@@ -336,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
         a10 = __fadd_rn(a10, aBB == e10 ? gBB : 0.f);
         a11 = __fadd_rn(a11, aBB == e11 ? gBB : 0.f);
         const bool r0 = h0 >= 0, r1 = h0 + 1 < g.H, k0 = w0 >= 0, k1 = w0 + 1 < g.W;
-        if (!MASK && relu_from_x) {
+        if (MODE == 0 && relu_from_x) {
           if (r0 && k0) a00 = xs[e00] > 0.f ? a00 : 0.f;
           if (r0 && k1) a01 = xs[e01] > 0.f ? a01 : 0.f;
           if (r1 && k0) a10 = xs[e10] > 0.f ? a10 : 0.f;
@@ -372,7 +400,8 @@ inline int align_planes(int per_plane_floats) {  // smallest G with G * f % 4 ==
   return 4;
 }
 
-// bwd: 0 forward, 1 backward recomputing the argmax from x, 2 backward from the mask
+// bwd: 0 forward, 1 backward recomputing the argmax from x, 2 backward from the
+// float mask, 3 backward from the signed mask (the same geometry as 2)
 bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int pad) {
   g.H = H; g.W = W; g.P = P; g.Q = Q; g.pad = pad;
   g.planes = (int64_t)N * C;
@@ -380,6 +409,7 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
   const int HW = H * W, PQ = P * Q;
   // every window must overlap the plane (the oracle's windows never lie fully in padding)
   if ((P - 1) * S - pad >= H || (Q - 1) * S - pad >= W) return false;
+  if (bwd == 3) bwd = 2;  // the signed mask: the float mask's geometry
   const int a = std::max(align_planes(HW), align_planes(PQ));
   if ((g.planes * HW) % 4 || (g.planes * PQ) % 4) return false;
   const int64_t per_plane = bwd == 2 ? 2LL * PQ : bwd ? (int64_t)HW + 2LL * PQ : (int64_t)HW;
@@ -387,8 +417,9 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
   G = (G + a - 1) / a * a;
   if (G > g.planes) G = (int)((g.planes + a - 1) / a * a);
   auto stage_floats = [&](int G_) {
-    return bwd == 2 ? ((G_ * PQ + 3) & ~3) * 2
-                    : bwd ? ((G_ * HW + 3) & ~3) + ((G_ * PQ + 3) & ~3) + G_ * PQ : G_ * HW;
+    return bwd == 2   ? ((G_ * PQ + 3) & ~3) * 2
+           : bwd      ? ((G_ * HW + 3) & ~3) + ((G_ * PQ + 3) & ~3) + G_ * PQ
+                      : G_ * HW;
   };
   const int64_t sb = (int64_t)stage_floats(G) * 4;
   if (sb * 2 > kSmemBudget) return false;
@@ -483,6 +514,13 @@ extern "C" {
 int bf_maxpool_staged_ok(int N, int C, int H, int W, int P, int Q, int kernel, int stride,
                          int pad, int backward) {
   pools::Geo g;
+  if (backward == 3) {  // the signed-mask pair: forward and backward both fit
+    pools::Geo g0;
+    return kernel == 3 && pools::plan(g0, 0, N, C, H, W, P, Q, stride, pad) &&
+                   pools::plan(g, 3, N, C, H, W, P, Q, stride, pad)
+               ? 1
+               : 0;
+  }
   // backward 1 (argmax recomputed from x) at stride 1: the recompute + 9-window
   // gather costs ~140 instructions per pixel (1.5 TB/s), so stride-1 pools keep
   // their mask unless PURINE_B200_POOL_STAGED bit 0 asks otherwise
@@ -502,8 +540,47 @@ int bf_maxpool_fwd_staged(const float* x, float* y, float* mask, int N, int C, i
   auto kern = stride == 1 ? pools::maxpool3_fwd_staged<1> : pools::maxpool3_fwd_staged<2>;
   const int grid = pools::grid_for(kern, g, cfg[stride - 1]);
   if (grid <= 0) return 1;
-  kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(x, y, mask, g);
+  kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(x, y, mask, g, 0);
   return check_launch("maxpool_forward(staged)");
+}
+
+int bf_maxpool_fwd_smask(const float* x, float* y, float* smask, int N, int C, int H, int W,
+                         int P, int Q, int kernel, int stride, int pad, bf_stream_t s) {
+  pools::Geo g, gb;
+  BF_REQUIRE(kernel == 3 && pools::plan(g, 0, N, C, H, W, P, Q, stride, pad) &&
+                 pools::plan(gb, 3, N, C, H, W, P, Q, stride, pad),
+             "maxpool_forward(signed mask): unsupported shape %dx%dx%dx%d k%d s%d p%d", N, C, H,
+             W, kernel, stride, pad);
+  BF_REQUIRE((reinterpret_cast<uintptr_t>(x) & 15) == 0 && smask != nullptr,
+             "maxpool_forward(signed mask): x not 16B aligned or no mask buffer");
+  const int smem = g.NS * g.stage_floats * 4;
+  static bool cfg[2] = {false, false};
+  auto kern = stride == 1 ? pools::maxpool3_fwd_staged<1> : pools::maxpool3_fwd_staged<2>;
+  const int grid = pools::grid_for(kern, g, cfg[stride - 1]);
+  if (grid <= 0) return 1;
+  kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(x, y, smask, g, 1);
+  return check_launch("maxpool_forward(signed mask)");
+}
+
+int bf_maxpool_bwd_smask(const float* smask, const float* dy, float* dx, int relu_from_sign,
+                         int N, int C, int H, int W, int P, int Q, int kernel, int stride, int pad,
+                         bf_stream_t s) {
+  pools::Geo g;
+  BF_REQUIRE(kernel == 3 && pools::plan(g, 3, N, C, H, W, P, Q, stride, pad),
+             "maxpool_backward(signed mask): unsupported shape %dx%dx%dx%d k%d s%d p%d", N, C, H,
+             W, kernel, stride, pad);
+  BF_REQUIRE((reinterpret_cast<uintptr_t>(smask) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(dy) & 15) == 0,
+             "maxpool_backward(signed mask): mask / dy not 16B aligned");
+  const int smem = g.NS * g.stage_floats * 4;
+  static bool cfg[4] = {false, false, false, false};
+  auto kern = relu_from_sign
+                  ? (stride == 1 ? pools::maxpool3_bwd_staged<1, 3> : pools::maxpool3_bwd_staged<2, 3>)
+                  : (stride == 1 ? pools::maxpool3_bwd_staged<1, 2> : pools::maxpool3_bwd_staged<2, 2>);
+  const int grid = pools::grid_for(kern, g, cfg[(stride - 1) + (relu_from_sign ? 2 : 0)]);
+  if (grid <= 0) return 1;
+  kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(smask, dy, dx, g, relu_from_sign);
+  return check_launch("maxpool_backward(signed mask)");
 }
 
 int bf_maxpool_bwd_x(const float* x, const float* dy, float* dx, int relu_from_x, int N, int C,
@@ -516,7 +593,7 @@ int bf_maxpool_bwd_x(const float* x, const float* dy, float* dx, int relu_from_x
              "maxpool_backward(staged): x / dy not 16B aligned");
   const int smem = g.NS * g.stage_floats * 4;
   static bool cfg[2] = {false, false};
-  auto kern = stride == 1 ? pools::maxpool3_bwd_staged<1, false> : pools::maxpool3_bwd_staged<2, false>;
+  auto kern = stride == 1 ? pools::maxpool3_bwd_staged<1, 0> : pools::maxpool3_bwd_staged<2, 0>;
   const int grid = pools::grid_for(kern, g, cfg[stride - 1]);
   if (grid <= 0) return 1;
   kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(x, dy, dx, g, relu_from_x);
@@ -534,7 +611,7 @@ int bf_maxpool_bwd_staged(const float* mask, const float* dy, float* dx, int N, 
              "maxpool_backward(staged mask): mask / dy not 16B aligned");
   const int smem = g.NS * g.stage_floats * 4;
   static bool cfg[2] = {false, false};
-  auto kern = stride == 1 ? pools::maxpool3_bwd_staged<1, true> : pools::maxpool3_bwd_staged<2, true>;
+  auto kern = stride == 1 ? pools::maxpool3_bwd_staged<1, 1> : pools::maxpool3_bwd_staged<2, 1>;
   const int grid = pools::grid_for(kern, g, cfg[stride - 1]);
   if (grid <= 0) return 1;
   kern<<<grid, pools::kThreads, smem, as_stream(s)>>>(mask, dy, dx, g, 0);

@@ -423,13 +423,15 @@ class _Plan:
 
         foldable = tuple(k for k in os.environ.get(RELU_FOLD_ENV, RELU_FOLD_DEFAULT).split(",") if k)
         # max-pool mask elision: when a maxpool_forward's argmax mask feeds only
-        # maxpool_backward operators of the same x and attributes, and the
-        # shared-memory staged kernels fit the shape, the backward recomputes
-        # every window's argmax from x (the forward's own scan: bit-identical)
-        # and the forward never stores the mask -- taken where the backward also
-        # absorbs the relu_backward of the ReLU that produced x (then x is read
-        # anyway, as the ReLU mask); elsewhere reading the mask is less traffic
-        # than re-reading x (a quarter of its size at stride 2)
+        # maxpool_backward operators of the same x and attributes, the backward
+        # also absorbs the relu_backward of the ReLU that produced x, and the
+        # shared-memory staged kernels fit the shape, the graph's float mask is
+        # never stored: the forward writes a signed mask instead (argmax, with
+        # the sign of the window's maximum = the ReLU mask at that pixel), so
+        # the backward reads neither x nor a (pool1: 0.23 -> 0.12 ms); with
+        # PURINE_B200_POOL_SMASK=0 the backward recomputes every argmax from x
+        # (the forward's own scan: bit-identical).  Elsewhere the staged
+        # backward reads the graph's mask (a quarter of x at stride 2)
         for oid, op in graph.operators.items():
             if op.kind != "maxpool_forward" or len(op.outputs) != 2:
                 continue
@@ -441,7 +443,19 @@ class _Plan:
                     graph.operators[c].inputs[1] != mk or
                     graph.operators[c].attrs != op.attrs for c, _ in cons):
                 continue
-            if not _pool_staged(graph, op) or not _pool_relu_foldable(graph, cons, foldable):
+            if not _pool_relu_foldable(graph, cons, foldable):
+                continue
+            if os.environ.get(POOL_SMASK_ENV, "1") != "0" and _pool_staged(graph, op, 3):
+                # the signed mask: each window's argmax with the sign of its
+                # maximum, which is the folded ReLU's mask at that pixel -- the
+                # backward reads neither x nor the graph's float mask
+                name = graph.tensors[mk].name + "#signed"
+                self.fusion.setdefault(oid, {})["pool_smask"] = name
+                for c, _ in cons:
+                    self.fusion.setdefault(c, {})["pool_smask"] = name
+                self.elided.add(graph.tensors[mk].name)
+                continue
+            if not _pool_staged(graph, op):
                 continue
             self.fusion.setdefault(oid, {})["pool_no_mask"] = True
             for c, _ in cons:
@@ -458,7 +472,8 @@ class _Plan:
             g = op.inputs[1]
             p = graph.producer_of(g)
             if (p is None or graph.operators[p].kind not in foldable
-                    or (p in self.fusion and set(self.fusion[p]) != {"pool_recompute"})
+                    or (p in self.fusion
+                        and set(self.fusion[p]) not in ({"pool_recompute"}, {"pool_smask"}))
                     or len(graph.consumers_of(g)) != 1 or p in self.fused_away):
                 continue
             rx = graph.tensors[op.inputs[0]].name
@@ -847,6 +862,7 @@ GROUP_ENV = "PURINE_B200_GROUP_1X1"  # "0" disables the Inception 1x1 horizontal
 PREACT_ENV = "PURINE_B200_PREACT_ELISION"  # "0" keeps every conv pre-activation stored
 # producer kinds that may absorb the relu_backward after them (all three have the
 # kernel support; measured net gains decide the default)
+POOL_SMASK_ENV = "PURINE_B200_POOL_SMASK"  # "0": recompute the argmax from x instead
 RELU_FOLD_ENV = "PURINE_B200_RELU_FOLD"
 RELU_FOLD_DEFAULT = "conv2d_backward_data,lrn_backward,maxpool_backward"
 
@@ -868,9 +884,10 @@ def _pool_relu_foldable(graph: BiGraph, cons, foldable) -> bool:
                for c, _ in graph.consumers_of(rb.inputs[0]))
 
 
-def _pool_staged(graph: BiGraph, op) -> bool:
+def _pool_staged(graph: BiGraph, op, mode: int = 1) -> bool:
     """Whether the shared-memory staged max-pool kernels take this shape (both
-    directions): the condition for eliding the argmax mask."""
+    directions; mode 1: the backward recomputing the argmax from x, 3: the
+    signed-mask pair): the condition for eliding the float argmax mask."""
     from .kinds import pool_attrs
 
     try:
@@ -880,6 +897,8 @@ def _pool_staged(graph: BiGraph, op) -> bool:
         n, c, h, w = graph.tensors[op.inputs[0]].shape
         _, _, ph, pw = graph.tensors[op.outputs[0]].shape
         ok = _native.lib().raw("bf_maxpool_staged_ok")
+        if mode == 3:
+            return bool(ok(n, c, h, w, ph, pw, k, s, p, 3))
         return bool(ok(n, c, h, w, ph, pw, k, s, p, 0) and ok(n, c, h, w, ph, pw, k, s, p, 1))
     except Exception:  # noqa: BLE001 - no library: the plain kernels run (and fail loudly)
         return False
@@ -906,7 +925,8 @@ def _plan(graph: BiGraph, cap: int) -> _Plan:
     that happens to reuse its address."""
     branches = _branch_streams()
     key = (cap, branches, _finite_mode(), os.environ.get(GROUP_ENV, "1"),
-           os.environ.get(RELU_FOLD_ENV, RELU_FOLD_DEFAULT), os.environ.get(PREACT_ENV, "1"))
+           os.environ.get(RELU_FOLD_ENV, RELU_FOLD_DEFAULT), os.environ.get(PREACT_ENV, "1"),
+           os.environ.get(POOL_SMASK_ENV, "1"))
     stamp = len(graph.insertion_order) * 1_000_003 + len(graph.tensors)
     cache = graph.__dict__.setdefault("_launch_plans", {})
     hit = cache.get(key)

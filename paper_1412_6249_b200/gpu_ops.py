@@ -423,6 +423,11 @@ def _maxpool_fwd(ctx, op):
     g = ctx.graph
     yv = g.tensors[op.outputs[0]]
     y = ctx.store.ensure(yv.name, yv.shape)
+    if fused.get("pool_smask"):  # the signed mask (dispatcher _Plan): argmax + sign per window
+        sm = ctx.store.ensure(fused["pool_smask"], y.shape)
+        _L()("bf_maxpool_fwd_smask", x.ptr, y.ptr, sm.ptr, n, c, h, w, y.shape[2], y.shape[3],
+             k, s, p, ctx.stream)
+        return
     if fused.get("pool_no_mask"):  # only maxpool_backward reads it, and it recomputes it
         _L()("bf_maxpool_fwd_staged", x.ptr, y.ptr, None, n, c, h, w, y.shape[2], y.shape[3], k,
              s, p, ctx.stream)
@@ -436,6 +441,20 @@ def _maxpool_fwd(ctx, op):
 def _maxpool_bwd(ctx, op):
     k, s, p = pool_attrs(op.attrs)
     fused = getattr(ctx, "fused", None) or {}
+    if fused.get("pool_smask"):  # gather from the signed mask and dy; x is not read
+        g = ctx.graph
+        xv = g.tensors[op.inputs[0]]
+        dy = ctx.store.get(g.tensors[op.inputs[2]].name)
+        n, c, h, w = xv.shape
+        sm = ctx.store.get(fused["pool_smask"])
+        if fused.get("relu_from_x"):  # + the relu_backward of x = relu(a), from the sign
+            dx = ctx.store.ensure(fused["relu_dx"], xv.shape)
+        else:
+            dxv = g.tensors[op.outputs[0]]
+            dx = ctx.store.ensure(dxv.name, dxv.shape)
+        _L()("bf_maxpool_bwd_smask", sm.ptr, dy.ptr, dx.ptr, int(bool(fused.get("relu_from_x"))),
+             n, c, h, w, dy.shape[2], dy.shape[3], k, s, p, ctx.stream)
+        return
     if fused.get("pool_recompute"):  # argmax recomputed from x (the mask is elided)
         g = ctx.graph
         x = ctx.store.get(g.tensors[op.inputs[0]].name)

@@ -268,16 +268,21 @@ MAXPOOL_STAGED_SHAPES = [((2, 64, 112, 112), 3, 2, 0), ((2, 192, 56, 56), 3, 2, 
 @pytest.mark.parametrize("fold", [False, True], ids=["pool", "relu+pool"])
 @pytest.mark.parametrize("values", ["normal", "coarse"])
 @pytest.mark.parametrize("s1_bwd", ["0", "1"], ids=["default", "s1-staged"])
-def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values, s1_bwd, monkeypatch):
+@pytest.mark.parametrize("smask", ["1", "0"], ids=["signed-mask", "recompute"])
+def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values, s1_bwd, smask,
+                                            monkeypatch):
     """The product pairing: maxpool_forward and maxpool_backward in one graph,
-    the mask elided (the backward recomputes each window's argmax from x with
-    the forward's scan) and, after a ReLU, the relu_backward folded in through
-    the pool's own input.  y, dx (or the folded da) bit-exact vs the oracle."""
+    the float mask elided -- the forward writes a signed mask (each window's
+    argmax carrying the sign of its maximum) that the backward gathers from, or
+    (smask off) the backward recomputes each argmax from x with the forward's scan --
+    and, after a ReLU, the relu_backward folded in through the pool's own
+    input.  y, dx (or the folded da) bit-exact vs the oracle."""
     from paper_1412_6249_b200 import BiGraph, Location, TensorStore, run
     from paper_1412_6249_b200._native import lib
     from paper_1412_6249_b200.dispatcher import _plan
 
     monkeypatch.setenv("PURINE_B200_POOL_STAGED", s1_bwd)  # 1: stride-1 backward staged too
+    monkeypatch.setenv("PURINE_B200_POOL_SMASK", smask)
     loc = Location("local", 0)
     a = rnd(*shape)
     a[:, :, ::3, ::3] = 0.5
@@ -304,8 +309,9 @@ def test_maxpool_staged_mask_elided_bitwise(shape, k, s, p, fold, values, s1_bwd
     n, c, h, w = shape
     # the mask is elided where the backward also absorbs the ReLU backward
     # through x (fold); otherwise the staged backward reads the mask
-    staged = fold and bool(lib().raw("bf_maxpool_staged_ok")(n, c, h, w, y.shape[2], y.shape[3],
-                                                              k, s, p, 1))
+    ok = lib().raw("bf_maxpool_staged_ok")
+    staged = fold and bool(ok(n, c, h, w, y.shape[2], y.shape[3], k, s, p, 1) or
+                           (smask == "1" and ok(n, c, h, w, y.shape[2], y.shape[3], k, s, p, 3)))
     plan = _plan(g, 8)
     assert ("m" in plan.elided) == staged
     st = TensorStore("cuda:0")
