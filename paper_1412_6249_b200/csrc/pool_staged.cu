@@ -56,6 +56,10 @@ struct Geo {
   // (backward phase 2), its inner extent
   uint64_t m_pp1, m_q, m_pp2, m_in2;
   int s_pp1, s_q, s_pp2, s_in2;
+  // stride-1 forward over column pairs (Q even): items per plane, pairs per row
+  int pairs;  // 0: one column per item
+  uint64_t m_pp1p, m_qp;
+  int s_pp1p, s_qp;
 };
 
 __device__ __forceinline__ int fdiv(int x, uint64_t m, int s) {
@@ -113,6 +117,63 @@ __device__ __forceinline__ void walk_windows(const float* __restrict__ xs, int H
   }
 }
 
+// stride 1, two adjacent output columns pw, pw + 1 (windows a, b over input
+// columns ws..ws+2 and ws+1..ws+3): four shared loads and five first-max folds
+// per new row instead of six and six.  The folds are seeded with -inf, so the
+// result is the first maximum in window raster order with strict '>', exactly
+// walk_windows' (NaN never wins, ties keep the earlier tap).
+struct Mx {
+  float m;
+  int d;  // column offset inside the window, -1: none
+};
+__device__ __forceinline__ void fold(Mx& a, float v, int d) {
+  if (v > a.m) { a.m = v; a.d = d; }
+}
+template <class Emit>
+__device__ __forceinline__ void walk_pair(const float* __restrict__ xs, int H, int W, int pad,
+                                          int pw, int ph0, int ph1, Emit&& emit) {
+  const int ws = pw - pad;
+  const bool c0 = (unsigned)ws < (unsigned)W, c1 = (unsigned)(ws + 1) < (unsigned)W,
+             c2 = (unsigned)(ws + 2) < (unsigned)W, c3 = (unsigned)(ws + 3) < (unsigned)W;
+  auto row = [&](int h, Mx& ra, Mx& rb) {
+    const bool rv = (unsigned)h < (unsigned)H;
+    const int off = h * W + ws;
+    const float v0 = (rv && c0) ? xs[off] : -INFINITY;
+    const float v1 = (rv && c1) ? xs[off + 1] : -INFINITY;
+    const float v2 = (rv && c2) ? xs[off + 2] : -INFINITY;
+    const float v3 = (rv && c3) ? xs[off + 3] : -INFINITY;
+    Mx p{-INFINITY, -1};  // first max of columns ws+1, ws+2 (offsets 0, 1 from ws+1)
+    fold(p, v1, 0);
+    fold(p, v2, 1);
+    ra = Mx{-INFINITY, -1};
+    fold(ra, v0, 0);
+    if (p.m > ra.m) { ra.m = p.m; ra.d = p.d + 1; }
+    rb = p;
+    fold(rb, v3, 2);
+  };
+  Mx a0, a1, a2, b0, b1, b2;
+  int h = ph0 - pad;
+  row(h, a0, b0);
+  row(h + 1, a1, b1);
+  row(h + 2, a2, b2);
+  for (int ph = ph0;;) {
+    float ba = -INFINITY, bb = -INFINITY;
+    int ga = -1, gb = -1;
+    if (a0.m > ba) { ba = a0.m; ga = h * W + ws + a0.d; }
+    if (a1.m > ba) { ba = a1.m; ga = (h + 1) * W + ws + a1.d; }
+    if (a2.m > ba) { ba = a2.m; ga = (h + 2) * W + ws + a2.d; }
+    if (b0.m > bb) { bb = b0.m; gb = h * W + ws + 1 + b0.d; }
+    if (b1.m > bb) { bb = b1.m; gb = (h + 1) * W + ws + 1 + b1.d; }
+    if (b2.m > bb) { bb = b2.m; gb = (h + 2) * W + ws + 1 + b2.d; }
+    emit(ph, ba, ga, bb, gb);
+    if (++ph >= ph1) break;
+    ++h;
+    a0 = a1; a1 = a2;
+    b0 = b1; b1 = b2;
+    row(h + 2, a2, b2);
+  }
+}
+
 __device__ __forceinline__ void issue_loads(uint32_t dst, const float* src0, int64_t n0,
                                             uint32_t dst1, const float* src1, int64_t n1,
                                             uint64_t* bar) {
@@ -160,13 +221,32 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_fwd_staged(const float* 
   }
   int s = 0;
   uint32_t phase = 0;
-  const int per_plane = g.runs * g.Q;
+  const int per_plane = g.runs * (S == 1 && g.pairs ? g.pairs : g.Q);
   for (int64_t c = blockIdx.x; c < g.nchunks; c += gridDim.x) {
     mbar_wait(&full[s], phase);
     const float* xs0 = sm + s * g.stage_floats;
     const int items = planes_of(c) * per_plane;
     float* yc = y + c * g.G * PQ;
     float* mc = mask ? mask + c * g.G * PQ : nullptr;
+    if (S == 1 && g.pairs) {
+      // two columns per item: float2 stores of y and the mask
+      for (int it = threadIdx.x; it < items; it += kThreads) {
+        const int gl = fdiv(it, g.m_pp1p, g.s_pp1p), r = it - gl * per_plane;
+        const int run = fdiv(r, g.m_qp, g.s_qp), pw = 2 * (r - run * g.pairs);
+        const int ph0 = run * g.RB, ph1 = min(g.P, ph0 + g.RB);
+        float* yp = yc + gl * PQ + pw;
+        float* mp = mc ? mc + gl * PQ + pw : nullptr;
+        walk_pair(xs0 + gl * HW, g.H, g.W, g.pad, pw, ph0, ph1,
+                  [&](int ph, float ba, int ga, float bb, int gb) {
+                    *reinterpret_cast<float2*>(yp + ph * g.Q) = make_float2(ba, bb);
+                    if (mp) {
+                      *reinterpret_cast<float2*>(mp + ph * g.Q) =
+                          signed_mask ? make_float2(enc_signed(ga, ba), enc_signed(gb, bb))
+                                      : make_float2((float)ga, (float)gb);
+                    }
+                  });
+      }
+    } else
     for (int it = threadIdx.x; it < items; it += kThreads) {
       const int gl = fdiv(it, g.m_pp1, g.s_pp1), r = it - gl * per_plane;
       const int run = fdiv(r, g.m_q, g.s_q), pw = r - run * g.Q;
@@ -464,6 +544,16 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
   };
   magic((uint32_t)(g.runs * Q), g.m_pp1, g.s_pp1);
   magic((uint32_t)Q, g.m_q, g.s_q);
+  g.pairs = 0;
+  static const int pair_cols = [] {
+    const char* e = getenv("PURINE_B200_POOL_PAIRS");
+    return e && *e ? atoi(e) : 1;
+  }();
+  if (pair_cols && bwd == 0 && S == 1 && Q % 2 == 0) {
+    g.pairs = Q / 2;
+    magic((uint32_t)(g.runs * g.pairs), g.m_pp1p, g.s_pp1p);
+    magic((uint32_t)g.pairs, g.m_qp, g.s_qp);
+  }
   if (S == 1) {
     magic((uint32_t)(g.hruns * W), g.m_pp2, g.s_pp2);
     magic((uint32_t)W, g.m_in2, g.s_in2);
