@@ -522,17 +522,28 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
   g.nchunks = (g.planes + G - 1) / G;
   // walker runs: enough items to occupy the CTA twice over, long runs for the
   // row reuse
-  auto run_len = [&](int rows, int cols) {
+  auto run_len = [&](int rows, int cols, int min_rows = 8) {
     const int64_t colitems = (int64_t)G * cols;
     int rb = rows;
     // (runs shorter than ~8 rows spend more on the walker's warm-up rows and
     // index decode than an idle thread costs: measured 226 -> ~70 instructions
     // per pixel for the stride-1 backward)
     if (colitems < 2 * kThreads)
-      rb = (int)std::max<int64_t>(8, rows * colitems / (2 * kThreads));
+      rb = (int)std::max<int64_t>(min_rows, rows * colitems / (2 * kThreads));
     return rb > rows ? rows : rb;
   };
-  g.RB = run_len(P, Q);
+  static const int pair_cols = [] {
+    const char* e = getenv("PURINE_B200_POOL_PAIRS");
+    return e && *e ? atoi(e) : 1;
+  }();
+  // the pair walker: half the items per row, so shorter runs keep the CTA
+  // busy (28x28 planes 76 -> 66 us with 4-row runs, 14x14 46 -> 42)
+  static const int pair_rb = [] {
+    const char* e = getenv("PURINE_B200_POOL_PAIR_RB");
+    return e && *e ? atoi(e) : 4;
+  }();
+  const bool pairs = pair_cols && bwd == 0 && S == 1 && Q % 2 == 0;
+  g.RB = pairs ? run_len(P, Q / 2, pair_rb) : run_len(P, Q);
   g.runs = (P + g.RB - 1) / g.RB;
   g.RBh = run_len(H, W);
   g.hruns = (H + g.RBh - 1) / g.RBh;
@@ -545,11 +556,7 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
   magic((uint32_t)(g.runs * Q), g.m_pp1, g.s_pp1);
   magic((uint32_t)Q, g.m_q, g.s_q);
   g.pairs = 0;
-  static const int pair_cols = [] {
-    const char* e = getenv("PURINE_B200_POOL_PAIRS");
-    return e && *e ? atoi(e) : 1;
-  }();
-  if (pair_cols && bwd == 0 && S == 1 && Q % 2 == 0) {
+  if (pairs) {
     g.pairs = Q / 2;
     magic((uint32_t)(g.runs * g.pairs), g.m_pp1p, g.s_pp1p);
     magic((uint32_t)g.pairs, g.m_qp, g.s_qp);
