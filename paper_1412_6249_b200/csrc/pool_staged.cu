@@ -543,9 +543,13 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
     return e && *e ? atoi(e) : 4;
   }();
   const bool pairs = pair_cols && bwd == 0 && S == 1 && Q % 2 == 0;
-  g.RB = pairs ? run_len(P, Q / 2, pair_rb) : run_len(P, Q);
+  static const int rb_min = [] {  // probe: the other walkers' minimum run
+    const char* e = getenv("PURINE_B200_POOL_RB_MIN");
+    return e && *e ? atoi(e) : 8;
+  }();
+  g.RB = pairs ? run_len(P, Q / 2, pair_rb) : run_len(P, Q, rb_min);
   g.runs = (P + g.RB - 1) / g.RB;
-  g.RBh = run_len(H, W);
+  g.RBh = run_len(H, W, rb_min);
   g.hruns = (H + g.RBh - 1) / g.RBh;
   auto magic = [](uint32_t d, uint64_t& m, int& sh) {  // exact for x < 2^31
     int l = 0;
