@@ -60,6 +60,10 @@ struct Geo {
   int pairs;  // 0: one column per item
   uint64_t m_pp1p, m_qp;
   int s_pp1p, s_qp;
+  // stride-1 backward over input-column pairs (W even)
+  int pairs2, RBh2, hruns2;
+  uint64_t m_pp2p, m_in2p;
+  int s_pp2p, s_in2p;
 };
 
 __device__ __forceinline__ int fdiv(int x, uint64_t m, int s) {
@@ -353,7 +357,72 @@ __global__ void __launch_bounds__(kThreads, 2) maxpool3_bwd_staged(const float* 
     // phase 2: per input pixel, dy of the windows whose argmax it is, in window
     // raster order
     float* dxc = dx + c * g.G * HW;
-    if (S == 1) {
+    if (S == 1 && g.pairs2) {
+      // two input columns w, w + 1 per item: their candidate windows share
+      // columns q0 + 1, q0 + 2, so four (argmax, dy) loads per window row
+      // serve both pixels; each pixel sums in window raster order as below
+      const int half = g.W / 2;
+      const int per_plane2 = g.hruns2 * half;
+      for (int it = threadIdx.x; it < gh * per_plane2; it += kThreads) {
+        const int gl = fdiv(it, g.m_pp2p, g.s_pp2p), r = it - gl * per_plane2;
+        const int run = fdiv(r, g.m_in2p, g.s_in2p), w = 2 * (r - run * half);
+        const int h0 = run * g.RBh2, h1 = min(g.H, h0 + g.RBh2);
+        const int* ap = as0 + gl * PQ;
+        const float* mp = mk0 + gl * PQ;
+        const float* gp = gs0 + gl * PQ;
+        const float* xs = xs0 + gl * HW;
+        float* dp = dxc + gl * HW + w;
+        const int q0 = w + g.pad - 2;
+        bool v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (unsigned)(q0 + j) < (unsigned)g.Q;
+        int A0[4], A1[4], A2[4];
+        float D0[4], D1[4], D2[4];
+        auto ld_row = [&](int ph, int (&a)[4], float (&d)[4]) {
+          const bool rv = (unsigned)ph < (unsigned)g.P;
+          const int o = ph * g.Q + q0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            a[j] = (rv && v[j]) ? arg_at(ap, mp, o + j) : -1;
+            d[j] = (rv && v[j]) ? gp[o + j] : 0.f;
+          }
+        };
+        int p = h0 + g.pad - 2;
+        ld_row(p, A0, D0);
+        ld_row(p + 1, A1, D1);
+        ld_row(p + 2, A2, D2);
+        int h = h0;
+        auto step = [&](int (&Aa)[4], float (&Da)[4], const int (&Ab)[4], const float (&Db)[4],
+                        const int (&Ac)[4], const float (&Dc)[4]) -> bool {
+          const int me = h * g.W + w;
+          float e0 = 0.f, e1 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) e0 = __fadd_rn(e0, Aa[j] == me ? Da[j] : 0.f);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) e0 = __fadd_rn(e0, Ab[j] == me ? Db[j] : 0.f);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) e0 = __fadd_rn(e0, Ac[j] == me ? Dc[j] : 0.f);
+#pragma unroll
+          for (int j = 1; j < 4; ++j) e1 = __fadd_rn(e1, Aa[j] == me + 1 ? Da[j] : 0.f);
+#pragma unroll
+          for (int j = 1; j < 4; ++j) e1 = __fadd_rn(e1, Ab[j] == me + 1 ? Db[j] : 0.f);
+#pragma unroll
+          for (int j = 1; j < 4; ++j) e1 = __fadd_rn(e1, Ac[j] == me + 1 ? Dc[j] : 0.f);
+          if (MODE == 0 && relu_from_x) {
+            e0 = xs[me] > 0.f ? e0 : 0.f;
+            e1 = xs[me + 1] > 0.f ? e1 : 0.f;
+          }
+          *reinterpret_cast<float2*>(dp + h * g.W) = make_float2(e0, e1);
+          if (++h >= h1) return false;
+          ++p;
+          ld_row(p + 2, Aa, Da);
+          return true;
+        };
+        while (step(A0, D0, A1, D1, A2, D2) && step(A1, D1, A2, D2, A0, D0) &&
+               step(A2, D2, A0, D0, A1, D1)) {
+        }
+      }
+    } else if (S == 1) {
       const int per_plane2 = g.hruns * g.W;
       for (int it = threadIdx.x; it < gh * per_plane2; it += kThreads) {
         const int gl = fdiv(it, g.m_pp2, g.s_pp2), r = it - gl * per_plane2;
@@ -559,6 +628,18 @@ bool plan(Geo& g, int bwd, int N, int C, int H, int W, int P, int Q, int S, int 
   };
   magic((uint32_t)(g.runs * Q), g.m_pp1, g.s_pp1);
   magic((uint32_t)Q, g.m_q, g.s_q);
+  g.pairs2 = 0;
+  static const int pair_rbh = [] {
+    const char* e = getenv("PURINE_B200_POOL_PAIR_RBH");
+    return e && *e ? atoi(e) : 8;
+  }();
+  if (pair_cols && bwd >= 1 && S == 1 && W % 2 == 0) {
+    g.pairs2 = 1;
+    g.RBh2 = run_len(H, W / 2, pair_rbh);
+    g.hruns2 = (H + g.RBh2 - 1) / g.RBh2;
+    magic((uint32_t)(g.hruns2 * (W / 2)), g.m_pp2p, g.s_pp2p);
+    magic((uint32_t)(W / 2), g.m_in2p, g.s_in2p);
+  }
   g.pairs = 0;
   if (pairs) {
     g.pairs = Q / 2;
